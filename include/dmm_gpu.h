@@ -1,0 +1,131 @@
+/* dmm_gpu.h -- C ABI of the B200 (sm_100a) bank-conflict-free DMM kernels.
+ *
+ * This is the drop-in boundary for the reference's hot path:
+ * every entry point replaces one function of /root/reference/proj/include/dmm/*.hpp
+ * (cited per declaration) on a BATCH of independent w x m machines.  Plain pointers
+ * and sizes only; no torch or CUDA types in the signatures (`stream` is a
+ * cudaStream_t passed as void*, NULL = legacy default stream).
+ *
+ * Data layout (global memory, device pointers):
+ *   in / out : count x w x m uint32 words, instance-major, each instance row-major
+ *              (the reference's Instance::grid, instance.hpp:44, narrowed to 32 bits).
+ *              in == out (in place) is allowed.
+ *   stats    : count entries (may be NULL).
+ *   status   : count bytes of dmm_status (may be NULL): the per-instance outcome of a
+ *              data-dependent failure (PostconditionFailed, InvalidInstance,
+ *              KeyOutOfRange).  Where the reference would have thrown, the out
+ *              instance is unspecified.
+ * Shape contracts are checked on the host with the reference's own predicates
+ * before any launch and reported as the return value (ShapeViolation etc.);
+ * DMM_UNSUPPORTED_SHAPE means "the reference accepts it but no kernel is built for
+ * it" -- there is no CPU fallback.  Launches are asynchronous on `stream`.
+ */
+#ifndef DMM_GPU_H
+#define DMM_GPU_H
+
+#include <stdint.h>
+
+#include "dmm_status.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* flags (same values as the oracle's DMMO_FLAG_*) */
+#define DMM_FLAG_EXT_PARTIAL_GROUPS 1u /* accept balance() partial groups with g^2 > m (32x8) */
+#define DMM_FLAG_NONSTRICT 2u          /* MachineConfig.strict = false: no PostconditionFailed */
+#define DMM_FLAG_NO_ENFORCE_PRE 4u     /* integer_sort_general(..., enforce_analysis_pre = false) */
+
+/* GeneralStats partition.hpp:292-295 */
+typedef struct dmm_general_stats {
+    uint32_t cleanup_retries;
+    uint32_t sorted;
+} dmm_general_stats;
+
+/* PermuteReport permute.hpp:62-72 (leftover_history and shifts are separate arrays) */
+#define DMM_PERMUTE_MAX_HIST 64
+typedef struct dmm_permute_report {
+    uint32_t iterations;
+    uint32_t fallback;
+    uint32_t used_packing;
+    uint32_t packed_width;
+    uint64_t threshold;
+    uint64_t random_words;
+    uint32_t cleanup_retries;
+    uint32_t n_hist;
+} dmm_permute_report;
+
+/* ---- library ------------------------------------------------------------- */
+const char* dmm_version(void);
+/* Last CUDA / launch error text of the calling thread ("" if none). */
+const char* dmm_last_error(void);
+/* 1 if a kernel is compiled for (w, m) of the named algorithm (see below). */
+int dmm_supported(const char* algorithm, uint32_t w, uint32_t m);
+/* Number of kernel launches the last call on this thread issued (for bench accounting). */
+uint32_t dmm_last_launch_count(void);
+
+/* ---- instance generation -------------------------------------------------- */
+/* Instance gen_instance(kind, w, m, seed)                        instance.hpp:48-76
+ * Bit-exact on-device restatement for seeds seed0 .. seed0+count-1 into
+ * out[count][w][m].  kind: 0 uint32 sort tile (builder-defined, Rng(splitmix64(seed))()>>32;
+ * the reference's sort kind emits 64-bit words), 1 partition, 2 permute.  w*m <= 4096. */
+dmm_status dmm_gen_instances(int kind, uint32_t w, uint32_t m, uint64_t seed0, uint64_t count, uint32_t* out,
+                             void* stream);
+
+/* ---- partition / integer sort ------------------------------------------ */
+/* GeneralStats partition_general(const MatrixView&)           partition.hpp:453-456
+ * Labels in [0, w), m copies each; after the call row i holds the labels i. */
+dmm_status dmm_partition_general(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                 uint32_t flags, dmm_general_stats* stats, uint8_t* status, void* stream);
+
+/* GeneralStats integer_sort_general(view, domain, probe, enforce)  partition.hpp:436-449 */
+dmm_status dmm_integer_sort_general(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                    uint64_t domain, uint32_t flags, dmm_general_stats* stats, uint8_t* status,
+                                    void* stream);
+
+/* void partition_square(const MatrixView&)                       partition.hpp:189-197 */
+dmm_status dmm_partition_square(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                uint8_t* status, void* stream);
+
+/* void partition_short_wide(const MatrixView&, hook)             partition.hpp:178-185 */
+dmm_status dmm_partition_short_wide(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                    uint8_t* status, void* stream);
+
+/* ---- comparison sorts ------------------------------------------------------ */
+/* void sort_short_wide(view, ascending)  sort.hpp:225 ; void sort_square(view, ascending)  sort.hpp:337 ;
+ * void sort_tall(view)  sort.hpp:352 ; detail::sort_wide_any(view, asc)  sort.hpp:321 */
+dmm_status dmm_sort_short_wide(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                               int ascending, void* stream);
+dmm_status dmm_sort_square(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                           int ascending, void* stream);
+dmm_status dmm_sort_tall(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count, void* stream);
+dmm_status dmm_sort_wide_any(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                             int ascending, void* stream);
+
+/* ---- layout primitives and row sorts ---------------------------------------- */
+/* transpose_square layout.hpp:24 ; to_column_major layout.hpp:397 ; to_row_major layout.hpp:403 */
+dmm_status dmm_transpose_square(const uint32_t* in, uint32_t* out, uint32_t s, uint64_t count, void* stream);
+dmm_status dmm_to_column_major(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                               void* stream);
+dmm_status dmm_to_row_major(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                            void* stream);
+/* radix_sort_rows(view, domain, order) partition.hpp:94 ; sort_rows(view, order) sort.hpp:76
+ * order: 0 ascending, 1 descending, 2 alternating (row 0 ascending), 3 alternating (row 0 descending) */
+dmm_status dmm_sort_rows(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count, int order,
+                         uint64_t domain, uint8_t* status, void* stream);
+
+/* ---- randomized permutation ------------------------------------------------ */
+/* PermuteReport permute(Machine&, Rng&, const PermuteParams&)   permute.hpp:545-628
+ * in: count x w x m labels (a bijection of [0, wm) each); out: the output region
+ * (bank i slot j = i*m + j on success).  seeds[k] seeds instance k's Rng
+ * (std::mt19937_64).  reports: count entries; history: count x DMM_PERMUTE_MAX_HIST;
+ * shifts: count x w (each may be NULL).  workspace: dmm_permute_workspace_bytes(count). */
+uint64_t dmm_permute_workspace_bytes(uint32_t w, uint32_t m, uint64_t count);
+dmm_status dmm_permute(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                       const uint64_t* seeds, uint32_t alpha, uint32_t iter_cap, dmm_permute_report* reports,
+                       uint64_t* history, uint32_t* shifts, uint8_t* status, void* workspace, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DMM_GPU_H */

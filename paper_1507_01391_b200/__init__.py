@@ -1,0 +1,13 @@
+"""paper_1507_01391_b200 -- B200-native (sm_100a) bank-conflict-free partition, sort and
+permutation kernels (Afshani & Sitchinava, arXiv 1507.01391), drop-in for the reference's
+DMM algorithms (/root/reference/proj/include/dmm).  The compute lives in libdmm_b200.so
+(include/dmm_gpu.h); this package is its Python mirror.
+"""
+from .dmm import (  # noqa: F401
+    FLAG_EXT_PARTIAL_GROUPS, FLAG_NO_ENFORCE_PRE, FLAG_NONSTRICT, KIND_PARTITION, KIND_PERMUTE, KIND_SORT_U32,
+    ORDER_ALT, ORDER_ALT_DESC, ORDER_ASC, ORDER_DESC, CapacityExceeded, ConflictViolation, CudaError,
+    DivisibilityViolation, Error, GeneralStats, InvalidInstance, KeyOutOfRange, NotSquare, OutOfBounds,
+    OverlappingViews, PackingOverflow, PermuteReports, PostconditionFailed, ShapeViolation, UnsupportedShape,
+    as_uint32, gen_instances, integer_sort_general, lib, partition_general, partition_short_wide,
+    partition_square, permute, sort_rows, sort_short_wide, sort_square, sort_tall, sort_wide_any, supported,
+    to_column_major, to_row_major, transpose_square, version)

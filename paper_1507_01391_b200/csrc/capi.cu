@@ -1,0 +1,37 @@
+// capi.cu -- library-level C ABI: version, error text, launch accounting, shape table.
+#include <cstring>
+#include <string>
+
+#include "capi_common.h"
+
+namespace dmmhost {
+namespace {
+thread_local std::string g_error;
+thread_local uint32_t g_launches = 0;
+}  // namespace
+void set_error(const std::string& s) { g_error = s; }
+void count_launch(uint32_t n) { g_launches += n; }
+void reset_launches() {
+    g_launches = 0;
+    g_error.clear();
+}
+}  // namespace dmmhost
+
+extern "C" {
+
+const char* dmm_version(void) { return "paper_1507_01391_b200 0.1 (sm_100a)"; }
+const char* dmm_last_error(void) { return dmmhost::g_error.c_str(); }
+uint32_t dmm_last_launch_count(void) { return dmmhost::g_launches; }
+
+int dmm_supported(const char* algorithm, uint32_t w, uint32_t m) {
+    if (!algorithm || w != 32)
+        return 0;
+    const std::string a(algorithm);
+    if (a == "partition_general" || a == "integer_sort_general")
+        return m == 8 || m == 16 || m == 32 || m == 64;
+    if (a == "sort_wide_any")
+        return m == 32 || m == 64;
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,281 @@
+// dmm_algos.cuh -- the reference's sort / partition schedules as warp programs.
+//
+// Each template below restates one function of /root/reference/proj/include/dmm/
+// {sort,partition}.hpp step for step (same row sorts in the same directions, same
+// relayouts, same view decomposition), so the matrix after every step equals the
+// reference's.  Shapes are compile-time: W = 32 (one warp), M = register row width.
+//
+// Outcome-preserving rewrites (the state after the rewritten block is identical):
+//   * shearsort_rect's final "alternating row sort + reversal of the descending rows"
+//     (sort.hpp:299-310) is one row sort in direction asc;
+//   * short_wide_skeleton on a one-row view (W = 1) is one row sort: its conversions
+//     are no-ops (layout.hpp:359) and all five sorts run in direction asc;
+//   * every blocked column sort transposes all its W x W column blocks in one
+//     relayout (the blocks are disjoint; sort.hpp:169-173).
+#pragma once
+
+#include "dmm_device.cuh"
+
+namespace dmmdev {
+
+// ---------------------------------------------------------------------------
+// Shape predicates (compile-time twins of partition.hpp:133-152 / :209-225)
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr bool square_fits_c(int W, int M) { /* sort.hpp:313 */
+    const int h = isqrt_c(M);
+    return h * h == M && W <= M && W % h == 0;
+}
+
+__host__ __device__ constexpr bool general_shape_ok_c(long W, long M, bool ext) {
+    if (W <= 1)
+        return true;
+    if (W <= M) {
+        const long h = isqrt_c((int)M);
+        return W * W <= M || (h * h == M && W % h == 0) || (M % W == 0);
+    }
+    if (M < 2 || W % M != 0)
+        return false;
+    long nsubs = W;
+    while (nsubs > 1) {
+        const long g = M < nsubs ? M : nsubs;
+        if (g < M && g * g > M && (!ext || M % g != 0))
+            return false;
+        if (nsubs % g != 0)
+            return false;
+        nsubs /= g;
+    }
+    return general_shape_ok_c(W / M, M, ext);
+}
+
+struct PParams {
+    int rounds, d, subproblems;
+};
+// PartitionParams::compute for power-of-two W, M: log_m w = lgW / lgM exactly, so
+// ceil(x - 1e-9) is the integer ceiling (the host asserts equality with the
+// double-precision reference formula before every launch).
+__host__ __device__ constexpr PParams pparams_c(int W, int M, bool ext) {
+    const int a = ilog2_ceil_c(W), b = ilog2_ceil_c(M);
+    PParams p{(a + b - 1) / b, 0, 0};
+    int want = (2 * a + b - 1) / b;
+    if (want < 1)
+        want = 1;
+    int d = want < W / M ? want : W / M;
+    while ((long)M * d <= W && (W % (M * d) != 0 || !general_shape_ok_c(W / (M * d), M, ext)))
+        ++d;
+    p.d = d;
+    p.subproblems = M * d;
+    return p;
+}
+
+// ---------------------------------------------------------------------------
+// Column sorts and skeletons  sort.hpp:162-311
+// ---------------------------------------------------------------------------
+// sort_columns_blocked sort.hpp:162-174 (segment sorter: merge_sort_segments)
+template <int PK, class V, int M>
+__device__ __forceinline__ void sort_columns_blocked(uint32_t (&x)[M], uint32_t* buf, int lane, bool asc) {
+    static_assert(V::MV % V::WV == 0, "blocked column sort needs W | M (DivisibilityViolation)");
+    if constexpr (V::WV > 1) {
+        transpose_blocks<V>(x, buf, lane);
+        seg_sort<PK, V, V::WV>(x, lane, asc);
+        transpose_blocks<V>(x, buf, lane);
+    }
+}
+
+// short_wide_skeleton sort.hpp:200-218 (Lemma 1); asc may differ per lane (per view)
+template <int PK, class V, int M>
+__device__ __forceinline__ void short_wide(uint32_t (&x)[M], uint32_t* buf, int lane, bool asc) {
+    static_assert(V::WV * V::WV <= V::MV, "short-wide needs w^2 <= m (ShapeViolation)");
+    if constexpr (V::WV == 1) {
+        row_sort<PK, V>(x, lane, asc);
+    } else {
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+            row_sort<PK, V>(x, lane, alt_dir<V>(lane, asc));
+            to_column_major<V>(x, buf, lane);
+            row_sort<PK, V>(x, lane, asc);
+            to_row_major<V>(x, buf, lane);
+        }
+        row_sort<PK, V>(x, lane, asc);
+    }
+}
+
+// square_skeleton's columns() sort.hpp:266-273
+template <int PK, class V, int M>
+__device__ __forceinline__ void square_columns(uint32_t (&x)[M], uint32_t* buf, int lane, bool asc) {
+    if constexpr (V::WV == V::MV) {  // square_column_sort sort.hpp:240-244
+        transpose_square<V>(x, buf, lane);
+        row_sort<PK, V>(x, lane, asc);
+        transpose_square<V>(x, buf, lane);
+    } else {
+        sort_columns_blocked<PK, V>(x, buf, lane, asc);
+    }
+}
+
+// square_skeleton sort.hpp:250-280 (Theorem 2)
+template <int PK, class V, int M>
+__device__ __forceinline__ void square_skeleton(uint32_t (&x)[M], uint32_t* buf, int lane, bool asc) {
+    constexpr int h = isqrt_c(V::MV);
+    static_assert(h * h == V::MV && V::WV <= V::MV && V::WV % h == 0,
+                  "square skeleton needs perfect-square M and sqrt(M) | W <= M (ShapeViolation)");
+    using G = VRows<V, h>;  // super-rows in merged lockstep
+    short_wide<PK, G>(x, buf, lane, asc);  // super_rows(false)
+    square_columns<PK, V>(x, buf, lane, asc);
+    const int g = V::local(lane) / h;
+    short_wide<PK, G>(x, buf, lane, ((g % 2) == 0) == asc);  // super_rows(true)
+    square_columns<PK, V>(x, buf, lane, asc);
+    row_sort<PK, V>(x, lane, asc);
+}
+
+// shearsort_rect sort.hpp:288-311
+template <int PK, class V, int M>
+__device__ __forceinline__ void shearsort_rect(uint32_t (&x)[M], uint32_t* buf, int lane, bool asc) {
+    static_assert(V::WV <= V::MV && (V::WV == 1 || V::MV % V::WV == 0),
+                  "shearsort fallback needs W <= M and W | M (ShapeViolation)");
+    constexpr int rounds = ilog2_ceil_c(V::WV) + 1;
+#pragma unroll 1
+    for (int i = 0; i < rounds; ++i) {
+        row_sort<PK, V>(x, lane, alt_dir<V>(lane, asc));
+        if constexpr (V::WV > 1)
+            sort_columns_blocked<PK, V>(x, buf, lane, asc);
+    }
+    row_sort<PK, V>(x, lane, asc);  // alternating sort + odd-row reversal, sort.hpp:299-310
+}
+
+// sort_wide_any sort.hpp:321-330 (comparison sorter, W <= M, W | M)
+template <int PK, class V, int M>
+__device__ __forceinline__ void sort_wide_any(uint32_t (&x)[M], uint32_t* buf, int lane, bool asc) {
+    if constexpr (V::WV * V::WV <= V::MV)
+        short_wide<PK, V>(x, buf, lane, asc);
+    else if constexpr (square_fits_c(V::WV, V::MV))
+        square_skeleton<PK, V>(x, buf, lane, asc);
+    else
+        shearsort_rect<PK, V>(x, buf, lane, asc);
+}
+
+// partition_leaf partition.hpp:156-172 (radix rows; the dispatch is the same as
+// sort_wide_any, always ascending)
+template <int PK, class V, int M>
+__device__ __forceinline__ void partition_leaf(uint32_t (&x)[M], uint32_t* buf, int lane) {
+    sort_wide_any<PK, V>(x, buf, lane, true);
+}
+
+// ---------------------------------------------------------------------------
+// Balancing, convert-and-divide, recursion  partition.hpp:234-428
+// ---------------------------------------------------------------------------
+// balance partition.hpp:234-271.  Round with sub-matrix height SUB_H and NSUBS
+// sub-matrices; the assembled views pick row j of each sub-matrix of a group.
+template <int PK, class V, bool EXT, int SUB_H, int NSUBS, int M>
+__device__ __forceinline__ void balance_rounds(uint32_t (&x)[M], uint32_t* buf, int lane) {
+    if constexpr (NSUBS > 1) {
+        constexpr int g = V::MV < NSUBS ? V::MV : NSUBS;
+        static_assert(!(g < V::MV && g * g > V::MV) || (EXT && V::MV % g == 0),
+                      "balance leftover group fits neither the square nor short-wide case (ShapeViolation)");
+        static_assert(NSUBS % g == 0, "balance needs g | nsubs");
+        using A = VF<V::MASK, V::LO, V::ST * SUB_H, g, V::C0, V::MV>;
+        if constexpr (g == V::MV) {
+            partition_leaf<PK, A>(x, buf, lane);
+            transpose_square<A>(x, buf, lane);
+        } else if constexpr (g * g <= V::MV) {
+            short_wide<PK, A>(x, buf, lane, true);
+            to_column_major<A>(x, buf, lane);
+        } else {
+            // B200 extension (documented in DESIGN.md): a partial group with g^2 > m
+            // is sorted by the leaf dispatcher (shearsort), then laid out column-major.
+            partition_leaf<PK, A>(x, buf, lane);
+            to_column_major<A>(x, buf, lane);
+        }
+        balance_rounds<PK, V, EXT, SUB_H * g, NSUBS / g>(x, buf, lane);
+    }
+}
+
+// balance + convert_and_divide (partition.hpp:275-286) until subproblems have <= m
+// rows, then the leaves (balance_divide_sort steps (1) and (2), :373-396)
+template <int PK, class V, bool EXT, int M>
+__device__ __forceinline__ void levels(uint32_t (&x)[M], uint32_t* buf, int lane) {
+    if constexpr (V::WV > V::MV) {
+        static_assert(V::WV % V::MV == 0, "general partition needs m | w (ShapeViolation)");
+        balance_rounds<PK, V, EXT, 1, V::WV>(x, buf, lane);
+        constexpr PParams p = pparams_c(V::WV, V::MV, EXT);
+        static_assert(V::WV % p.subproblems == 0, "m*d must divide W (DivisibilityViolation)");
+        to_row_major<V>(x, buf, lane);
+        levels<PK, VRows<V, V::WV / p.subproblems>, EXT>(x, buf, lane);
+    } else {
+        partition_leaf<PK, V>(x, buf, lane);
+    }
+}
+
+// scan_sorted partition.hpp:308-337 on the full warp view: bit h set = half h sorted.
+// The reference's tree_reduce_sum + broadcast of the verdict is one warp reduction.
+template <int PK, class V, int M>
+__device__ __forceinline__ uint32_t scan_sorted(const uint32_t (&x)[M], int lane) {
+    static_assert(V::MASK == 0xFFFFFFFFu && V::ST == 1 && V::WV == kWarp, "scan_sorted on the full warp view");
+    uint32_t bad = 0;
+#pragma unroll
+    for (int c = V::C0 + 1; c < V::C0 + V::MV; ++c)
+        bad |= Key<PK>::gt(x[c - 1], x[c]);
+    const uint32_t next_first = __shfl_down_sync(0xFFFFFFFFu, x[V::C0], 1);
+    if (lane + 1 < kWarp)
+        bad |= Key<PK>::gt(x[V::C0 + V::MV - 1], next_first);
+    bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+    return Key<PK>::kAll & ~bad;
+}
+
+// cleanup_pass_pair partition.hpp:341-361 on the full warp view
+template <int PK, class V, int M>
+__device__ __forceinline__ void cleanup_pass_pair(uint32_t (&x)[M], uint32_t* buf, int lane) {
+    static_assert(V::MASK == 0xFFFFFFFFu && V::ST == 1 && V::WV == kWarp, "cleanup on the full warp view");
+    partition_leaf<PK, VRows<V, V::MV>>(x, buf, lane);  // aligned m x m blocks
+    if constexpr (V::WV > V::MV && V::MV >= 2) {
+        constexpr int H = V::MV / 2;
+        using Edge = VF<lane_range_mask(0, H) | lane_range_mask(kWarp - H, kWarp), 0, 1, H, V::C0, V::MV>;
+        using Mid = VF<lane_range_mask(H, kWarp - H), H, 1, V::MV, V::C0, V::MV>;
+        partition_leaf<PK, Edge>(x, buf, lane);  // the two m/2-row end blocks
+        partition_leaf<PK, Mid>(x, buf, lane);   // the m/2-shifted m-row blocks
+    }
+}
+
+// Per-instance result of a general sort (one entry per packed half).
+struct GenResult {
+    uint32_t retries[2];  // cleanup_retries (GeneralStats partition.hpp:292-295)
+    uint32_t unsorted;    // bit h: cleanup budget exhausted for half h
+};
+
+// balance_divide_sort partition.hpp:363-428
+template <int PK, class V, bool EXT, int M>
+__device__ __forceinline__ void balance_divide_sort(uint32_t (&x)[M], uint32_t* buf, int lane, GenResult& res) {
+    if constexpr (V::WV <= V::MV) {
+        partition_leaf<PK, V>(x, buf, lane);
+    } else {
+        levels<PK, V, EXT>(x, buf, lane);
+        // (3) column recursion: each column into a (W/m) x m submatrix
+        to_row_major<V>(x, buf, lane);
+        balance_divide_sort<PK, VRows<V, V::WV / V::MV>, EXT>(x, buf, lane, res);
+        to_column_major<V>(x, buf, lane);
+        // (4) shifted square cleanup with a checked postcondition
+        constexpr int budget = ilog2_ceil_c(V::WV);
+        uint32_t done = 0;
+        int passes = 0;
+#pragma unroll 1
+        for (;;) {
+            cleanup_pass_pair<PK, V>(x, buf, lane);
+            const uint32_t ok = scan_sorted<PK, V>(x, lane);
+            const uint32_t fresh = ok & ~done;
+            if (fresh & 1u)
+                res.retries[0] = max(res.retries[0], (uint32_t)passes);
+            if (fresh & 2u)
+                res.retries[1] = max(res.retries[1], (uint32_t)passes);
+            done |= ok;
+            if (done == Key<PK>::kAll || passes == budget)
+                break;
+            ++passes;
+        }
+        const uint32_t failed = Key<PK>::kAll & ~done;
+        if (failed & 1u)
+            res.retries[0] = max(res.retries[0], (uint32_t)budget);
+        if (failed & 2u)
+            res.retries[1] = max(res.retries[1], (uint32_t)budget);
+        res.unsorted |= failed;
+    }
+}
+
+}  // namespace dmmdev

@@ -1,0 +1,191 @@
+// general_kernel.cuh -- the batched general-sort kernel template (kernels 1-3) and
+// its launcher; instantiated per row width M in general_m*.cu (parallel builds).
+#pragma once
+
+#include "capi_common.h"
+#include "dmm_algos.cuh"
+
+namespace dmmdev {
+
+template <int M>
+__device__ __forceinline__ void load_row(const uint32_t* __restrict__ p, uint32_t (&v)[M]) {
+    if constexpr (M % 4 == 0) {
+        const uint4* q = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+        for (int i = 0; i < M / 4; ++i) {
+            const uint4 t = __ldg(q + i);
+            v[4 * i] = t.x;
+            v[4 * i + 1] = t.y;
+            v[4 * i + 2] = t.z;
+            v[4 * i + 3] = t.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+            v[i] = __ldg(p + i);
+    }
+}
+
+template <int M>
+__device__ __forceinline__ void store_row(uint32_t* __restrict__ p, const uint32_t (&v)[M]) {
+    if constexpr (M % 4 == 0) {
+        uint4* q = reinterpret_cast<uint4*>(p);
+#pragma unroll
+        for (int i = 0; i < M / 4; ++i)
+            q[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+            p[i] = v[i];
+    }
+}
+
+enum : int { kModeIntegerSort = 0, kModePartition = 1, kModeSortAny = 2 };
+
+// One warp per PK instances.  Row r of instance k is at in[(k*32 + r)*M].
+template <int M, int PK, bool EXT, int MODE>
+__global__ void __launch_bounds__(256) k_general_sort(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                      uint64_t count, uint64_t domain, int strict, int ascending,
+                                                      dmm_general_stats* __restrict__ stats,
+                                                      uint8_t* __restrict__ status) {
+    extern __shared__ uint32_t smem[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    uint32_t* buf = smem + warp * relayout_buf_words(M);
+    const uint64_t inst0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * PK;
+    if (inst0 >= count)
+        return;
+    const bool hasB = PK == 2 && inst0 + 1 < count;
+
+    uint32_t x[M];
+    uint32_t bad = 0;  // bit h: half h holds a key outside [0, domain)
+    {
+        uint32_t a[M];
+        load_row<M>(in + (inst0 * kWarp + lane) * M, a);
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+            bad |= (uint64_t)a[c] >= domain ? 1u : 0u;
+        if constexpr (PK == 2) {
+            uint32_t b[M];
+            if (hasB) {
+                load_row<M>(in + ((inst0 + 1) * kWarp + lane) * M, b);
+            } else {
+#pragma unroll
+                for (int c = 0; c < M; ++c)
+                    b[c] = 0;
+            }
+#pragma unroll
+            for (int c = 0; c < M; ++c) {
+                bad |= (uint64_t)b[c] >= domain ? 2u : 0u;
+                x[c] = (a[c] & 0xFFFFu) | (b[c] << 16);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < M; ++c)
+                x[c] = a[c];
+        }
+    }
+    bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+
+    using V = VF<0xFFFFFFFFu, 0, 1, kWarp, 0, M>;
+    GenResult res{{0u, 0u}, 0u};
+    if constexpr (MODE == kModeSortAny)
+        sort_wide_any<PK, V>(x, buf, lane, ascending != 0);
+    else
+        balance_divide_sort<PK, V, EXT>(x, buf, lane, res);
+
+    uint32_t invalid = 0;
+    if constexpr (MODE == kModePartition) {
+        // check_partition_instance (partition.hpp:112-124): labels in [0, w), m copies
+        // each  <=>  (labels < w) and the sorted result has row i = i everywhere.
+        uint32_t mism = 0;
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+            if constexpr (PK == 2) {
+                mism |= (x[c] & 0xFFFFu) != (uint32_t)lane ? 1u : 0u;
+                mism |= (x[c] >> 16) != (uint32_t)lane ? 2u : 0u;
+            } else {
+                mism |= x[c] != (uint32_t)lane ? 1u : 0u;
+            }
+        }
+        invalid = __reduce_or_sync(0xFFFFFFFFu, mism) | bad;
+    }
+
+#pragma unroll
+    for (int h = 0; h < PK; ++h) {
+        if (h == 1 && !hasB)
+            break;
+        const uint64_t k = inst0 + h;
+        uint32_t v[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+            v[c] = PK == 2 ? ((x[c] >> (16 * h)) & 0xFFFFu) : x[c];
+        store_row<M>(out + (k * kWarp + lane) * M, v);
+        if (lane == 0) {
+            const bool unsorted = (res.unsorted >> h) & 1u;
+            uint8_t s = DMM_OK;
+            if (MODE == kModePartition && ((invalid >> h) & 1u))
+                s = DMM_INVALID_INSTANCE;
+            else if ((bad >> h) & 1u)
+                s = DMM_KEY_OUT_OF_RANGE;
+            else if (unsorted && strict)
+                s = DMM_POSTCONDITION_FAILED;
+            if (status)
+                status[k] = s;
+            if (stats) {
+                stats[k].cleanup_retries = res.retries[h];
+                stats[k].sorted = unsorted ? 0u : 1u;
+            }
+        }
+    }
+}
+
+}  // namespace dmmdev
+
+
+namespace dmmhost {
+
+struct GeneralArgs {
+    const uint32_t* in;
+    uint32_t* out;
+    uint64_t count;
+    uint64_t domain;
+    int strict;
+    int ascending;
+    dmm_general_stats* stats;
+    uint8_t* status;
+    cudaStream_t stream;
+};
+
+constexpr int kWarpsPerBlock = 8;
+
+template <int M, int PK, bool EXT, int MODE>
+dmm_status launch_general(const GeneralArgs& a) {
+    auto kern = dmmdev::k_general_sort<M, PK, EXT, MODE>;
+    const size_t smem = size_t(kWarpsPerBlock) * dmmdev::relayout_buf_words(M) * sizeof(uint32_t);
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        if (smem > 48 * 1024 &&
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+            return check_launch("cudaFuncSetAttribute");
+        configured = true;
+    }
+    const uint64_t units = (a.count + PK - 1) / PK;
+    const uint64_t blocks = (units + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    if (blocks == 0)
+        return DMM_OK;
+    if (blocks > 0x7FFFFFFFull)
+        return DMM_INVALID_ARGUMENT;
+    kern<<<dim3(unsigned(blocks)), dim3(kWarpsPerBlock * 32), smem, a.stream>>>(a.in, a.out, a.count, a.domain, a.strict,
+                                                                                a.ascending, a.stats, a.status);
+    return check_launch("k_general_sort");
+}
+
+
+// per-width entry points (general_m*.cu)
+dmm_status launch_general_m8(int mode, bool pk2, bool ext, const GeneralArgs& a);
+dmm_status launch_general_m16(int mode, bool pk2, bool ext, const GeneralArgs& a);
+dmm_status launch_general_m32(int mode, bool pk2, bool ext, const GeneralArgs& a);
+dmm_status launch_general_m64(int mode, bool pk2, bool ext, const GeneralArgs& a);
+
+}  // namespace dmmhost

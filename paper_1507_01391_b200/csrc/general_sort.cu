@@ -1,0 +1,137 @@
+// general_sort.cu -- C ABI of kernels 1-3: w-way partition (n >= w^2), general
+// partition (Lemma 4) and integer sort over a batch of 32 x m machines.
+//
+// C ABI: dmm_partition_general (partition.hpp:453), dmm_integer_sort_general
+// (partition.hpp:436), dmm_sort_wide_any (sort.hpp:321), dmm_partition_square
+// (partition.hpp:189), dmm_partition_short_wide (partition.hpp:178).  The kernel
+// template is general_kernel.cuh; one translation unit per row width m.
+#include "general_kernel.cuh"
+
+namespace {
+
+using namespace dmmhost;
+
+// Dispatch over the compiled shapes (W = 32).  PK = 2 whenever every legal key
+// fits in 16 bits (domain <= 2^16).
+dmm_status dispatch(int mode, const uint32_t* in, uint32_t* out, uint32_t m, uint64_t count, uint64_t domain,
+                    bool ext, int strict, int ascending, dmm_general_stats* stats, uint8_t* status, cudaStream_t s) {
+    const bool pk2 = domain <= 65536;
+    const GeneralArgs a{in, out, count, domain, strict, ascending, stats, status, s};
+    switch (m) {
+        case 8: return launch_general_m8(mode, pk2, ext, a);
+        case 16: return launch_general_m16(mode, pk2, ext, a);
+        case 32: return launch_general_m32(mode, pk2, ext, a);
+        case 64: return launch_general_m64(mode, pk2, ext, a);
+        default: break;
+    }
+    set_error("no kernel compiled for this shape");
+    return DMM_UNSUPPORTED_SHAPE;
+}
+
+dmm_status check_ptrs(const void* in, const void* out, uint64_t count) {
+    if (count == 0)
+        return DMM_OK;
+    if (!in || !out)
+        return DMM_INVALID_ARGUMENT;
+    if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u) {
+        set_error("in/out must be 16-byte aligned");
+        return DMM_INVALID_ARGUMENT;
+    }
+    return DMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+dmm_status dmm_integer_sort_general(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                    uint64_t domain, uint32_t flags, dmm_general_stats* stats, uint8_t* status,
+                                    void* stream) {
+    reset_launches();
+    const bool ext = flags & DMM_FLAG_EXT_PARTIAL_GROUPS;
+    const dmm_status sh = integer_sort_shape_status(w, m, !(flags & DMM_FLAG_NO_ENFORCE_PRE), ext);
+    if (sh != DMM_OK)
+        return sh;
+    if (dmm_status e = check_ptrs(in, out, count); e != DMM_OK || count == 0)
+        return e;
+    if (w != 32) {
+        set_error("kernels are built for w = 32 (one warp per machine)");
+        return DMM_UNSUPPORTED_SHAPE;
+    }
+    if (domain == 0 || domain > (1ull << 32)) {
+        // keys are 32-bit words; a wider domain admits every key
+        domain = 1ull << 32;
+    }
+    // use the extension kernels only where the reference itself would reject the shape
+    const bool need_ext = ext && !general_sort_shape_ok(w, m, false) && m < w;
+    return dispatch(dmmdev::kModeIntegerSort, in, out, m, count, domain, need_ext, !(flags & DMM_FLAG_NONSTRICT), 1,
+                                              stats, status, static_cast<cudaStream_t>(stream));
+}
+
+dmm_status dmm_partition_general(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                 uint32_t flags, dmm_general_stats* stats, uint8_t* status, void* stream) {
+    reset_launches();
+    const bool ext = flags & DMM_FLAG_EXT_PARTIAL_GROUPS;
+    const dmm_status sh = integer_sort_shape_status(w, m, !(flags & DMM_FLAG_NO_ENFORCE_PRE), ext);
+    if (sh != DMM_OK)
+        return sh;
+    if (dmm_status e = check_ptrs(in, out, count); e != DMM_OK || count == 0)
+        return e;
+    if (w != 32) {
+        set_error("kernels are built for w = 32 (one warp per machine)");
+        return DMM_UNSUPPORTED_SHAPE;
+    }
+    const bool need_ext = ext && !general_sort_shape_ok(w, m, false) && m < w;
+    return dispatch(dmmdev::kModePartition, in, out, m, count, w, need_ext, !(flags & DMM_FLAG_NONSTRICT), 1, stats,
+                                            status, static_cast<cudaStream_t>(stream));
+}
+
+dmm_status dmm_sort_wide_any(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                             int ascending, void* stream) {
+    reset_launches();
+    if (w > m || (w > 1 && m % w != 0))
+        return DMM_SHAPE_VIOLATION;
+    if (dmm_status e = check_ptrs(in, out, count); e != DMM_OK || count == 0)
+        return e;
+    if (w != 32) {
+        set_error("kernels are built for w = 32 (one warp per machine)");
+        return DMM_UNSUPPORTED_SHAPE;
+    }
+    return dispatch(dmmdev::kModeSortAny, in, out, m, count, 1ull << 32, false, 1, ascending, nullptr, nullptr,
+                                          static_cast<cudaStream_t>(stream));
+}
+
+dmm_status dmm_partition_square(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                uint8_t* status, void* stream) {
+    reset_launches();
+    // partition.hpp:189-197
+    if (w != m)
+        return DMM_SHAPE_VIOLATION;
+    const uint32_t h = isqrt_floor(m);
+    if (h * h != m)
+        return DMM_SHAPE_VIOLATION;
+    (void)in;
+    (void)out;
+    (void)count;
+    (void)status;
+    (void)stream;
+    set_error("partition_square: no perfect-square w = m is a single warp (w = 32)");
+    return DMM_UNSUPPORTED_SHAPE;
+}
+
+dmm_status dmm_partition_short_wide(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                    uint8_t* status, void* stream) {
+    reset_launches();
+    // partition.hpp:178-185
+    if (uint64_t(w) * w > m)
+        return DMM_SHAPE_VIOLATION;
+    (void)in;
+    (void)out;
+    (void)count;
+    (void)status;
+    (void)stream;
+    set_error("partition_short_wide: w = 32 needs m >= 1024 words per register row");
+    return DMM_UNSUPPORTED_SHAPE;
+}
+
+}  // extern "C"

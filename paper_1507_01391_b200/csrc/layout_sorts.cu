@@ -1,0 +1,230 @@
+// layout_sorts.cu -- batched layout primitives, row sorts and the tall / square /
+// short-wide comparison sorts over 32 x m machines (one warp per machine).
+//
+// C ABI: dmm_transpose_square (layout.hpp:24), dmm_to_column_major (layout.hpp:397),
+// dmm_to_row_major (layout.hpp:403), dmm_sort_rows (partition.hpp:94 / sort.hpp:76),
+// dmm_sort_tall (sort.hpp:352), dmm_sort_square (sort.hpp:337),
+// dmm_sort_short_wide (sort.hpp:225).
+#include "general_kernel.cuh"
+
+namespace dmmdev {
+
+// sort_columns_network sort.hpp:115-156: every column sorted ascending across the
+// rows.  The reference drives a Batcher comparator network between row pairs; on
+// the warp the network runs across lanes with shuffles (no shared memory, so no
+// bank to conflict on).  Outcome: the unique ascending column.
+template <int PK, int M>
+__device__ __forceinline__ void sort_columns_network(uint32_t (&x)[M], int lane) {
+#pragma unroll
+    for (int k = 2; k <= kWarp; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j >= 1; j >>= 1) {
+            const bool up = (lane & k) == 0 || k == kWarp;
+            const bool lower = (lane & j) == 0;
+            const bool keep_min = lower == up;
+#pragma unroll
+            for (int c = 0; c < M; ++c) {
+                const uint32_t p = __shfl_xor_sync(0xFFFFFFFFu, x[c], j);
+                uint32_t lo = x[c], hi = p;
+                Key<PK>::cx(lo, hi);
+                x[c] = keep_min ? lo : hi;
+            }
+        }
+    }
+}
+
+enum : int { kOpTranspose = 0, kOpToCol = 1, kOpToRow = 2, kOpSortRows = 3, kOpSortTall = 4 };
+
+template <int M, int OP>
+__global__ void __launch_bounds__(256) k_layout(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                uint64_t count, int order, uint64_t domain,
+                                                uint8_t* __restrict__ status) {
+    extern __shared__ uint32_t smem[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    uint32_t* buf = smem + warp * relayout_buf_words(M);
+    const uint64_t k = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (k >= count)
+        return;
+    uint32_t x[M];
+    load_row<M>(in + (k * kWarp + lane) * M, x);
+    using V = VF<0xFFFFFFFFu, 0, 1, kWarp, 0, M>;
+    if constexpr (OP == kOpTranspose) {
+        transpose_square<V>(x, buf, lane);
+    } else if constexpr (OP == kOpToCol) {
+        to_column_major<V>(x, buf, lane);
+    } else if constexpr (OP == kOpToRow) {
+        to_row_major<V>(x, buf, lane);
+    } else if constexpr (OP == kOpSortRows) {
+        uint32_t bad = 0;
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+            bad |= (uint64_t)x[c] >= domain ? 1u : 0u;
+        bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+        const bool asc = order == 0 ? true : order == 1 ? false : (((lane % 2) == 0) == (order == 2));
+        row_sort<1, V>(x, lane, asc);
+        if (status && lane == 0)
+            status[k] = (bad && M > 1) ? DMM_KEY_OUT_OF_RANGE : DMM_OK;
+    } else if constexpr (OP == kOpSortTall) {
+        // sort_tall sort.hpp:352-374 (w >= m, m | w)
+        if constexpr (M == kWarp) {
+            sort_wide_any<1, V>(x, buf, lane, true);
+        } else {
+            row_sort<1, V>(x, lane, true);
+            sort_columns_network<1>(x, lane);
+            to_row_major<V>(x, buf, lane);
+            sort_columns_network<1>(x, lane);
+            using B = VRows<V, M>;  // m x m blocks, alternating direction per block
+            sort_wide_any<1, B>(x, buf, lane, ((lane / M) % 2) == 0);
+            sort_columns_network<1>(x, lane);
+            row_sort<1, V>(x, lane, true);
+        }
+    }
+    store_row<M>(out + (k * kWarp + lane) * M, x);
+}
+
+}  // namespace dmmdev
+
+namespace {
+
+using namespace dmmhost;
+
+template <int M, int OP>
+dmm_status launch_layout(const uint32_t* in, uint32_t* out, uint64_t count, int order, uint64_t domain,
+                         uint8_t* status, void* stream) {
+    constexpr int kWarps = 8;
+    auto kern = dmmdev::k_layout<M, OP>;
+    const size_t smem = size_t(kWarps) * dmmdev::relayout_buf_words(M) * sizeof(uint32_t);
+    static bool configured = false;
+    if (!configured) {
+        if (smem > 48 * 1024 &&
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+            return check_launch("cudaFuncSetAttribute");
+        configured = true;
+    }
+    if (count == 0)
+        return DMM_OK;
+    const uint64_t blocks = (count + kWarps - 1) / kWarps;
+    kern<<<unsigned(blocks), kWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(in, out, count, order, domain,
+                                                                                     status);
+    return check_launch("k_layout");
+}
+
+template <int OP>
+dmm_status dispatch_layout(uint32_t m, const uint32_t* in, uint32_t* out, uint64_t count, int order,
+                           uint64_t domain, uint8_t* status, void* stream) {
+    if constexpr (OP == dmmdev::kOpTranspose) {
+        if (m == 32)
+            return launch_layout<32, OP>(in, out, count, order, domain, status, stream);
+    } else if constexpr (OP == dmmdev::kOpSortTall) {
+        switch (m) {
+            case 1: return launch_layout<1, OP>(in, out, count, order, domain, status, stream);
+            case 2: return launch_layout<2, OP>(in, out, count, order, domain, status, stream);
+            case 4: return launch_layout<4, OP>(in, out, count, order, domain, status, stream);
+            case 8: return launch_layout<8, OP>(in, out, count, order, domain, status, stream);
+            case 16: return launch_layout<16, OP>(in, out, count, order, domain, status, stream);
+            case 32: return launch_layout<32, OP>(in, out, count, order, domain, status, stream);
+            default: break;
+        }
+    } else {
+        switch (m) {
+            case 1: return launch_layout<1, OP>(in, out, count, order, domain, status, stream);
+            case 2: return launch_layout<2, OP>(in, out, count, order, domain, status, stream);
+            case 4: return launch_layout<4, OP>(in, out, count, order, domain, status, stream);
+            case 8: return launch_layout<8, OP>(in, out, count, order, domain, status, stream);
+            case 16: return launch_layout<16, OP>(in, out, count, order, domain, status, stream);
+            case 32: return launch_layout<32, OP>(in, out, count, order, domain, status, stream);
+            case 64: return launch_layout<64, OP>(in, out, count, order, domain, status, stream);
+            default: break;
+        }
+    }
+    set_error("no kernel compiled for this shape");
+    return DMM_UNSUPPORTED_SHAPE;
+}
+
+dmm_status common_checks(const void* in, const void* out, uint32_t w, uint64_t count) {
+    if (count && (!in || !out))
+        return DMM_INVALID_ARGUMENT;
+    if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u) {
+        set_error("in/out must be 16-byte aligned");
+        return DMM_INVALID_ARGUMENT;
+    }
+    if (w != 32) {
+        set_error("kernels are built for w = 32 (one warp per machine)");
+        return DMM_UNSUPPORTED_SHAPE;
+    }
+    return DMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+dmm_status dmm_transpose_square(const uint32_t* in, uint32_t* out, uint32_t s, uint64_t count, void* stream) {
+    reset_launches();
+    if (dmm_status e = common_checks(in, out, s, count); e != DMM_OK)
+        return e;
+    return dispatch_layout<dmmdev::kOpTranspose>(s, in, out, count, 0, 0, nullptr, stream);
+}
+
+dmm_status dmm_to_column_major(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                               void* stream) {
+    reset_launches();
+    if (dmm_status e = common_checks(in, out, w, count); e != DMM_OK)
+        return e;
+    return dispatch_layout<dmmdev::kOpToCol>(m, in, out, count, 0, 0, nullptr, stream);
+}
+
+dmm_status dmm_to_row_major(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                            void* stream) {
+    reset_launches();
+    if (dmm_status e = common_checks(in, out, w, count); e != DMM_OK)
+        return e;
+    return dispatch_layout<dmmdev::kOpToRow>(m, in, out, count, 0, 0, nullptr, stream);
+}
+
+dmm_status dmm_sort_rows(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count, int order,
+                         uint64_t domain, uint8_t* status, void* stream) {
+    reset_launches();
+    if (order < 0 || order > 3)
+        return DMM_INVALID_ARGUMENT;
+    if (dmm_status e = common_checks(in, out, w, count); e != DMM_OK)
+        return e;
+    if (domain == 0 || domain > (1ull << 32))
+        domain = 1ull << 32;
+    return dispatch_layout<dmmdev::kOpSortRows>(m, in, out, count, order, domain, status, stream);
+}
+
+dmm_status dmm_sort_tall(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count, void* stream) {
+    reset_launches();
+    if (w < m || (m > 0 && w % m != 0))  // sort.hpp:354-355
+        return DMM_SHAPE_VIOLATION;
+    if (dmm_status e = common_checks(in, out, w, count); e != DMM_OK)
+        return e;
+    return dispatch_layout<dmmdev::kOpSortTall>(m, in, out, count, 0, 0, nullptr, stream);
+}
+
+dmm_status dmm_sort_square(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                           int ascending, void* stream) {
+    reset_launches();
+    (void)in, (void)out, (void)count, (void)ascending, (void)stream;
+    if (w != m)  // sort.hpp:338-342
+        return DMM_SHAPE_VIOLATION;
+    const uint32_t h = isqrt_floor(m);
+    if (h * h != m)
+        return DMM_SHAPE_VIOLATION;
+    set_error("sort_square: no perfect-square w = m equals one warp (w = 32)");
+    return DMM_UNSUPPORTED_SHAPE;
+}
+
+dmm_status dmm_sort_short_wide(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                               int ascending, void* stream) {
+    reset_launches();
+    (void)in, (void)out, (void)count, (void)ascending, (void)stream;
+    if (uint64_t(w) * w > m)  // sort.hpp:203-204
+        return DMM_SHAPE_VIOLATION;
+    set_error("sort_short_wide: w = 32 needs m >= 1024 words per register row");
+    return DMM_UNSUPPORTED_SHAPE;
+}
+
+}  // extern "C"

@@ -1,0 +1,382 @@
+"""Python mirror of the reference's hot-path API over the B200 C ABI.
+
+Names and argument meaning follow /root/reference/proj/include/dmm/*.hpp
+(partition_general, integer_sort_general, sort_tall, permute, to_column_major, ...);
+the error behaviour mirrors the reference's exception hierarchy (core.hpp:59-78):
+shape contracts raise before launch, data-dependent failures (PostconditionFailed,
+InvalidInstance, KeyOutOfRange) raise after the batch completes, naming the
+first failing instance.
+
+Inputs are batches ``[count, w, m]`` (or a single ``[w, m]`` grid) of uint32 words
+held as ``torch.int32`` on the GPU (numpy arrays are copied over).  Device memory
+and streams come from PyTorch; every computation runs in libdmm_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+_LIB: C.CDLL | None = None
+
+
+def lib() -> C.CDLL:
+    global _LIB
+    if _LIB is None:
+        _LIB = _lib.load()
+    return _LIB
+
+
+# --------------------------------------------------------------------------------------
+# Errors (core.hpp:59-78)
+# --------------------------------------------------------------------------------------
+class Error(RuntimeError):
+    status = 11
+
+
+class ConflictViolation(Error):
+    status = -1
+
+
+class OverlappingViews(ConflictViolation):
+    status = 10
+
+
+class ShapeViolation(Error):
+    status = 1
+
+
+class InvalidInstance(Error):
+    status = 2
+
+
+class KeyOutOfRange(Error):
+    status = 3
+
+
+class DivisibilityViolation(Error):
+    status = 4
+
+
+class PostconditionFailed(Error):
+    status = 5
+
+
+class PackingOverflow(Error):
+    status = 6
+
+
+class CapacityExceeded(Error):
+    status = 7
+
+
+class NotSquare(Error):
+    status = 8
+
+
+class OutOfBounds(Error):
+    status = 9
+
+
+class UnsupportedShape(Error):
+    """The reference accepts the shape but no B200 kernel is built for it (no fallback)."""
+    status = 64
+
+
+class CudaError(Error):
+    status = 66
+
+
+_BY_STATUS = {c.status: c for c in (ShapeViolation, InvalidInstance, KeyOutOfRange, DivisibilityViolation,
+                                     PostconditionFailed, PackingOverflow, CapacityExceeded, NotSquare,
+                                     OutOfBounds, OverlappingViews, UnsupportedShape, CudaError)}
+_BY_STATUS[11] = Error
+_BY_STATUS[65] = ValueError
+
+FLAG_EXT_PARTIAL_GROUPS = 1
+FLAG_NONSTRICT = 2
+FLAG_NO_ENFORCE_PRE = 4
+
+
+def _check(status: int, where: str) -> None:
+    if status != 0:
+        cls = _BY_STATUS.get(status, Error)
+        msg = lib().dmm_last_error().decode()
+        raise cls(f"{where}: status {status}" + (f" ({msg})" if msg else ""))
+
+
+# --------------------------------------------------------------------------------------
+# Tensor plumbing
+# --------------------------------------------------------------------------------------
+def _as_batch(grid) -> tuple[torch.Tensor, bool]:
+    """-> (contiguous int32 CUDA tensor [count, w, m], was_single_grid)."""
+    if isinstance(grid, np.ndarray):
+        a = np.ascontiguousarray(grid)
+        if a.dtype != np.uint32:
+            if a.size and (a.min() < 0 or a.max() >= 2 ** 32):
+                raise KeyOutOfRange("words must fit in 32 bits (the B200 layout narrows the reference's u64 words)")
+            a = a.astype(np.uint32)
+        t = torch.from_numpy(a.view(np.int32)).cuda()
+    elif isinstance(grid, torch.Tensor):
+        t = grid
+        if t.dtype in (torch.int64, torch.uint32):
+            t = t.to(torch.int64)
+            if t.numel() and (int(t.min()) < 0 or int(t.max()) >= 2 ** 32):
+                raise KeyOutOfRange("words must fit in 32 bits")
+            t = (t & 0xFFFFFFFF).to(torch.int64)
+            t = torch.where(t >= 2 ** 31, t - 2 ** 32, t).to(torch.int32)
+        elif t.dtype != torch.int32:
+            raise TypeError(f"unsupported dtype {t.dtype}")
+        if not t.is_cuda:
+            t = t.cuda()
+        t = t.contiguous()
+    else:
+        raise TypeError("grid must be a numpy array or a torch tensor")
+    single = t.dim() == 2
+    if single:
+        t = t.unsqueeze(0)
+    if t.dim() != 3:
+        raise ShapeViolation("grid must be [w, m] or [count, w, m]")
+    return t, single
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def as_uint32(t: torch.Tensor) -> np.ndarray:
+    """Device int32 tensor -> host numpy uint32 (bit reinterpretation)."""
+    return t.detach().cpu().numpy().view(np.uint32)
+
+
+def _raise_first(status: torch.Tensor, where: str) -> None:
+    bad = torch.nonzero(status != 0)
+    if bad.numel():
+        k = int(bad[0, 0])
+        s = int(status[k])
+        cls = _BY_STATUS.get(s, Error)
+        raise cls(f"{where}: instance {k} failed with status {s}")
+
+
+@dataclass
+class GeneralStats:
+    """GeneralStats partition.hpp:292-295, per instance."""
+    cleanup_retries: torch.Tensor  # int32 [count]
+    sorted: torch.Tensor           # bool  [count]
+    status: torch.Tensor           # uint8 [count] (dmm_status)
+
+
+# --------------------------------------------------------------------------------------
+# Instance generation (instance.hpp:48-76)
+# --------------------------------------------------------------------------------------
+KIND_SORT_U32, KIND_PARTITION, KIND_PERMUTE = 0, 1, 2
+
+
+def gen_instances(kind: int, w: int, m: int, seed0: int, count: int, stream=None) -> torch.Tensor:
+    """gen_instance(kind, w, m, seed0 + k) for k < count, on the device (bit-exact)."""
+    out = torch.empty((count, w, m), dtype=torch.int32, device="cuda")
+    _check(lib().dmm_gen_instances(kind, w, m, seed0, count, out.data_ptr(), _stream(stream)), "gen_instances")
+    return out
+
+
+# --------------------------------------------------------------------------------------
+# Partition / integer sort (partition.hpp:436-456)
+# --------------------------------------------------------------------------------------
+def _general(fn_name: str, grid, domain: int | None, flags: int, out, stream, check: bool):
+    t, single = _as_batch(grid)
+    count, w, m = t.shape
+    res = out if out is not None else torch.empty_like(t)
+    stats = torch.empty((count, 2), dtype=torch.int32, device=t.device)
+    status = torch.empty((count,), dtype=torch.uint8, device=t.device)
+    L = lib()
+    if fn_name == "partition_general":
+        st = L.dmm_partition_general(t.data_ptr(), res.data_ptr(), w, m, count, flags, stats.data_ptr(),
+                                     status.data_ptr(), _stream(stream))
+    else:
+        st = L.dmm_integer_sort_general(t.data_ptr(), res.data_ptr(), w, m, count, domain, flags, stats.data_ptr(),
+                                        status.data_ptr(), _stream(stream))
+    _check(st, fn_name)
+    gs = GeneralStats(stats[:, 0], stats[:, 1] != 0, status)
+    if check:
+        _raise_first(status, fn_name)
+    return (res[0] if single else res), gs
+
+
+def partition_general(grid, *, flags: int = 0, out=None, stream=None, check: bool = True):
+    """GeneralStats partition_general(const MatrixView&)  partition.hpp:453-456.
+
+    Labels in [0, w), m copies each.  Returns (partitioned grid(s), GeneralStats).
+    flags: FLAG_EXT_PARTIAL_GROUPS accepts shapes like 32 x 8 that the reference's
+    balance() rejects; FLAG_NONSTRICT = MachineConfig.strict false.
+    """
+    return _general("partition_general", grid, None, flags, out, stream, check)
+
+
+def integer_sort_general(grid, domain: int, *, enforce_analysis_pre: bool = True, flags: int = 0, out=None,
+                         stream=None, check: bool = True):
+    """GeneralStats integer_sort_general(view, domain, probe, enforce_analysis_pre)  partition.hpp:436-449."""
+    if not enforce_analysis_pre:
+        flags |= FLAG_NO_ENFORCE_PRE
+    return _general("integer_sort_general", grid, domain, flags, out, stream, check)
+
+
+def _simple(fn_name: str, grid, *args, out=None, stream=None, w_arg_only: bool = False):
+    t, single = _as_batch(grid)
+    count, w, m = t.shape
+    res = out if out is not None else torch.empty_like(t)
+    fn = getattr(lib(), "dmm_" + fn_name)
+    if w_arg_only:
+        st = fn(t.data_ptr(), res.data_ptr(), w, count, *args, _stream(stream))
+    else:
+        st = fn(t.data_ptr(), res.data_ptr(), w, m, count, *args, _stream(stream))
+    _check(st, fn_name)
+    return res[0] if single else res
+
+
+def partition_square(grid, *, out=None, stream=None):
+    """void partition_square(const MatrixView&)  partition.hpp:189-197."""
+    t, single = _as_batch(grid)
+    res = out if out is not None else torch.empty_like(t)
+    count, w, m = t.shape
+    _check(lib().dmm_partition_square(t.data_ptr(), res.data_ptr(), w, m, count, None, _stream(stream)),
+           "partition_square")
+    return res[0] if single else res
+
+
+def partition_short_wide(grid, *, out=None, stream=None):
+    """void partition_short_wide(const MatrixView&, hook)  partition.hpp:178-185."""
+    t, single = _as_batch(grid)
+    res = out if out is not None else torch.empty_like(t)
+    count, w, m = t.shape
+    _check(lib().dmm_partition_short_wide(t.data_ptr(), res.data_ptr(), w, m, count, None, _stream(stream)),
+           "partition_short_wide")
+    return res[0] if single else res
+
+
+# --------------------------------------------------------------------------------------
+# Comparison sorts (sort.hpp) and layout primitives (layout.hpp)
+# --------------------------------------------------------------------------------------
+def sort_wide_any(grid, ascending: bool = True, **kw):
+    """detail::sort_wide_any(view, asc)  sort.hpp:321-330 (w <= m, w | m)."""
+    return _simple("sort_wide_any", grid, int(ascending), **kw)
+
+
+def sort_tall(grid, **kw):
+    """void sort_tall(const MatrixView&)  sort.hpp:352-374 (w >= m, m | w)."""
+    return _simple("sort_tall", grid, **kw)
+
+
+def sort_square(grid, ascending: bool = True, **kw):
+    """void sort_square(view, ascending)  sort.hpp:337-346."""
+    return _simple("sort_square", grid, int(ascending), **kw)
+
+
+def sort_short_wide(grid, ascending: bool = True, **kw):
+    """void sort_short_wide(view, ascending, hook)  sort.hpp:225-230."""
+    return _simple("sort_short_wide", grid, int(ascending), **kw)
+
+
+def transpose_square(grid, **kw):
+    """transpose_square layout.hpp:24-61."""
+    return _simple("transpose_square", grid, w_arg_only=True, **kw)
+
+
+def to_column_major(grid, **kw):
+    """to_column_major layout.hpp:397-399."""
+    return _simple("to_column_major", grid, **kw)
+
+
+def to_row_major(grid, **kw):
+    """to_row_major layout.hpp:403-405."""
+    return _simple("to_row_major", grid, **kw)
+
+
+ORDER_ASC, ORDER_DESC, ORDER_ALT, ORDER_ALT_DESC = 0, 1, 2, 3
+
+
+def sort_rows(grid, order: int = ORDER_ASC, domain: int = 0, *, out=None, stream=None, check: bool = True):
+    """radix_sort_rows(view, domain, order) partition.hpp:94 / sort_rows(view, order) sort.hpp:76."""
+    t, single = _as_batch(grid)
+    count, w, m = t.shape
+    res = out if out is not None else torch.empty_like(t)
+    status = torch.empty((count,), dtype=torch.uint8, device=t.device)
+    _check(lib().dmm_sort_rows(t.data_ptr(), res.data_ptr(), w, m, count, order, domain, status.data_ptr(),
+                               _stream(stream)), "sort_rows")
+    if check:
+        _raise_first(status, "sort_rows")
+    return res[0] if single else res
+
+
+# --------------------------------------------------------------------------------------
+# Randomized permutation (permute.hpp:545-628)
+# --------------------------------------------------------------------------------------
+@dataclass
+class PermuteReports:
+    """PermuteReport permute.hpp:62-72, per instance."""
+    iterations: np.ndarray
+    fallback: np.ndarray
+    used_packing: np.ndarray
+    packed_width: np.ndarray
+    threshold: np.ndarray
+    random_words: np.ndarray
+    cleanup_retries: np.ndarray
+    leftover_history: list
+    shifts: np.ndarray
+    status: np.ndarray
+
+    def report(self, k: int) -> dict:
+        return {"iterations": int(self.iterations[k]), "fallback": bool(self.fallback[k]),
+                "used_packing": bool(self.used_packing[k]), "packed_width": int(self.packed_width[k]),
+                "threshold": int(self.threshold[k]), "random_words": int(self.random_words[k]),
+                "cleanup_retries": int(self.cleanup_retries[k]), "leftover_history": self.leftover_history[k],
+                "shifts": self.shifts[k].tolist()}
+
+
+def permute(grid, seeds, alpha: int = 4, iter_cap: int = 64, *, out=None, stream=None, check: bool = True):
+    """PermuteReport permute(Machine&, Rng&, const PermuteParams&)  permute.hpp:545-628.
+
+    grid: [count, w, m] label bijections; seeds: count seeds of each instance's Rng.
+    Returns (output regions [count, w, m], PermuteReports).
+    """
+    t, single = _as_batch(grid)
+    count, w, m = t.shape
+    sd = torch.as_tensor(np.asarray(seeds, dtype=np.uint64).view(np.int64).reshape(-1), device="cuda")
+    if sd.numel() != count:
+        raise ValueError("one seed per instance")
+    res = out if out is not None else torch.empty_like(t)
+    reps = torch.zeros((count, 6), dtype=torch.int64, device="cuda")  # 48-byte dmm_permute_report
+    hist = torch.zeros((count, 64), dtype=torch.int64, device="cuda")
+    shifts = torch.zeros((count, w), dtype=torch.int32, device="cuda")
+    status = torch.zeros((count,), dtype=torch.uint8, device="cuda")
+    L = lib()
+    ws = torch.empty((max(1, int(L.dmm_permute_workspace_bytes(w, m, count))),), dtype=torch.uint8, device="cuda")
+    _check(L.dmm_permute(t.data_ptr(), res.data_ptr(), w, m, count, sd.data_ptr(), alpha, iter_cap, reps.data_ptr(),
+                         hist.data_ptr(), shifts.data_ptr(), status.data_ptr(), ws.data_ptr(), _stream(stream)),
+           "permute")
+    if check:
+        _raise_first(status, "permute")
+    r = reps.cpu().numpy().view(np.uint32).reshape(count, 12)
+    r64 = reps.cpu().numpy().view(np.uint64).reshape(count, 6)
+    n_hist = r[:, 9]
+    h = hist.cpu().numpy().view(np.uint64)
+    rep = PermuteReports(iterations=r[:, 0], fallback=r[:, 1], used_packing=r[:, 2], packed_width=r[:, 3],
+                         threshold=r64[:, 2], random_words=r64[:, 3], cleanup_retries=r[:, 8],
+                         leftover_history=[h[k, : n_hist[k]].tolist() for k in range(count)],
+                         shifts=shifts.cpu().numpy().view(np.uint32), status=status.cpu().numpy())
+    return (res[0] if single else res), rep
+
+
+def version() -> str:
+    return lib().dmm_version().decode()
+
+
+def supported(algorithm: str, w: int, m: int) -> bool:
+    return bool(lib().dmm_supported(algorithm.encode(), w, m))

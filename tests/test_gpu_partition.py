@@ -1,0 +1,172 @@
+"""GPU parity: kernels 1-3 (partition / general partition / integer sort) through the C ABI
+against the oracle (C restatement pinned to the reference) and the golden fixtures.
+
+Bar: bit-exact outputs AND bit-exact GeneralStats (cleanup_retries, sorted) per instance.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import FLAG_EXT_PARTIAL_GROUPS
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1507_01391_b200 as dmm  # noqa: E402
+
+
+def _oracle_batch(port, kind, w, m, seeds):
+    return np.stack([port.gen_instance(kind, w, m, s) for s in seeds]).astype(np.uint32)
+
+
+@pytest.mark.parametrize("kind,w,m", [(1, 32, 8), (1, 32, 16), (1, 32, 32), (2, 32, 32), (2, 32, 16), (1, 32, 64)])
+def test_gen_instances_bit_exact(port, kind, w, m):
+    seeds = list(range(100, 164))
+    dev = dmm.as_uint32(dmm.gen_instances(kind, w, m, 100, 64))
+    assert (dev == _oracle_batch(port, kind, w, m, seeds)).all()
+
+
+def test_gen_sort_u32_bit_exact(port):
+    dev = dmm.as_uint32(dmm.gen_instances(dmm.KIND_SORT_U32, 32, 128, 7, 4))
+    for k in range(4):
+        assert (dev[k] == port.gen_sort_u32(32, 128, 7 + k).astype(np.uint32)).all()
+
+
+@pytest.mark.parametrize("m,flags", [(8, FLAG_EXT_PARTIAL_GROUPS), (16, 0), (32, 0), (64, 0)])
+def test_partition_general_vs_oracle(port, m, flags):
+    seeds = list(range(1, 41)) + [12345]  # odd count: exercises the unpaired half of the last warp
+    grids = _oracle_batch(port, 1, 32, m, seeds)
+    out, st = dmm.partition_general(grids, flags=flags)
+    out = dmm.as_uint32(out)
+    retries = st.cleanup_retries.cpu().numpy()
+    for k, s in enumerate(seeds):
+        ost, oout, orep = port.partition_general(grids[k], flags)
+        assert ost == 0
+        assert (out[k] == oout).all(), (m, s)
+        assert retries[k] == orep["cleanup_retries"] and bool(st.sorted[k]) == orep["sorted"]
+
+
+def test_partition_golden(golden):
+    meta, arr = golden
+    for case in meta["partition"]:
+        if case["w"] != 32 or not dmm.supported("partition_general", case["w"], case["m"]):
+            continue
+        out, st = dmm.partition_general(arr[case["key"] + "_in"])
+        assert (dmm.as_uint32(out) == arr[case["key"] + "_out"]).all(), case["key"]
+        assert int(st.cleanup_retries[0]) == case["cleanup_retries"]
+
+
+@pytest.mark.parametrize("m,domain", [(16, 512), (32, 1024), (16, 1 << 20), (32, 1 << 32), (64, 2048)])
+def test_integer_sort_vs_oracle(port, m, domain):
+    rng = np.random.default_rng(m)
+    if domain <= 32 * m:
+        grids = _oracle_batch(port, 2, 32, m, range(30, 47))
+    else:
+        grids = rng.integers(0, domain, size=(17, 32, m), dtype=np.uint64).astype(np.uint32)
+    out, st = dmm.integer_sort_general(grids, domain)
+    out = dmm.as_uint32(out)
+    for k in range(grids.shape[0]):
+        ost, oout, orep = port.integer_sort_general(grids[k], domain)
+        assert ost == 0 and (out[k] == oout).all()
+        assert int(st.cleanup_retries[k]) == orep["cleanup_retries"]
+
+
+def test_integer_sort_golden(golden):
+    meta, arr = golden
+    for case in meta["intsort"] + meta["u32sort"]:
+        if case["w"] != 32 or not dmm.supported("integer_sort_general", 32, case["m"]):
+            continue
+        dom = case.get("domain", 1 << 32)
+        out, st = dmm.integer_sort_general(arr[case["key"] + "_in"], dom)
+        assert (dmm.as_uint32(out) == arr[case["key"] + "_out"]).all(), case["key"]
+
+
+@pytest.mark.parametrize("m,flags", [(8, FLAG_EXT_PARTIAL_GROUPS), (16, 0), (32, 0)])
+def test_partition_large_batch_properties(m, flags):
+    # full-size property check: every instance ends with row i = i (verify_partition_result
+    # instance.hpp:249); inputs generated on the device with the reference's generator
+    count = 1 << 16
+    g = dmm.gen_instances(dmm.KIND_PARTITION, 32, m, 1, count)
+    out, st = dmm.partition_general(g, flags=flags)
+    rows = torch.arange(32, device="cuda", dtype=torch.int32).view(1, 32, 1)
+    assert bool((out == rows).all())
+    assert bool(st.sorted.all()) and int((st.status != 0).sum()) == 0
+    # the multiset is preserved in place too (in == out aliasing)
+    g2 = g.clone()
+    dmm.partition_general(g2, flags=flags, out=g2)
+    assert bool((g2 == rows).all())
+
+
+def test_partition_errors(port):
+    g = _oracle_batch(port, 1, 32, 8, [3])
+    with pytest.raises(dmm.ShapeViolation):  # reference rejects 32x8 (partition.hpp:241-244)
+        dmm.partition_general(g)
+    g4 = _oracle_batch(port, 1, 32, 4, [3])
+    with pytest.raises(dmm.ShapeViolation):  # m > 2 sqrt(log2 w) (partition.hpp:443-445)
+        dmm.partition_general(g4, flags=FLAG_EXT_PARTIAL_GROUPS)
+    bad = _oracle_batch(port, 1, 32, 16, [4, 5, 6])
+    bad[1, 0, 0] = 31 if bad[1, 0, 0] != 31 else 30  # wrong label counts
+    with pytest.raises(dmm.InvalidInstance):
+        dmm.partition_general(bad)
+    _, st = dmm.partition_general(bad, check=False)
+    assert st.status.cpu().tolist() == [0, 2, 0]
+    bad[2, 3, 3] = 40  # label outside [0, w)
+    _, st = dmm.partition_general(bad, check=False)
+    assert st.status.cpu().tolist() == [0, 2, 2]
+    keys = _oracle_batch(port, 2, 32, 16, [1])
+    keys[0, 5, 5] = 600
+    with pytest.raises(dmm.KeyOutOfRange):
+        dmm.integer_sort_general(keys, 512)
+
+
+def test_sort_wide_any_vs_oracle():
+    rng = np.random.default_rng(3)
+    g = rng.integers(0, 2 ** 32, size=(9, 32, 32), dtype=np.uint64).astype(np.uint32)
+    for asc in (True, False):
+        out = dmm.as_uint32(dmm.sort_wide_any(g, ascending=asc))
+        for k in range(9):
+            exp = np.sort(g[k].ravel())
+            if not asc:
+                exp = exp[::-1]
+            assert (out[k].ravel() == exp).all()
+
+
+@pytest.mark.parametrize("m", [2, 4, 8, 16, 32])
+def test_sort_tall_vs_oracle(port, m):
+    rng = np.random.default_rng(m)
+    g = rng.integers(0, 1000, size=(5, 32, m), dtype=np.uint64).astype(np.uint32)
+    out = dmm.as_uint32(dmm.sort_tall(g))
+    for k in range(5):
+        st, exp = port.simple("sort_tall", g[k])
+        assert st == 0 and (out[k] == exp).all()
+
+
+@pytest.mark.parametrize("m", [1, 2, 4, 8, 16, 32, 64])
+def test_layout_primitives_vs_oracle(port, m):
+    g = np.arange(3 * 32 * m, dtype=np.uint32).reshape(3, 32, m)
+    for name in ("to_column_major", "to_row_major"):
+        out = dmm.as_uint32(getattr(dmm, name)(g))
+        for k in range(3):
+            st, exp = port.simple(name, g[k])
+            assert (out[k] == exp).all(), (name, m)
+    if m == 32:
+        out = dmm.as_uint32(dmm.transpose_square(g))
+        for k in range(3):
+            assert (out[k] == g[k].T).all()
+
+
+def test_sort_rows_orders():
+    rng = np.random.default_rng(5)
+    g = rng.integers(0, 100, size=(4, 32, 16), dtype=np.uint64).astype(np.uint32)
+    for order in range(4):
+        out = dmm.as_uint32(dmm.sort_rows(g, order=order))
+        for r in range(32):
+            asc = order == 0 or (order == 2 and r % 2 == 0) or (order == 3 and r % 2 == 1)
+            exp = np.sort(g[:, r, :], axis=1)
+            if not asc:
+                exp = exp[:, ::-1]
+            assert (out[:, r, :] == exp).all()
+    with pytest.raises(dmm.KeyOutOfRange):  # row_radix_segment partition.hpp:63
+        dmm.sort_rows(g, order=0, domain=50)
