@@ -159,6 +159,50 @@ __device__ __forceinline__ void partition_leaf(uint32_t (&x)[M], uint32_t* buf, 
     sort_wide_any<PK, V>(x, buf, lane, true);
 }
 
+// sort_columns_network sort.hpp:115-156: every column sorted ascending across the
+// rows.  The reference drives a Batcher comparator network between row pairs; on
+// the warp the network runs across lanes with shuffles (no shared memory, so no
+// bank to conflict on).  Outcome: the unique ascending column.
+template <int PK, int M>
+__device__ __forceinline__ void sort_columns_network(uint32_t (&x)[M], int lane) {
+#pragma unroll
+    for (int k = 2; k <= kWarp; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j >= 1; j >>= 1) {
+            const bool up = (lane & k) == 0 || k == kWarp;
+            const bool lower = (lane & j) == 0;
+            const bool keep_min = lower == up;
+#pragma unroll
+            for (int c = 0; c < M; ++c) {
+                const uint32_t p = __shfl_xor_sync(0xFFFFFFFFu, x[c], j);
+                uint32_t lo = x[c], hi = p;
+                Key<PK>::cx(lo, hi);
+                x[c] = keep_min ? lo : hi;
+            }
+        }
+    }
+}
+
+// sort_tall sort.hpp:352-374 on the full warp view (w = 32 >= m, m | w)
+template <int PK, class V, int M>
+__device__ __forceinline__ void sort_tall(uint32_t (&x)[M], uint32_t* buf, int lane) {
+    static_assert(V::MASK == 0xFFFFFFFFu && V::ST == 1 && V::WV == kWarp && V::C0 == 0 && V::MV == M,
+                  "sort_tall on the full warp view");
+    static_assert(V::WV >= V::MV && V::WV % V::MV == 0, "sort_tall needs w >= m and m | w (ShapeViolation)");
+    if constexpr (V::WV == V::MV) {
+        sort_wide_any<PK, V>(x, buf, lane, true);
+    } else {
+        row_sort<PK, V>(x, lane, true);
+        sort_columns_network<PK>(x, lane);
+        to_row_major<V>(x, buf, lane);
+        sort_columns_network<PK>(x, lane);
+        using B = VRows<V, V::MV>;  // m x m blocks, alternating direction per block
+        sort_wide_any<PK, B>(x, buf, lane, ((lane / V::MV) % 2) == 0);
+        sort_columns_network<PK>(x, lane);
+        row_sort<PK, V>(x, lane, true);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Balancing, convert-and-divide, recursion  partition.hpp:234-428
 // ---------------------------------------------------------------------------
@@ -204,40 +248,63 @@ __device__ __forceinline__ void levels(uint32_t (&x)[M], uint32_t* buf, int lane
     }
 }
 
-// scan_sorted partition.hpp:308-337 on the full warp view: bit h set = half h sorted.
-// The reference's tree_reduce_sum + broadcast of the verdict is one warp reduction.
+// Lane masks of the shifted-cleanup blocks inside aligned contiguous views of WV rows.
+__host__ __device__ constexpr uint32_t edge_mask(int WV, int H) {
+    uint32_t m = 0;
+    for (int l = 0; l < kWarp; ++l)
+        if (l % WV < H || l % WV >= WV - H)
+            m |= 1u << l;
+    return m;
+}
+__host__ __device__ constexpr uint32_t mid_mask(int WV, int H) { return ~edge_mask(WV, H); }
+
+// scan_sorted partition.hpp:308-337 over a family of aligned contiguous views: each
+// lane returns its view's verdict (bit h set = half h sorted row-major).  The
+// reference's tree_reduce_sum + broadcast of the verdict is a butterfly OR inside
+// each group of WV lanes.
 template <int PK, class V, int M>
 __device__ __forceinline__ uint32_t scan_sorted(const uint32_t (&x)[M], int lane) {
-    static_assert(V::MASK == 0xFFFFFFFFu && V::ST == 1 && V::WV == kWarp, "scan_sorted on the full warp view");
+    static_assert(V::MASK == 0xFFFFFFFFu && V::ST == 1 && V::LO == 0 && kWarp % V::WV == 0,
+                  "scan_sorted on aligned contiguous views");
     uint32_t bad = 0;
 #pragma unroll
     for (int c = V::C0 + 1; c < V::C0 + V::MV; ++c)
         bad |= Key<PK>::gt(x[c - 1], x[c]);
     const uint32_t next_first = __shfl_down_sync(0xFFFFFFFFu, x[V::C0], 1);
-    if (lane + 1 < kWarp)
+    if (V::local(lane) + 1 < V::WV)
         bad |= Key<PK>::gt(x[V::C0 + V::MV - 1], next_first);
-    bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+#pragma unroll
+    for (int off = 1; off < V::WV; off <<= 1)
+        bad |= __shfl_xor_sync(0xFFFFFFFFu, bad, off);
     return Key<PK>::kAll & ~bad;
 }
 
-// cleanup_pass_pair partition.hpp:341-361 on the full warp view
+// cleanup_pass_pair partition.hpp:341-361 over a family of aligned contiguous views
 template <int PK, class V, int M>
 __device__ __forceinline__ void cleanup_pass_pair(uint32_t (&x)[M], uint32_t* buf, int lane) {
-    static_assert(V::MASK == 0xFFFFFFFFu && V::ST == 1 && V::WV == kWarp, "cleanup on the full warp view");
+    static_assert(V::MASK == 0xFFFFFFFFu && V::ST == 1 && V::LO == 0 && kWarp % V::WV == 0,
+                  "cleanup on aligned contiguous views");
     partition_leaf<PK, VRows<V, V::MV>>(x, buf, lane);  // aligned m x m blocks
     if constexpr (V::WV > V::MV && V::MV >= 2) {
         constexpr int H = V::MV / 2;
-        using Edge = VF<lane_range_mask(0, H) | lane_range_mask(kWarp - H, kWarp), 0, 1, H, V::C0, V::MV>;
-        using Mid = VF<lane_range_mask(H, kWarp - H), H, 1, V::MV, V::C0, V::MV>;
-        partition_leaf<PK, Edge>(x, buf, lane);  // the two m/2-row end blocks
+        using Edge = VF<edge_mask(V::WV, H), 0, 1, H, V::C0, V::MV>;
+        using Mid = VF<mid_mask(V::WV, H), H, 1, V::MV, V::C0, V::MV>;
+        partition_leaf<PK, Edge>(x, buf, lane);  // the two m/2-row end blocks of every view
         partition_leaf<PK, Mid>(x, buf, lane);   // the m/2-shifted m-row blocks
     }
 }
 
-// Per-instance result of a general sort (one entry per packed half).
+// Per-instance result of a general sort (one entry per packed half).  Accumulated
+// per lane (each lane sees its own views); finish() reduces over the warp:
+// GeneralStats.cleanup_retries is the max over every recursion level and view.
 struct GenResult {
     uint32_t retries[2];  // cleanup_retries (GeneralStats partition.hpp:292-295)
     uint32_t unsorted;    // bit h: cleanup budget exhausted for half h
+    __device__ void finish() {
+        retries[0] = __reduce_max_sync(0xFFFFFFFFu, retries[0]);
+        retries[1] = __reduce_max_sync(0xFFFFFFFFu, retries[1]);
+        unsorted = __reduce_or_sync(0xFFFFFFFFu, unsorted);
+    }
 };
 
 // balance_divide_sort partition.hpp:363-428
@@ -265,7 +332,7 @@ __device__ __forceinline__ void balance_divide_sort(uint32_t (&x)[M], uint32_t* 
             if (fresh & 2u)
                 res.retries[1] = max(res.retries[1], (uint32_t)passes);
             done |= ok;
-            if (done == Key<PK>::kAll || passes == budget)
+            if (__all_sync(0xFFFFFFFFu, done == Key<PK>::kAll) || passes == budget)
                 break;
             ++passes;
         }

@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(256) k_general_sort(const uint32_t* __restrict
         sort_wide_any<PK, V>(x, buf, lane, ascending != 0);
     else
         balance_divide_sort<PK, V, EXT>(x, buf, lane, res);
+    res.finish();
 
     uint32_t invalid = 0;
     if constexpr (MODE == kModePartition) {

@@ -9,30 +9,6 @@
 
 namespace dmmdev {
 
-// sort_columns_network sort.hpp:115-156: every column sorted ascending across the
-// rows.  The reference drives a Batcher comparator network between row pairs; on
-// the warp the network runs across lanes with shuffles (no shared memory, so no
-// bank to conflict on).  Outcome: the unique ascending column.
-template <int PK, int M>
-__device__ __forceinline__ void sort_columns_network(uint32_t (&x)[M], int lane) {
-#pragma unroll
-    for (int k = 2; k <= kWarp; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j >= 1; j >>= 1) {
-            const bool up = (lane & k) == 0 || k == kWarp;
-            const bool lower = (lane & j) == 0;
-            const bool keep_min = lower == up;
-#pragma unroll
-            for (int c = 0; c < M; ++c) {
-                const uint32_t p = __shfl_xor_sync(0xFFFFFFFFu, x[c], j);
-                uint32_t lo = x[c], hi = p;
-                Key<PK>::cx(lo, hi);
-                x[c] = keep_min ? lo : hi;
-            }
-        }
-    }
-}
-
 enum : int { kOpTranspose = 0, kOpToCol = 1, kOpToRow = 2, kOpSortRows = 3, kOpSortTall = 4 };
 
 template <int M, int OP>
@@ -67,18 +43,7 @@ __global__ void __launch_bounds__(256) k_layout(const uint32_t* __restrict__ in,
             status[k] = (bad && M > 1) ? DMM_KEY_OUT_OF_RANGE : DMM_OK;
     } else if constexpr (OP == kOpSortTall) {
         // sort_tall sort.hpp:352-374 (w >= m, m | w)
-        if constexpr (M == kWarp) {
-            sort_wide_any<1, V>(x, buf, lane, true);
-        } else {
-            row_sort<1, V>(x, lane, true);
-            sort_columns_network<1>(x, lane);
-            to_row_major<V>(x, buf, lane);
-            sort_columns_network<1>(x, lane);
-            using B = VRows<V, M>;  // m x m blocks, alternating direction per block
-            sort_wide_any<1, B>(x, buf, lane, ((lane / M) % 2) == 0);
-            sort_columns_network<1>(x, lane);
-            row_sort<1, V>(x, lane, true);
-        }
+        sort_tall<1, V>(x, buf, lane);
     }
     store_row<M>(out + (k * kWarp + lane) * M, x);
 }

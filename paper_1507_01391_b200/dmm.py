@@ -352,7 +352,7 @@ def permute(grid, seeds, alpha: int = 4, iter_cap: int = 64, *, out=None, stream
     if sd.numel() != count:
         raise ValueError("one seed per instance")
     res = out if out is not None else torch.empty_like(t)
-    reps = torch.zeros((count, 6), dtype=torch.int64, device="cuda")  # 48-byte dmm_permute_report
+    reps = torch.zeros((count, 5), dtype=torch.int64, device="cuda")  # 40-byte dmm_permute_report
     hist = torch.zeros((count, 64), dtype=torch.int64, device="cuda")
     shifts = torch.zeros((count, w), dtype=torch.int32, device="cuda")
     status = torch.zeros((count,), dtype=torch.uint8, device="cuda")
@@ -363,8 +363,8 @@ def permute(grid, seeds, alpha: int = 4, iter_cap: int = 64, *, out=None, stream
            "permute")
     if check:
         _raise_first(status, "permute")
-    r = reps.cpu().numpy().view(np.uint32).reshape(count, 12)
-    r64 = reps.cpu().numpy().view(np.uint64).reshape(count, 6)
+    r = reps.cpu().numpy().view(np.uint32).reshape(count, 10)
+    r64 = reps.cpu().numpy().view(np.uint64).reshape(count, 5)
     n_hist = r[:, 9]
     h = hist.cpu().numpy().view(np.uint64)
     rep = PermuteReports(iterations=r[:, 0], fallback=r[:, 1], used_packing=r[:, 2], packed_width=r[:, 3],
