@@ -35,10 +35,13 @@ CONFIGS = {
              "general w-way partition w=32, n=256 (n<w^2) per instance, 2^18 instances"),
     "cfg2b": ("partition_general", 32, 16, 1 << 17, 0,
               "general w-way partition w=32, n=512 (reference-accepted stand-in of cfg2), 2^17 instances"),
-    "cfg3s": ("integer_sort_general", 32, 32, 1 << 16, 0,
-              "integer sort of uint32 keys, 32x32 tiles (domain 2^32), 2^16 tiles"),
+    "cfg3": ("integer_sort_general", 32, 128, 1 << 20, 0,
+             "bank-conflict-free sort w=32, n=4096 uint32 keys per block-tile (32x128), 2^20 tiles"),
+    "cfg4": ("permute", 32, 32, 1 << 18, 0,
+             "randomized permutation w=32, n=1024 per instance (32x32: the reference rejects n=8192 at w=32), "
+             "seeded Rng per instance, 2^18 instances"),
 }
-ALG_ID = {"partition_general": 5, "integer_sort_general": 6}
+ALG_ID = {"partition_general": 5, "integer_sort_general": 6, "permute": 7}
 
 
 def _peaks():
@@ -110,11 +113,17 @@ def cpu_baseline(cfg_name: str, seconds: float = 15.0):
     import numpy as np
     nthreads = os.cpu_count() or 1
     kind = 1 if alg == "partition_general" else 2
+    if alg == "integer_sort_general":
+        kind = 0
     sample = 64
     # grow the sample until the run takes ~seconds/4 (bounded)
     while True:
-        inst = np.stack([port.gen_instance(kind, w, m, s) for s in range(sample)]).astype(np.uint32)
-        st, secs, good = ref.cpu_baseline(ALG_ID[alg], inst, nthreads=nthreads)
+        if kind == 0:
+            inst = np.stack([port.gen_sort_u32(w, m, s) for s in range(sample)]).astype(np.uint32)
+        else:
+            inst = np.stack([port.gen_instance(kind, w, m, s) for s in range(sample)]).astype(np.uint32)
+        st, secs, good = ref.cpu_baseline(ALG_ID[alg], inst, seeds=np.arange(sample, dtype=np.uint64),
+                                          domain=1 << 32, nthreads=nthreads)
         if secs * 4 >= seconds or sample >= (1 << 16):
             break
         sample *= 2
@@ -151,11 +160,13 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--count", type=int, default=0, help="instances per GPU (default: the config's)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
 
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -169,16 +180,25 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     alg, w, m, count, flags, desc = CONFIGS[args.config]
+    if args.count:
+        count = args.count
+        desc += f" [count overridden: {count}]"
     keys_per_gpu = count * w * m
-    kind = dmm.KIND_PARTITION if alg == "partition_general" else dmm.KIND_SORT_U32
+    kind = {"partition_general": dmm.KIND_PARTITION, "integer_sort_general": dmm.KIND_SORT_U32,
+            "permute": dmm.KIND_PERMUTE}[alg]
     # rank r owns instances [r*count, (r+1)*count): seeds are disjoint across ranks
     g = dmm.gen_instances(kind, w, m, 1 + rank * count, count)
     out = torch.empty_like(g)
     stream = torch.cuda.current_stream()
 
+    seeds = np.arange(1 + rank * count, 1 + (rank + 1) * count, dtype=np.uint64)
+    perm_bufs = {}
+
     def step(src, dst):
         if alg == "partition_general":
             return dmm.partition_general(src, flags=flags, out=dst, check=False)
+        if alg == "permute":
+            return dmm.permute_into(src, dst, seeds, perm_bufs)
         return dmm.integer_sort_general(src, 1 << 32, out=dst, check=False)
 
     for _ in range(args.warmup):
@@ -210,6 +230,9 @@ def main():
     if alg == "partition_general":
         rows = torch.arange(w, device="cuda", dtype=torch.int32).view(1, w, 1)
         ok = bool((out == rows).all()) and int((st.status != 0).sum()) == 0
+    elif alg == "permute":
+        exp = torch.arange(w * m, device="cuda", dtype=torch.int32).view(1, w, m)
+        ok = bool((out == exp).all())
     else:
         ok = bool((out.view(count, -1)[:, 1:].to(torch.int64) & 0xFFFFFFFF >=
                    out.view(count, -1)[:, :-1].to(torch.int64) & 0xFFFFFFFF).all())

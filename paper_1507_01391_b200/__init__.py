@@ -9,5 +9,5 @@ from .dmm import (  # noqa: F401
     DivisibilityViolation, Error, GeneralStats, InvalidInstance, KeyOutOfRange, NotSquare, OutOfBounds,
     OverlappingViews, PackingOverflow, PermuteReports, PostconditionFailed, ShapeViolation, UnsupportedShape,
     as_uint32, gen_instances, integer_sort_general, lib, partition_general, partition_short_wide,
-    partition_square, permute, sort_rows, sort_short_wide, sort_square, sort_tall, sort_wide_any, supported,
+    partition_square, permute, permute_into, sort_rows, sort_short_wide, sort_square, sort_tall, sort_wide_any, supported,
     to_column_major, to_row_major, transpose_square, version)

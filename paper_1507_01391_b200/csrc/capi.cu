@@ -28,7 +28,7 @@ int dmm_supported(const char* algorithm, uint32_t w, uint32_t m) {
         return 0;
     const std::string a(algorithm);
     if (a == "partition_general" || a == "integer_sort_general")
-        return m == 8 || m == 16 || m == 32 || m == 64;
+        return m == 8 || m == 16 || m == 32 || m == 64 || m == 128;
     if (a == "sort_wide_any")
         return m == 32 || m == 64;
     return 0;

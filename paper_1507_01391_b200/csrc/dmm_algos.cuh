@@ -152,11 +152,93 @@ __device__ __forceinline__ void sort_wide_any(uint32_t (&x)[M], uint32_t* buf, i
         shearsort_rect<PK, V>(x, buf, lane, asc);
 }
 
-// partition_leaf partition.hpp:156-172 (radix rows; the dispatch is the same as
-// sort_wide_any, always ascending)
+// ---------------------------------------------------------------------------
+// Block sort: bitonic network over a whole view (WV lanes x MV registers) into
+// row-major order.  Element e = local_row * MV + c has bits [r | q | l]: r = low
+// log2(WV) register bits, q = the remaining register bits, l = the local row.
+// Stages on r/q bits are register-local; stages on l bits run after a
+// conflict-free blocked transpose (which turns l into register bits).  A comparator's
+// direction is bit kc of e: static when that bit is a register bit, otherwise the
+// whole lane flips its keys (x ^= ~0 reverses the order) around the stages.
+// ---------------------------------------------------------------------------
+// stages jb = JB..0 on registers [OFF, OFF+N): pairs (p, p ^ 2^jb); ascending iff
+// DIRBIT < 0 or bit DIRBIT of p is clear
+template <int PK, int OFF, int N, int JB, int DIRBIT, int M>
+__device__ __forceinline__ void reg_stages(uint32_t (&x)[M]) {
+    if constexpr (JB >= 0) {
+#pragma unroll
+        for (int p = 0; p < N; ++p) {
+            if (((p >> JB) & 1) == 0) {
+                if (DIRBIT < 0 || ((p >> DIRBIT) & 1) == 0)
+                    Key<PK>::cx(x[OFF + p], x[OFF + (p | (1 << JB))]);
+                else
+                    Key<PK>::cx(x[OFF + (p | (1 << JB))], x[OFF + p]);
+            }
+        }
+        reg_stages<PK, OFF, N, JB - 1, DIRBIT>(x);
+    }
+}
+
+// l-bit stages of merge level KC in the transposed layout, for every group of WV
+// registers (group QI = one value of the q bits; l bits are the group's low bits)
+template <int PK, class V, int KC, int QI, int M>
+__device__ __forceinline__ void tstages_q(uint32_t (&x)[M]) {
+    constexpr int R = ilog2_ceil_c(V::WV), QB = ilog2_ceil_c(V::MV / V::WV), NB = 2 * R + QB;
+    if constexpr (QI < V::MV / V::WV) {
+        reg_stages<PK, V::C0 + QI * V::WV, V::WV, KC - 1 - (R + QB), (KC < NB ? KC - R - QB : -1)>(x);
+        tstages_q<PK, V, KC, QI + 1>(x);
+    }
+}
+
+template <int PK, class V, int KC, int M>
+__device__ __forceinline__ void block_merge_levels(uint32_t (&x)[M], uint32_t* buf, int lane) {
+    constexpr int R = ilog2_ceil_c(V::WV), QB = ilog2_ceil_c(V::MV / V::WV), NB = 2 * R + QB;
+    if constexpr (KC <= NB) {
+        if constexpr (KC < R + QB) {
+            // the whole merge lives in the lane's registers; direction bit KC is a register bit
+            if (V::active(lane))
+                reg_stages<PK, V::C0, V::MV, KC - 1, KC>(x);
+        } else {
+            if constexpr (KC > R + QB) {
+                // l-bit stages jb = KC-1 .. R+QB in the transposed layout (l = low register bits)
+                transpose_blocks<V>(x, buf, lane);
+                if (V::active(lane))
+                    tstages_q<PK, V, KC, 0>(x);
+                transpose_blocks<V>(x, buf, lane);
+            }
+            // r/q-bit stages in the row layout; direction bit KC is an l bit: per lane
+            if (V::active(lane)) {
+                uint32_t f = 0;
+                if constexpr (KC < NB)
+                    f = ((V::local(lane) >> (KC - R - QB)) & 1) ? 0xFFFFFFFFu : 0u;
+                flip<V::C0, V::MV>(x, f);
+                reg_stages<PK, V::C0, V::MV, R + QB - 1, -1>(x);
+                flip<V::C0, V::MV>(x, f);
+            }
+        }
+        block_merge_levels<PK, V, KC + 1>(x, buf, lane);
+    }
+}
+
+// sort each view's WV x MV block ascending in row-major order (WV, MV powers of two, WV | MV)
+template <int PK, class V, int M>
+__device__ __forceinline__ void sort_block(uint32_t (&x)[M], uint32_t* buf, int lane) {
+    static_assert(V::MV % V::WV == 0, "block sort needs WV | MV");
+    if constexpr (V::WV == 1) {
+        row_sort<PK, V>(x, lane, true);
+    } else {
+        block_merge_levels<PK, V, 1>(x, buf, lane);
+    }
+}
+
+// partition_leaf partition.hpp:156-172.  Its outcome is the view's multiset in
+// row-major sorted order (the reference's short-wide / square / shearsort dispatch
+// always ends there, sort.hpp:200-311), so the leaf runs the cheaper bitonic block
+// sort above; the state after the call is bit-identical.  The skeletons stay in use
+// for the reference's comparison-sort entry points (dmm_sort_wide_any, sort_tall).
 template <int PK, class V, int M>
 __device__ __forceinline__ void partition_leaf(uint32_t (&x)[M], uint32_t* buf, int lane) {
-    sort_wide_any<PK, V>(x, buf, lane, true);
+    sort_block<PK, V>(x, buf, lane);
 }
 
 // sort_columns_network sort.hpp:115-156: every column sorted ascending across the

@@ -158,11 +158,13 @@ struct GeneralArgs {
     cudaStream_t stream;
 };
 
-constexpr int kWarpsPerBlock = 8;
+template <int M>
+constexpr int warps_per_block() { return M >= 128 ? 4 : 8; }
 
 template <int M, int PK, bool EXT, int MODE>
 dmm_status launch_general(const GeneralArgs& a) {
     auto kern = dmmdev::k_general_sort<M, PK, EXT, MODE>;
+    constexpr int kWarpsPerBlock = warps_per_block<M>();
     const size_t smem = size_t(kWarpsPerBlock) * dmmdev::relayout_buf_words(M) * sizeof(uint32_t);
     static bool configured = false;  // per instantiation
     if (!configured) {
@@ -188,5 +190,6 @@ dmm_status launch_general_m8(int mode, bool pk2, bool ext, const GeneralArgs& a)
 dmm_status launch_general_m16(int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_m32(int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_m64(int mode, bool pk2, bool ext, const GeneralArgs& a);
+dmm_status launch_general_m128(int mode, bool pk2, bool ext, const GeneralArgs& a);
 
 }  // namespace dmmhost

@@ -22,6 +22,7 @@ dmm_status dispatch(int mode, const uint32_t* in, uint32_t* out, uint32_t m, uin
         case 16: return launch_general_m16(mode, pk2, ext, a);
         case 32: return launch_general_m32(mode, pk2, ext, a);
         case 64: return launch_general_m64(mode, pk2, ext, a);
+        case 128: return launch_general_m128(mode, pk2, ext, a);
         default: break;
     }
     set_error("no kernel compiled for this shape");

@@ -374,6 +374,24 @@ def permute(grid, seeds, alpha: int = 4, iter_cap: int = 64, *, out=None, stream
     return (res[0] if single else res), rep
 
 
+def permute_into(src: torch.Tensor, dst: torch.Tensor, seeds, bufs: dict, alpha: int = 4, iter_cap: int = 64,
+                 stream=None):
+    """Allocation-free permute over device tensors (bench / pipelines): reports, history,
+    shifts and status land in the reusable buffers of `bufs`; nothing is copied to the host.
+    Returns the status tensor."""
+    count, w, m = src.shape
+    if "seeds" not in bufs or bufs["seeds"].numel() != count:
+        bufs["seeds"] = torch.as_tensor(np.asarray(seeds, dtype=np.uint64).view(np.int64), device="cuda")
+        bufs["reps"] = torch.zeros((count, 5), dtype=torch.int64, device="cuda")
+        bufs["hist"] = torch.zeros((count, 64), dtype=torch.int64, device="cuda")
+        bufs["shifts"] = torch.zeros((count, w), dtype=torch.int32, device="cuda")
+        bufs["status"] = torch.zeros((count,), dtype=torch.uint8, device="cuda")
+    _check(lib().dmm_permute(src.data_ptr(), dst.data_ptr(), w, m, count, bufs["seeds"].data_ptr(), alpha, iter_cap,
+                             bufs["reps"].data_ptr(), bufs["hist"].data_ptr(), bufs["shifts"].data_ptr(),
+                             bufs["status"].data_ptr(), None, _stream(stream)), "permute")
+    return None, bufs["status"]
+
+
 def version() -> str:
     return lib().dmm_version().decode()
 

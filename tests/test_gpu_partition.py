@@ -58,7 +58,8 @@ def test_partition_golden(golden):
         assert int(st.cleanup_retries[0]) == case["cleanup_retries"]
 
 
-@pytest.mark.parametrize("m,domain", [(16, 512), (32, 1024), (16, 1 << 20), (32, 1 << 32), (64, 2048)])
+@pytest.mark.parametrize("m,domain", [(16, 512), (32, 1024), (16, 1 << 20), (32, 1 << 32), (64, 2048),
+                                      (128, 1 << 32), (128, 4096)])
 def test_integer_sort_vs_oracle(port, m, domain):
     rng = np.random.default_rng(m)
     if domain <= 32 * m:
