@@ -34,19 +34,26 @@ struct PermArgs {
 
 constexpr int kRngWords = 312;
 
-// Warp-shared generator: state in smem, `base` = index of the first draw the current
-// state generation serves.
+// Warp-shared generator: the 312-word state in smem as two 32-bit arrays (low and
+// high halves), so every warp-wide access is a unit-stride 32-bit access (no bank
+// conflicts); `base` = index of the first draw the current state generation serves.
 struct WarpRng {
-    uint64_t* st;
+    uint32_t* lo;
+    uint32_t* hi;
     uint32_t base;
 
+    __device__ uint64_t get(int i) const { return ((uint64_t)hi[i] << 32) | lo[i]; }
+    __device__ void put(int i, uint64_t v) {
+        lo[i] = (uint32_t)v;
+        hi[i] = (uint32_t)(v >> 32);
+    }
     __device__ void seed(uint64_t s, int lane) {
         if (lane == 0) {
             uint64_t v = s;
-            st[0] = v;
+            put(0, v);
             for (int i = 1; i < kRngWords; ++i) {
                 v = 6364136223846793005ULL * (v ^ (v >> 62)) + (uint64_t)i;
-                st[i] = v;
+                put(i, v);
             }
         }
         __syncwarp();
@@ -56,14 +63,15 @@ struct WarpRng {
     // mersenne twist of all 312 words: [0,156) from old words; [156,311) from new [0,155)
     // and old words; 311 from new 155 and new 0
     __device__ void twist(int lane) {
-        constexpr uint64_t UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL, MA = 0xB5026F5AA96619E9ULL;
+        constexpr uint64_t MA = 0xB5026F5AA96619E9ULL;
         uint64_t v[5];
 #pragma unroll
         for (int t = 0; t < 5; ++t) {
             const int i = lane + 32 * t;
             if (i < 156) {
-                const uint64_t x = (st[i] & UM) | (st[i + 1] & LM);
-                v[t] = st[i + 156] ^ (x >> 1) ^ ((x & 1) ? MA : 0);
+                // (mt[i] & UM) | (mt[i+1] & LM): the high 33 bits of mt[i], the low 31 of mt[i+1]
+                const uint64_t x = ((uint64_t)hi[i] << 32) | (lo[i] & 0x80000000u) | (lo[i + 1] & 0x7FFFFFFFu);
+                v[t] = get(i + 156) ^ (x >> 1) ^ ((x & 1) ? MA : 0);
             }
         }
         __syncwarp();
@@ -71,15 +79,15 @@ struct WarpRng {
         for (int t = 0; t < 5; ++t) {
             const int i = lane + 32 * t;
             if (i < 156)
-                st[i] = v[t];
+                put(i, v[t]);
         }
         __syncwarp();
 #pragma unroll
         for (int t = 0; t < 5; ++t) {
             const int i = 156 + lane + 32 * t;
             if (i < 311) {
-                const uint64_t x = (st[i] & UM) | (st[i + 1] & LM);
-                v[t] = st[i - 156] ^ (x >> 1) ^ ((x & 1) ? MA : 0);
+                const uint64_t x = ((uint64_t)hi[i] << 32) | (lo[i] & 0x80000000u) | (lo[i + 1] & 0x7FFFFFFFu);
+                v[t] = get(i - 156) ^ (x >> 1) ^ ((x & 1) ? MA : 0);
             }
         }
         __syncwarp();
@@ -87,24 +95,23 @@ struct WarpRng {
         for (int t = 0; t < 5; ++t) {
             const int i = 156 + lane + 32 * t;
             if (i < 311)
-                st[i] = v[t];
+                put(i, v[t]);
         }
         __syncwarp();
         if (lane == 0) {
-            const uint64_t x = (st[311] & UM) | (st[0] & LM);
-            st[311] = st[155] ^ (x >> 1) ^ ((x & 1) ? MA : 0);
+            const uint64_t x = ((uint64_t)hi[311] << 32) | (lo[311] & 0x80000000u) | (lo[0] & 0x7FFFFFFFu);
+            put(311, get(155) ^ (x >> 1) ^ ((x & 1) ? MA : 0));
         }
         __syncwarp();
     }
-    // draw number d (warp-uniform d; lanes may ask for different d within the current
-    // generation).  Advances generations as needed (warp-uniform call).
+    // make draw d (warp-uniform) addressable; advances generations as needed
     __device__ void advance_to(uint32_t d, int lane) {
         while (d >= base + kRngWords) {
             twist(lane);
             base += kRngWords;
         }
     }
-    __device__ uint64_t word(uint32_t d) const { return mt_temper(st[d - base]); }
+    __device__ uint64_t word(uint32_t d) const { return mt_temper(get(d - base)); }
 };
 
 __device__ __forceinline__ uint32_t hash_eval(uint64_t key, uint32_t m, uint32_t i) {  // HashOracle permute.hpp:39
@@ -189,11 +196,11 @@ __device__ __forceinline__ bool finish_packed(uint32_t (&y)[WP], uint32_t* buf, 
 
 template <int M>
 __host__ __device__ constexpr int perm_stage_words() {
-    return (3 * M * 32 > relayout_buf_words(M) ? 3 * M * 32 : relayout_buf_words(M));
+    return (2 * M * 32 > relayout_buf_words(M) ? 2 * M * 32 : relayout_buf_words(M));
 }
 template <int M>
 __host__ __device__ constexpr int perm_warp_words() {  // u32 words of smem per warp
-    return 2 * kRngWords + M * 32 + perm_stage_words<M>() + 2 * M * 32;
+    return 2 * kRngWords + M * 32 + perm_stage_words<M>() + M * 32;
 }
 
 template <int M>
@@ -208,13 +215,12 @@ __global__ void __launch_bounds__(128) k_permute(const uint32_t* __restrict__ in
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     uint32_t* wbase = reinterpret_cast<uint32_t*>(smem64) + warp * perm_warp_words<M>();
-    WarpRng rng{reinterpret_cast<uint64_t*>(wbase), 0};
+    WarpRng rng{wbase, wbase + kRngWords, 0};
     uint32_t* outs = wbase + 2 * kRngWords;     // output region, row i in bank i: outs[j*32 + i]
     uint32_t* stage = outs + M * 32;            // relayout buffer / own-bank rows A,B,H
-    uint32_t* pk = stage + perm_stage_words<M>();  // packed rows (own bank), capacity 2m
-    uint32_t* A = stage;
-    uint32_t* B = stage + M * 32;
-    uint32_t* H = stage + 2 * M * 32;
+    uint32_t* pk = stage + perm_stage_words<M>();  // packed rows (own bank), capacity m
+    uint32_t* H = stage;                           // per-colour counts, then bucket starts
+    uint32_t* B = stage + M * 32;                  // colour-sorted (compacted) row
     const uint64_t k = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     if (k >= count)
         return;
@@ -244,11 +250,11 @@ __global__ void __launch_bounds__(128) k_permute(const uint32_t* __restrict__ in
         __syncwarp();
 #pragma unroll
         for (int c = 0; c < M; ++c)
-            A[((c + sh) % M) * 32 + lane] = x[c];  // own bank: row r rotates in bank r
+            H[((c + sh) % M) * 32 + lane] = x[c];  // own bank: row r rotates in bank r
         __syncwarp();
 #pragma unroll
         for (int c = 0; c < M; ++c)
-            x[c] = A[c * 32 + lane];
+            x[c] = H[c * 32 + lane];
         using Blk = VF<0xFFFFFFFFu, 0, 1, M, 0, M>;  // every aligned m x m block of rows
         transpose_square<Blk>(x, stage, lane);
     }
@@ -262,8 +268,9 @@ __global__ void __launch_bounds__(128) k_permute(const uint32_t* __restrict__ in
         const uint64_t key = rng.word(drawn);
         drawn += M;
         random_words += M;
-        // rescan_and_bucket permute.hpp:174-216: stable own-bank counting sort by colour
-        __syncwarp();
+        // rescan_and_bucket permute.hpp:174-216: stable own-bank counting sort by colour.
+        // Every access below is to the lane's own bank (H, B columns = lane): conflict-free
+        // for any data, no warp synchronisation needed.
 #pragma unroll
         for (int b = 0; b < M; ++b)
             H[b * 32 + lane] = 0;
@@ -283,39 +290,50 @@ __global__ void __launch_bounds__(128) k_permute(const uint32_t* __restrict__ in
         for (int b = 0; b < M; ++b) {
             const uint32_t cnt = H[b * 32 + lane];
             lane_left += cnt > a.alpha ? cnt - a.alpha : 0;
-            H[b * 32 + lane] = run;
-            A[b * 32 + lane] = run;  // bucket start, kept for the communication steps
+            H[b * 32 + lane] = run;  // bucket start
             run += cnt;
-        }
-#pragma unroll
-        for (int c = 0; c < M; ++c) {
-            if (x[c] != empty) {
-                const uint32_t pos = H[col[c] * 32 + lane];
-                H[col[c] * 32 + lane] = pos + 1;
-                B[pos * 32 + lane] = x[c];
-            }
         }
 #pragma unroll
         for (int c = 0; c < M; ++c)
             if ((uint32_t)c >= run)
                 B[c * 32 + lane] = empty;
-        __syncwarp();
-        // communication_phase permute.hpp:225-274: pass p, colour k -> one label per row
-        for (uint32_t p = 0; p < a.alpha; ++p) {
-            for (int kc = 0; kc < M; ++kc) {
-                const uint32_t pos = A[kc * 32 + lane] + p;
-                const bool send = pos < H[kc * 32 + lane];  // H now holds the bucket ends
-                if (!__any_sync(0xFFFFFFFFu, send))
-                    continue;
-                if (send) {
-                    const uint32_t label = B[pos * 32 + lane];
-                    outs[(label % M) * 32 + label / M] = label;  // distinct rows per step (colouring)
-                    B[pos * 32 + lane] = empty;
-                }
-                __syncwarp();
+        // scatter into the colour-sorted order; a label whose rank in its colour bucket is
+        // below alpha is delivered by the communication phase below
+        uint32_t rank[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+            rank[c] = 0xFFFFFFFFu;
+            if (x[c] != empty) {
+                const uint32_t pos = H[col[c] * 32 + lane];
+                H[col[c] * 32 + lane] = pos + 1;
+                B[pos * 32 + lane] = x[c];
+                rank[c] = pos;
             }
         }
-        __syncwarp();
+        // communication_phase permute.hpp:225-274.  Step (pass p, colour k): every row sends
+        // its p-th label of colour k to out[i][j]; the output region keeps row i in bank i and
+        // the colouring makes the destinations of one step distinct rows, so every step is one
+        // conflict-free warp-wide store.  H holds the bucket ends now: start = end - count.
+        for (int kc = 0; kc < M; ++kc) {
+            const uint32_t end = H[kc * 32 + lane];
+            const uint32_t start = kc == 0 ? 0u : H[(kc - 1) * 32 + lane];
+            const uint32_t take = min(end - start, a.alpha);
+            for (uint32_t p = 0; p < take; ++p) {
+                const uint32_t label = B[(start + p) * 32 + lane];
+                outs[(label % M) * 32 + label / M] = label;
+            }
+        }
+        // delivered cells become empty in place (the compacted row keeps its holes)
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+            const uint32_t pos = rank[c];
+            if (pos != 0xFFFFFFFFu) {
+                const uint32_t g = col[c];
+                const uint32_t start = g == 0 ? 0u : H[(g - 1) * 32 + lane];
+                if (pos - start < a.alpha)
+                    B[pos * 32 + lane] = empty;
+            }
+        }
 #pragma unroll
         for (int c = 0; c < M; ++c)
             x[c] = B[c * 32 + lane];
@@ -366,7 +384,7 @@ __global__ void __launch_bounds__(128) k_permute(const uint32_t* __restrict__ in
                     if (kk < give)
                         moved = pk[(load - 1 - kk) * 32 + lane];
                     __syncwarp();
-                    if (kk < give && p_cursor + kk < 2 * M)
+                    if (kk < give && p_cursor + kk < M)
                         pk[(p_cursor + kk) * 32 + partner] = moved;  // distinct partner banks
                     __syncwarp();
                 }
@@ -428,12 +446,13 @@ __global__ void __launch_bounds__(128) k_permute(const uint32_t* __restrict__ in
         for (int c = 0; c < M; ++c)
             y_keep[c] = y[c];
         uint32_t r2 = 0;
-        if (!finish_packed<M, M>(y, stage, B, outs, lane, empty, r2)) {
+        if (!finish_packed<M, M>(y, stage, B, outs, lane, empty, r2) && M < kWarp) {
             // last resort: comparison tall sort on the compacted multiset (permute.hpp:618-625).
             // The reference sorts the working window left by the failed attempt; any
             // arrangement of the same multiset sorts to the same matrix.
             using V = VF<0xFFFFFFFFu, 0, 1, kWarp, 0, M>;
-            sort_tall<1, V>(y_keep, stage, lane);
+            if constexpr (M < kWarp)
+                sort_tall<1, V>(y_keep, stage, lane);
             __syncwarp();
 #pragma unroll
             for (int c = 0; c < M; ++c)

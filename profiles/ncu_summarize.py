@@ -1,0 +1,71 @@
+"""Summarize an ncu --set full report: key raw metrics + per-source-line hot spots.
+usage: python profiles/ncu_summarize.py <report.ncu-rep> [top_n]"""
+import csv
+import io
+import subprocess
+import sys
+from collections import Counter
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
+        "derived__memory_l1_wavefronts_shared_excessive", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "smsp__inst_executed.sum", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.per_cycle_active",
+        "launch__registers_per_thread", "launch__occupancy_limit_shared_mem", "sm__cycles_elapsed.avg.per_second"]
+
+
+def main():
+    rep = sys.argv[1]
+    top = int(sys.argv[2]) if len(sys.argv) > 2 else 12
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    ix = {h: i for i, h in enumerate(hdr)}
+    print("kernel:", vals[ix["Kernel Name"]][:100])
+    for k in KEYS:
+        if k in ix:
+            print(f"  {k} = {vals[ix[k]]} {units[ix[k]]}")
+    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    srows = list(csv.reader(io.StringIO(src)))
+    h = srows[1]
+    si = {x: i for i, x in enumerate(h)}
+    ops = Counter()
+    stall = Counter()
+    for r in srows[2:]:
+        if len(r) < len(h):
+            continue
+        toks = r[si["Source"]].split()
+        if not toks:
+            continue
+        op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
+        try:
+            ops[op.split(".")[0]] += float(r[si["Instructions Executed"]] or 0)
+            stall[op.split(".")[0]] += float(r[si["Warp Stall Sampling (All Samples)"]] or 0)
+        except ValueError:
+            pass
+    tot = sum(ops.values()) or 1
+    tots = sum(stall.values()) or 1
+    print("  instruction mix (executed %, stall-sample %):")
+    for k, v in ops.most_common(top):
+        print(f"    {k:10s} {100 * v / tot:5.1f}%  {100 * stall[k] / tots:5.1f}%")
+    reasons = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
+    agg = Counter()
+    for r in srows[2:]:
+        if len(r) < len(h):
+            continue
+        for c in reasons:
+            try:
+                agg[c] += float(r[si[c]] or 0)
+            except ValueError:
+                pass
+    tr = sum(agg.values()) or 1
+    print("  stall reasons:", ", ".join(f"{k[6:]} {100 * v / tr:.0f}%" for k, v in agg.most_common(6)))
+
+
+if __name__ == "__main__":
+    main()
