@@ -1,0 +1,241 @@
+// dmm_b200.hpp -- header-only C++ drop-in for the reference's hot path.
+//
+// Same names, argument meaning and error behaviour as /root/reference/proj/include/dmm/
+// (namespace dmm::b200 instead of dmm): a reference user keeps their Machine / MatrixView /
+// Rng objects and calls
+//
+//     dmm::b200::partition_general(view)            // partition.hpp:453
+//     dmm::b200::integer_sort_general(view, domain)  // partition.hpp:436
+//     dmm::b200::sort_tall(view)                     // sort.hpp:352
+//     dmm::b200::transpose_square(view)              // layout.hpp:24 (+ to_column_major / to_row_major)
+//     dmm::b200::permute(machine, rng, params)       // permute.hpp:545
+//
+// Each call gathers the view's cells (peek), runs the sm_100a kernel through the C ABI
+// (include/dmm_gpu.h) on a batch of one, writes the result back (poke) and rethrows the
+// reference's exception type for a non-OK status.  permute() continues the caller's
+// std::mt19937_64 from its exact state and advances it by report.random_words draws, so
+// host code after the call sees the same stream as with the reference.
+//
+// Not reproduced (GPU kernels have no DMM step meter): Machine::steps()/work() do not
+// advance; PartitionProbe hooks and traces are unsupported (Error); permute() reproduces
+// the output region, the report and the Rng position, not the scratch/counter cells.
+// Words must fit in 32 bits (KeyOutOfRange otherwise).  Requires <dmm/dmm.hpp>.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include <dmm/dmm.hpp>
+
+#include "dmm_gpu.h"
+
+namespace dmm {
+namespace b200 {
+
+[[noreturn]] inline void raise(dmm_status s, const std::string& where) {
+    const std::string msg = where + " (B200): " + dmm_last_error();
+    switch (s) {
+        case DMM_SHAPE_VIOLATION: throw ShapeViolation(msg);
+        case DMM_INVALID_INSTANCE: throw InvalidInstance(msg);
+        case DMM_KEY_OUT_OF_RANGE: throw KeyOutOfRange(msg);
+        case DMM_DIVISIBILITY_VIOLATION: throw DivisibilityViolation(msg);
+        case DMM_POSTCONDITION_FAILED: throw PostconditionFailed(msg);
+        case DMM_PACKING_OVERFLOW: throw PackingOverflow(msg);
+        case DMM_CAPACITY_EXCEEDED: throw CapacityExceeded(msg);
+        case DMM_NOT_SQUARE: throw NotSquare(msg);
+        case DMM_OUT_OF_BOUNDS: throw OutOfBounds(msg);
+        case DMM_OVERLAPPING_VIEWS: throw OverlappingViews(msg);
+        default: throw Error(msg);
+    }
+}
+
+inline void check(dmm_status s, const char* where) {
+    if (s != DMM_OK)
+        raise(s, where);
+}
+
+inline void cuda_check(cudaError_t e, const char* where) {
+    if (e != cudaSuccess)
+        throw Error(std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// RAII device buffer
+struct DeviceBuffer {
+    void* ptr = nullptr;
+    explicit DeviceBuffer(std::size_t bytes) { cuda_check(cudaMalloc(&ptr, bytes ? bytes : 16), "cudaMalloc"); }
+    ~DeviceBuffer() { cudaFree(ptr); }
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    template <class T>
+    T* as() const { return static_cast<T*>(ptr); }
+};
+
+template <class T>
+inline void to_device(DeviceBuffer& d, const std::vector<T>& h) {
+    cuda_check(cudaMemcpy(d.ptr, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice), "H2D");
+}
+template <class T>
+inline void to_host(std::vector<T>& h, const DeviceBuffer& d) {
+    cuda_check(cudaMemcpy(h.data(), d.ptr, sizeof(T) * h.size(), cudaMemcpyDeviceToHost), "D2H");
+}
+
+// view window -> row-major 32-bit grid (the narrowing of SURVEY 8(b))
+inline std::vector<uint32_t> gather(const MatrixView& v) {
+    std::vector<uint32_t> g(u64(v.W()) * v.M());
+    for (u32 r = 0; r < v.W(); ++r)
+        for (u32 c = 0; c < v.M(); ++c) {
+            const word x = v.machine().peek(v.bank(r), v.off(c));
+            if (x >> 32)
+                throw KeyOutOfRange("B200 kernels take 32-bit words");
+            g[u64(r) * v.M() + c] = static_cast<uint32_t>(x);
+        }
+    return g;
+}
+inline void scatter(const MatrixView& v, const std::vector<uint32_t>& g) {
+    for (u32 r = 0; r < v.W(); ++r)
+        for (u32 c = 0; c < v.M(); ++c)
+            v.machine().poke(v.bank(r), v.off(c), g[u64(r) * v.M() + c]);
+}
+
+inline void no_probe(const PartitionProbe* probe) {
+    if (probe && (probe->after_balance || probe->after_divide))
+        throw Error("PartitionProbe hooks are not supported by the B200 kernels");
+}
+
+inline GeneralStats general_impl(bool partition, const MatrixView& v, u64 domain, bool enforce,
+                                 const PartitionProbe* probe) {
+    no_probe(probe);
+    std::vector<uint32_t> g = gather(v);
+    const uint64_t bytes = sizeof(uint32_t) * g.size();
+    DeviceBuffer d(bytes), st(sizeof(dmm_general_stats)), ss(16);
+    to_device(d, g);
+    uint32_t flags = 0;
+    if (!v.machine().config().strict)
+        flags |= DMM_FLAG_NONSTRICT;
+    if (!enforce)
+        flags |= DMM_FLAG_NO_ENFORCE_PRE;
+    const dmm_status s =
+        partition ? dmm_partition_general(d.as<uint32_t>(), d.as<uint32_t>(), v.W(), v.M(), 1, flags,
+                                          st.as<dmm_general_stats>(), ss.as<uint8_t>(), nullptr)
+                  : dmm_integer_sort_general(d.as<uint32_t>(), d.as<uint32_t>(), v.W(), v.M(), 1, domain, flags,
+                                             st.as<dmm_general_stats>(), ss.as<uint8_t>(), nullptr);
+    check(s, partition ? "partition_general" : "integer_sort_general");
+    dmm_general_stats hs{};
+    uint8_t status = 0;
+    cuda_check(cudaMemcpy(&hs, st.ptr, sizeof(hs), cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(&status, ss.ptr, 1, cudaMemcpyDeviceToHost), "D2H");
+    if (status != DMM_OK)
+        raise(static_cast<dmm_status>(status), partition ? "partition_general" : "integer_sort_general");
+    to_host(g, d);
+    scatter(v, g);
+    GeneralStats out;
+    out.cleanup_retries = hs.cleanup_retries;
+    out.sorted = hs.sorted != 0;
+    return out;
+}
+
+/// GeneralStats partition_general(const MatrixView&)  partition.hpp:453-456
+inline GeneralStats partition_general(const MatrixView& v, const PartitionProbe* probe = nullptr) {
+    return general_impl(true, v, v.W(), true, probe);
+}
+
+/// GeneralStats integer_sort_general(view, domain, probe, enforce)  partition.hpp:436-449
+inline GeneralStats integer_sort_general(const MatrixView& v, u64 domain, const PartitionProbe* probe = nullptr,
+                                         bool enforce_analysis_pre = true) {
+    return general_impl(false, v, domain, enforce_analysis_pre, probe);
+}
+
+namespace detail {
+template <class Fn>
+inline void simple(const MatrixView& v, Fn&& fn, const char* where) {
+    std::vector<uint32_t> g = gather(v);
+    DeviceBuffer d(sizeof(uint32_t) * g.size());
+    to_device(d, g);
+    check(fn(d.as<uint32_t>()), where);
+    to_host(g, d);
+    scatter(v, g);
+}
+}  // namespace detail
+
+/// void sort_tall(const MatrixView&)  sort.hpp:352-374
+inline void sort_tall(const MatrixView& v) {
+    detail::simple(v, [&](uint32_t* p) { return dmm_sort_tall(p, p, v.W(), v.M(), 1, nullptr); }, "sort_tall");
+}
+/// transpose_square layout.hpp:24-61
+inline void transpose_square(const MatrixView& v) {
+    if (v.W() != v.M())
+        throw NotSquare("transpose_square needs a square view");
+    detail::simple(v, [&](uint32_t* p) { return dmm_transpose_square(p, p, v.W(), 1, nullptr); },
+                   "transpose_square");
+}
+/// to_column_major layout.hpp:397-399
+inline void to_column_major(const MatrixView& v) {
+    detail::simple(v, [&](uint32_t* p) { return dmm_to_column_major(p, p, v.W(), v.M(), 1, nullptr); },
+                   "to_column_major");
+}
+/// to_row_major layout.hpp:403-405
+inline void to_row_major(const MatrixView& v) {
+    detail::simple(v, [&](uint32_t* p) { return dmm_to_row_major(p, p, v.W(), v.M(), 1, nullptr); },
+                   "to_row_major");
+}
+
+/// PermuteReport permute(Machine&, Rng&, const PermuteParams&)  permute.hpp:545-628
+inline PermuteReport permute(Machine& mach, Rng& rng, const PermuteParams& params = {}) {
+    const u32 w = mach.w(), m = mach.m();
+    // the caller's engine, mid-stream: libstdc++ prints _M_x[0..312) then _M_p
+    std::vector<uint64_t> state(313);
+    {
+        std::ostringstream os;
+        os << rng;
+        std::istringstream is(os.str());
+        for (auto& s : state)
+            if (!(is >> s))
+                throw Error("cannot serialize the Rng state");
+    }
+    std::vector<uint32_t> g(u64(w) * m);
+    for (u32 r = 0; r < w; ++r)
+        for (u32 c = 0; c < m; ++c) {
+            const word x = mach.peek(r, mach.config().work_base() + c);
+            if (x >> 32)
+                throw KeyOutOfRange("B200 kernels take 32-bit words");
+            g[u64(r) * m + c] = static_cast<uint32_t>(x);
+        }
+    DeviceBuffer din(sizeof(uint32_t) * g.size()), dout(sizeof(uint32_t) * g.size()),
+        dst(sizeof(uint64_t) * state.size()), drep(sizeof(dmm_permute_report)),
+        dhist(sizeof(uint64_t) * DMM_PERMUTE_MAX_HIST), dsh(sizeof(uint32_t) * w), dss(16);
+    to_device(din, g);
+    to_device(dst, state);
+    check(dmm_permute_from_state(din.as<uint32_t>(), dout.as<uint32_t>(), w, m, 1, dst.as<uint64_t>(), params.alpha,
+                                 params.iter_cap, drep.as<dmm_permute_report>(), dhist.as<uint64_t>(),
+                                 dsh.as<uint32_t>(), dss.as<uint8_t>(), nullptr),
+          "permute");
+    dmm_permute_report hr{};
+    std::vector<uint64_t> hist(DMM_PERMUTE_MAX_HIST);
+    std::vector<uint32_t> shifts(w);
+    cuda_check(cudaMemcpy(&hr, drep.ptr, sizeof(hr), cudaMemcpyDeviceToHost), "D2H");
+    to_host(hist, dhist);
+    to_host(shifts, dsh);
+    to_host(g, dout);
+    for (u32 i = 0; i < w; ++i)
+        for (u32 j = 0; j < m; ++j)
+            mach.poke(i, mach.config().out_base() + j, g[u64(i) * m + j]);
+    rng.discard(hr.random_words);
+    PermuteReport rep;
+    rep.iterations = hr.iterations;
+    rep.fallback = hr.fallback != 0;
+    rep.used_packing = hr.used_packing != 0;
+    rep.packed_width = hr.packed_width;
+    rep.threshold = hr.threshold;
+    rep.random_words = hr.random_words;
+    rep.cleanup_retries = hr.cleanup_retries;
+    rep.leftover_history.assign(hist.begin(), hist.begin() + hr.n_hist);
+    rep.shifts = shifts;
+    return rep;
+}
+
+}  // namespace b200
+}  // namespace dmm

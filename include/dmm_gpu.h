@@ -121,6 +121,15 @@ dmm_status dmm_sort_rows(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t
  * (std::mt19937_64).  reports: count entries; history: count x DMM_PERMUTE_MAX_HIST;
  * shifts: count x w (each may be NULL).  workspace: dmm_permute_workspace_bytes(count). */
 uint64_t dmm_permute_workspace_bytes(uint32_t w, uint32_t m, uint64_t count);
+/* Same pipeline, each instance's generator given mid-stream instead of by seed:
+ * rng_states[k] = 313 words (device memory): the std::mt19937_64 state words _M_x[0..312)
+ * and the position _M_p of the next draw (libstdc++ layout; what `os << rng` prints).
+ * This is what a drop-in for permute(Machine&, Rng&, params) needs: the caller's engine is
+ * continued, then advanced by report.random_words (rng.discard). */
+dmm_status dmm_permute_from_state(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                  const uint64_t* rng_states, uint32_t alpha, uint32_t iter_cap,
+                                  dmm_permute_report* reports, uint64_t* history, uint32_t* shifts,
+                                  uint8_t* status, void* stream);
 dmm_status dmm_permute(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
                        const uint64_t* seeds, uint32_t alpha, uint32_t iter_cap, dmm_permute_report* reports,
                        uint64_t* history, uint32_t* shifts, uint8_t* status, void* workspace, void* stream);

@@ -43,6 +43,7 @@ SIGNATURES = {
     "dmm_sort_rows": (_int, [_vp, _vp, _u32, _u32, _u64, _int, _u64, _vp, _vp]),
     "dmm_permute_workspace_bytes": (_u64, [_u32, _u32, _u64]),
     "dmm_permute": (_int, [_vp, _vp, _u32, _u32, _u64, _vp, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "dmm_permute_from_state": (_int, [_vp, _vp, _u32, _u32, _u64, _vp, _u32, _u32, _vp, _vp, _vp, _vp, _vp]),
 }
 
 

@@ -40,7 +40,7 @@ constexpr int kRngWords = 312;
 struct WarpRng {
     uint32_t* lo;
     uint32_t* hi;
-    uint32_t base;
+    int64_t base;
 
     __device__ uint64_t get(int i) const { return ((uint64_t)hi[i] << 32) | lo[i]; }
     __device__ void put(int i, uint64_t v) {
@@ -104,14 +104,28 @@ struct WarpRng {
         }
         __syncwarp();
     }
+    // load an engine mid-stream: the 312 state words and the position p of the next draw
+    // (libstdc++'s mersenne_twister_engine layout _M_x[], _M_p): draw d reads word p + d
+    __device__ void load(const uint64_t* state, int lane) {
+        for (int i = lane; i < kRngWords; i += 32)
+            put(i, state[i]);
+        const uint64_t p = state[kRngWords];
+        __syncwarp();
+        if (p >= (uint64_t)kRngWords) {
+            twist(lane);
+            base = 0;
+        } else {
+            base = -(int64_t)p;
+        }
+    }
     // make draw d (warp-uniform) addressable; advances generations as needed
     __device__ void advance_to(uint32_t d, int lane) {
-        while (d >= base + kRngWords) {
+        while ((int64_t)d >= base + kRngWords) {
             twist(lane);
             base += kRngWords;
         }
     }
-    __device__ uint64_t word(uint32_t d) const { return mt_temper(get(d - base)); }
+    __device__ uint64_t word(uint32_t d) const { return mt_temper(get((int)((int64_t)d - base))); }
 };
 
 __device__ __forceinline__ uint32_t hash_eval(uint64_t key, uint32_t m, uint32_t i) {  // HashOracle permute.hpp:39
@@ -205,7 +219,8 @@ __host__ __device__ constexpr int perm_warp_words() {  // u32 words of smem per 
 
 template <int M>
 __global__ void __launch_bounds__(128) k_permute(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
-                                                 uint64_t count, const uint64_t* __restrict__ seeds, PermArgs a,
+                                                 uint64_t count, const uint64_t* __restrict__ seeds,
+                                                 const uint64_t* __restrict__ states, PermArgs a,
                                                  dmm_permute_report* __restrict__ reps, uint64_t* __restrict__ hist,
                                                  uint32_t* __restrict__ shifts_out, uint8_t* __restrict__ status) {
     extern __shared__ uint64_t smem64[];
@@ -234,7 +249,10 @@ __global__ void __launch_bounds__(128) k_permute(const uint32_t* __restrict__ in
         outs[c * 32 + lane] = 0xFFFFFFFFu;  // sentinel: undelivered
     }
     badkey = __reduce_or_sync(0xFFFFFFFFu, badkey);
-    rng.seed(seeds[k], lane);
+    if (states)
+        rng.load(states + k * (kRngWords + 1), lane);
+    else
+        rng.seed(seeds[k], lane);
 
     uint64_t random_words = 0;
     uint32_t drawn = 0;
@@ -507,7 +525,7 @@ uint64_t permute_threshold(uint32_t w, uint32_t m) {  // permute.hpp:97-101
 
 template <int M>
 dmm_status launch_permute(const uint32_t* in, uint32_t* out, uint64_t count, const uint64_t* seeds,
-                          const dmmdev::PermArgs& a, dmm_permute_report* reps, uint64_t* hist, uint32_t* shifts,
+                          const uint64_t* states, const dmmdev::PermArgs& a, dmm_permute_report* reps, uint64_t* hist, uint32_t* shifts,
                           uint8_t* status, cudaStream_t s) {
     constexpr int kWarps = 4;
     auto kern = dmmdev::k_permute<M>;
@@ -520,7 +538,7 @@ dmm_status launch_permute(const uint32_t* in, uint32_t* out, uint64_t count, con
         configured = true;
     }
     const uint64_t blocks = (count + kWarps - 1) / kWarps;
-    kern<<<unsigned(blocks), kWarps * 32, smem, s>>>(in, out, count, seeds, a, reps, hist, shifts, status);
+    kern<<<unsigned(blocks), kWarps * 32, smem, s>>>(in, out, count, seeds, states, a, reps, hist, shifts, status);
     return check_launch("k_permute");
 }
 
@@ -535,8 +553,12 @@ uint64_t dmm_permute_workspace_bytes(uint32_t w, uint32_t m, uint64_t count) {
     return 0;  // the generator state lives in shared memory
 }
 
-dmm_status dmm_permute(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
-                       const uint64_t* seeds, uint32_t alpha, uint32_t iter_cap, dmm_permute_report* reports,
+}  // extern "C"
+
+using namespace dmmhost;
+
+static dmm_status permute_impl(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                       const uint64_t* seeds, const uint64_t* states, uint32_t alpha, uint32_t iter_cap, dmm_permute_report* reports,
                        uint64_t* history, uint32_t* shifts, uint8_t* status, void* workspace, void* stream) {
     reset_launches();
     (void)workspace;
@@ -546,7 +568,7 @@ dmm_status dmm_permute(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m
         return DMM_SHAPE_VIOLATION;
     if (count == 0)
         return DMM_OK;
-    if (!in || !out || !seeds)
+    if (!in || !out || (!seeds && !states))
         return DMM_INVALID_ARGUMENT;
     if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u) {
         set_error("in/out must be 16-byte aligned");
@@ -575,14 +597,32 @@ dmm_status dmm_permute(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m
     }
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     switch (m) {
-        case 2: return launch_permute<2>(in, out, count, seeds, a, reports, history, shifts, status, s);
-        case 4: return launch_permute<4>(in, out, count, seeds, a, reports, history, shifts, status, s);
-        case 16: return launch_permute<16>(in, out, count, seeds, a, reports, history, shifts, status, s);
-        case 32: return launch_permute<32>(in, out, count, seeds, a, reports, history, shifts, status, s);
+        case 2: return launch_permute<2>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
+        case 4: return launch_permute<4>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
+        case 16: return launch_permute<16>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
+        case 32: return launch_permute<32>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
         default: break;
     }
     set_error("no permute kernel compiled for this shape");
     return DMM_UNSUPPORTED_SHAPE;
+}
+
+
+extern "C" {
+
+dmm_status dmm_permute(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                       const uint64_t* seeds, uint32_t alpha, uint32_t iter_cap, dmm_permute_report* reports,
+                       uint64_t* history, uint32_t* shifts, uint8_t* status, void* workspace, void* stream) {
+    return permute_impl(in, out, w, m, count, seeds, nullptr, alpha, iter_cap, reports, history, shifts, status,
+                        workspace, stream);
+}
+
+dmm_status dmm_permute_from_state(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                  const uint64_t* rng_states, uint32_t alpha, uint32_t iter_cap,
+                                  dmm_permute_report* reports, uint64_t* history, uint32_t* shifts, uint8_t* status,
+                                  void* stream) {
+    return permute_impl(in, out, w, m, count, nullptr, rng_states, alpha, iter_cap, reports, history, shifts, status,
+                        nullptr, stream);
 }
 
 }  // extern "C"

@@ -1,0 +1,201 @@
+// test_shim.cpp -- the reference's own API, run side by side on the CPU reference (dmm::)
+// and on the B200 drop-in (dmm::b200::), in one process.  Built by tests/cpp/Makefile where
+// /root/reference exists; run by tests/test_gpu_shim.py on the GPU box.  Cases follow the
+// reference's tests (test_partition.cpp, test_permute.cpp, test_layout.cpp, test_sort.cpp).
+#include <cstdio>
+#include <cstdlib>
+#include <functional>
+
+#include "dmm_b200.hpp"
+
+using namespace dmm;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                        \
+    do {                                                                   \
+        if (cond) {                                                        \
+            ++g_pass;                                                      \
+        } else {                                                           \
+            ++g_fail;                                                      \
+            std::fprintf(stderr, "FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond); \
+        }                                                                  \
+    } while (0)
+
+template <class E, class F>
+static bool throws_as(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+static Machine make_machine(u32 w, u32 m) { return Machine(MachineConfig::standard(w, m)); }
+
+static void partition_cases() {
+    for (u32 m : {16u, 32u, 64u}) {
+        for (u64 seed = 1; seed <= 6; ++seed) {
+            Instance in = gen_instance(InstanceKind::partition, 32, m, seed);
+            Machine a = make_machine(32, m), b = make_machine(32, m);
+            MatrixView va = MatrixView::full(a), vb = MatrixView::full(b);
+            va.load(in.grid);
+            vb.load(in.grid);
+            GeneralStats sa = partition_general(va);
+            GeneralStats sb = b200::partition_general(vb);
+            CHECK(va.snapshot() == vb.snapshot());
+            CHECK(sa.cleanup_retries == sb.cleanup_retries && sa.sorted == sb.sorted);
+            CHECK(verify_partition_result(in, vb.snapshot()));
+        }
+    }
+    // shape violations raise the same type (partition.hpp:241-244, 443-445)
+    {
+        Instance in = gen_instance(InstanceKind::partition, 32, 8, 1);
+        Machine b = make_machine(32, 8);
+        MatrixView vb = MatrixView::full(b);
+        vb.load(in.grid);
+        CHECK(throws_as<ShapeViolation>([&] { b200::partition_general(vb); }));
+        Machine a = make_machine(32, 8);
+        MatrixView va = MatrixView::full(a);
+        va.load(in.grid);
+        CHECK(throws_as<ShapeViolation>([&] { partition_general(va); }));
+    }
+    // invalid instance (test_partition.cpp:110-115)
+    {
+        Instance in = gen_instance(InstanceKind::partition, 32, 16, 2);
+        in.grid[0] = in.grid[0] == 3 ? 4 : 3;
+        Machine b = make_machine(32, 16);
+        MatrixView vb = MatrixView::full(b);
+        vb.load(in.grid);
+        CHECK(throws_as<InvalidInstance>([&] { b200::partition_general(vb); }));
+    }
+    // view transparency (test_sort.cpp:388-409): a 32-row view of a 64-row machine
+    {
+        Instance in = gen_instance(InstanceKind::partition, 32, 32, 9);
+        Machine a = make_machine(64, 32), b = make_machine(64, 32);
+        std::vector<u32> rows;
+        for (u32 r = 0; r < 32; ++r)
+            rows.push_back(2 * r + 1);  // odd banks
+        MatrixView va = make_view(a, rows, 0, 32), vb = make_view(b, rows, 0, 32);
+        va.load(in.grid);
+        vb.load(in.grid);
+        partition_general(va);
+        b200::partition_general(vb);
+        CHECK(va.snapshot() == vb.snapshot());
+    }
+}
+
+static void integer_sort_cases() {
+    for (u32 m : {16u, 32u, 128u}) {
+        Instance in = gen_instance(InstanceKind::permute, 32, m, 5);
+        Machine a = make_machine(32, m), b = make_machine(32, m);
+        MatrixView va = MatrixView::full(a), vb = MatrixView::full(b);
+        va.load(in.grid);
+        vb.load(in.grid);
+        GeneralStats sa = integer_sort_general(va, u64(32) * m);
+        GeneralStats sb = b200::integer_sort_general(vb, u64(32) * m);
+        CHECK(va.snapshot() == vb.snapshot());
+        CHECK(sa.cleanup_retries == sb.cleanup_retries);
+    }
+    {  // uint32 keys, domain 2^32 (cfg3 path)
+        Rng rng(77);
+        std::vector<word> g(32 * 128);
+        for (auto& x : g)
+            x = rng() >> 32;
+        Machine a = make_machine(32, 128), b = make_machine(32, 128);
+        MatrixView va = MatrixView::full(a), vb = MatrixView::full(b);
+        va.load(g);
+        vb.load(g);
+        integer_sort_general(va, u64(1) << 32);
+        b200::integer_sort_general(vb, u64(1) << 32);
+        CHECK(va.snapshot() == vb.snapshot());
+    }
+    {  // key outside the domain (test_partition.cpp:57-61)
+        Instance in = gen_instance(InstanceKind::permute, 32, 16, 5);
+        in.grid[7] = 9999;
+        Machine b = make_machine(32, 16);
+        MatrixView vb = MatrixView::full(b);
+        vb.load(in.grid);
+        CHECK(throws_as<KeyOutOfRange>([&] { b200::integer_sort_general(vb, 512); }));
+    }
+}
+
+static void layout_and_sort_cases() {
+    Rng rng(11);
+    for (u32 m : {8u, 16u, 32u}) {
+        std::vector<word> g(32 * m);
+        for (auto& x : g)
+            x = rng() >> 40;
+        Machine a = make_machine(32, m), b = make_machine(32, m);
+        MatrixView va = MatrixView::full(a), vb = MatrixView::full(b);
+        va.load(g);
+        vb.load(g);
+        to_column_major(va);
+        b200::to_column_major(vb);
+        CHECK(va.snapshot() == vb.snapshot());
+        to_row_major(va);
+        b200::to_row_major(vb);
+        CHECK(va.snapshot() == vb.snapshot() && vb.snapshot() == g);
+        sort_tall(va);
+        b200::sort_tall(vb);
+        CHECK(va.snapshot() == vb.snapshot());
+    }
+    {
+        std::vector<word> g(32 * 32);
+        for (auto& x : g)
+            x = rng() >> 40;
+        Machine a = make_machine(32, 32), b = make_machine(32, 32);
+        MatrixView va = MatrixView::full(a), vb = MatrixView::full(b);
+        va.load(g);
+        vb.load(g);
+        transpose_square(va);
+        b200::transpose_square(vb);
+        CHECK(va.snapshot() == vb.snapshot());
+    }
+}
+
+static void permute_cases() {
+    for (u32 m : {32u, 16u, 4u, 2u}) {
+        for (u64 seed = 1; seed <= 6; ++seed) {
+            Instance in = gen_instance(InstanceKind::permute, 32, m, seed);
+            Machine a = make_machine(32, m), b = make_machine(32, m);
+            MatrixView va = MatrixView::make(a, [] { std::vector<u32> r(32); for (u32 i = 0; i < 32; ++i) r[i] = i; return r; }(),
+                                             0, m, 2 * m, 3 * m);
+            MatrixView vb = MatrixView::make(b, va.rows(), 0, m, 2 * m, 3 * m);
+            va.load(in.grid);
+            vb.load(in.grid);
+            Rng ra(seed), rb(seed);
+            // a caller that already consumed some draws: the drop-in must continue the stream
+            for (u64 i = 0; i < seed; ++i) {
+                ra();
+                rb();
+            }
+            PermuteReport pa = permute(a, ra);
+            PermuteReport pb = b200::permute(b, rb);
+            CHECK(permute_output_correct(b));
+            CHECK(pa.iterations == pb.iterations && pa.fallback == pb.fallback);
+            CHECK(pa.used_packing == pb.used_packing && pa.packed_width == pb.packed_width);
+            CHECK(pa.threshold == pb.threshold && pa.random_words == pb.random_words);
+            CHECK(pa.cleanup_retries == pb.cleanup_retries);
+            CHECK(pa.leftover_history == pb.leftover_history && pa.shifts == pb.shifts);
+            CHECK(ra() == rb());  // the caller's Rng continues identically
+            for (u32 i = 0; i < 32; ++i)
+                for (u32 j = 0; j < m; ++j)
+                    CHECK(a.peek(i, m + j) == b.peek(i, m + j));
+        }
+    }
+    Machine bad = make_machine(32, 8);
+    Rng r(1);
+    CHECK(throws_as<ShapeViolation>([&] { b200::permute(bad, r); }));
+}
+
+int main() {
+    partition_cases();
+    integer_sort_cases();
+    layout_and_sort_cases();
+    permute_cases();
+    std::printf("shim parity: %d passed, %d failed\n", g_pass, g_fail);
+    return g_fail ? 1 : 0;
+}
