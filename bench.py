@@ -37,6 +37,9 @@ CONFIGS = {
               "general w-way partition w=32, n=512 (reference-accepted stand-in of cfg2), 2^17 instances"),
     "cfg3": ("integer_sort_general", 32, 128, 1 << 20, 0,
              "bank-conflict-free sort w=32, n=4096 uint32 keys per block-tile (32x128), 2^20 tiles"),
+    "cfg5": ("global_partition", 1, 1 << 26, 8, 0,
+             "global 8-way partition of 2^32 uint32 keys across 8 GPUs: 2^29 keys per GPU (label = key >> 29), "
+             "local stable multisplit + NCCL all-to-all"),
     "cfg4": ("permute", 32, 32, 1 << 18, 0,
              "randomized permutation w=32, n=1024 per instance (32x32: the reference rejects n=8192 at w=32), "
              "seeded Rng per instance, 2^18 instances"),
@@ -184,10 +187,14 @@ def main():
         count = args.count
         desc += f" [count overridden: {count}]"
     keys_per_gpu = count * w * m
-    kind = {"partition_general": dmm.KIND_PARTITION, "integer_sort_general": dmm.KIND_SORT_U32,
-            "permute": dmm.KIND_PERMUTE}[alg]
-    # rank r owns instances [r*count, (r+1)*count): seeds are disjoint across ranks
-    g = dmm.gen_instances(kind, w, m, 1 + rank * count, count)
+    if alg == "global_partition":
+        # 2^29 keys per GPU viewed as `count` x w x m; keys are splitmix64(global index) >> 32
+        g = dmm.gen_keys(rank * keys_per_gpu, keys_per_gpu).view(count, w, m)
+    else:
+        kind = {"partition_general": dmm.KIND_PARTITION, "integer_sort_general": dmm.KIND_SORT_U32,
+                "permute": dmm.KIND_PERMUTE}[alg]
+        # rank r owns instances [r*count, (r+1)*count): seeds are disjoint across ranks
+        g = dmm.gen_instances(kind, w, m, 1 + rank * count, count)
     out = torch.empty_like(g)
     stream = torch.cuda.current_stream()
 
@@ -199,6 +206,10 @@ def main():
             return dmm.partition_general(src, flags=flags, out=dst, check=False)
         if alg == "permute":
             return dmm.permute_into(src, dst, seeds, perm_bufs)
+        if alg == "global_partition":
+            from paper_1507_01391_b200.distributed import global_partition
+            res, _ = global_partition(src.view(-1))
+            return res, None
         return dmm.integer_sort_general(src, 1 << 32, out=dst, check=False)
 
     for _ in range(args.warmup):
@@ -233,6 +244,10 @@ def main():
     elif alg == "permute":
         exp = torch.arange(w * m, device="cuda", dtype=torch.int32).view(1, w, m)
         ok = bool((out == exp).all())
+    elif alg == "global_partition":
+        res, _ = step(g, out)
+        lab = (res.to(torch.int64) & 0xFFFFFFFF) >> 29
+        ok = bool((lab[1:] >= lab[:-1]).all()) and res.numel() == keys_per_gpu
     else:
         ok = bool((out.view(count, -1)[:, 1:].to(torch.int64) & 0xFFFFFFFF >=
                    out.view(count, -1)[:, :-1].to(torch.int64) & 0xFFFFFFFF).all())

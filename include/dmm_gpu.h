@@ -72,6 +72,9 @@ uint32_t dmm_last_launch_count(void);
 dmm_status dmm_gen_instances(int kind, uint32_t w, uint32_t m, uint64_t seed0, uint64_t count, uint32_t* out,
                              void* stream);
 
+/* cfg5's flat keys (builder-defined counter generator): out[i] = splitmix64(index0 + i) >> 32 */
+dmm_status dmm_gen_keys(uint64_t index0, uint64_t n, uint32_t* out, void* stream);
+
 /* ---- partition / integer sort ------------------------------------------ */
 /* GeneralStats partition_general(const MatrixView&)           partition.hpp:453-456
  * Labels in [0, w), m copies each; after the call row i holds the labels i. */
@@ -133,6 +136,15 @@ dmm_status dmm_permute_from_state(const uint32_t* in, uint32_t* out, uint32_t w,
 dmm_status dmm_permute(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
                        const uint64_t* seeds, uint32_t alpha, uint32_t iter_cap, dmm_permute_report* reports,
                        uint64_t* history, uint32_t* shifts, uint8_t* status, void* workspace, void* stream);
+
+/* ---- cfg5: local step of the global w-way partition across GPUs --------------- */
+/* Stable partition of n keys by label = (key >> shift) & (nbuckets-1), bucket-major into
+ * out; bucket_starts[b] (device, nbuckets entries) = first output index of bucket b.
+ * The exchange of bucket j to the GPU owning label j is an NCCL all-to-all
+ * (paper_1507_01391_b200/distributed.py).  workspace: dmm_multisplit_workspace_bytes. */
+uint64_t dmm_multisplit_workspace_bytes(uint64_t n, uint32_t nbuckets);
+dmm_status dmm_multisplit(const uint32_t* keys, uint64_t n, uint32_t shift, uint32_t nbuckets, uint32_t* out,
+                          uint64_t* bucket_starts, void* workspace, void* stream);
 
 #ifdef __cplusplus
 }

@@ -29,6 +29,7 @@ SIGNATURES = {
     "dmm_supported": (_int, [C.c_char_p, _u32, _u32]),
     "dmm_last_launch_count": (_u32, []),
     "dmm_gen_instances": (_int, [_int, _u32, _u32, _u64, _u64, _vp, _vp]),
+    "dmm_gen_keys": (_int, [_u64, _u64, _vp, _vp]),
     "dmm_partition_general": (_int, [_vp, _vp, _u32, _u32, _u64, _u32, _vp, _vp, _vp]),
     "dmm_integer_sort_general": (_int, [_vp, _vp, _u32, _u32, _u64, _u64, _u32, _vp, _vp, _vp]),
     "dmm_partition_square": (_int, [_vp, _vp, _u32, _u32, _u64, _vp, _vp]),
@@ -43,6 +44,8 @@ SIGNATURES = {
     "dmm_sort_rows": (_int, [_vp, _vp, _u32, _u32, _u64, _int, _u64, _vp, _vp]),
     "dmm_permute_workspace_bytes": (_u64, [_u32, _u32, _u64]),
     "dmm_permute": (_int, [_vp, _vp, _u32, _u32, _u64, _vp, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "dmm_multisplit_workspace_bytes": (_u64, [_u64, _u32]),
+    "dmm_multisplit": (_int, [_vp, _u64, _u32, _u32, _vp, _vp, _vp, _vp]),
     "dmm_permute_from_state": (_int, [_vp, _vp, _u32, _u32, _u64, _vp, _u32, _u32, _vp, _vp, _vp, _vp, _vp]),
 }
 

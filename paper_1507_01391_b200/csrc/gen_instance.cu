@@ -44,7 +44,24 @@ __global__ void k_gen_instances(int kind, uint32_t w, uint32_t m, uint64_t seed0
         dst[i] = g[i];
 }
 
+// cfg5 keys (builder-defined counter generator): key_i = splitmix64(i) >> 32
+__global__ void k_gen_keys(uint64_t index0, uint64_t n, uint32_t* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = (uint32_t)(splitmix64(index0 + i) >> 32);
+}
+
 }  // namespace dmmdev
+
+extern "C" dmm_status dmm_gen_keys(uint64_t index0, uint64_t n, uint32_t* out, void* stream) {
+    dmmhost::reset_launches();
+    if (n == 0)
+        return DMM_OK;
+    if (!out)
+        return DMM_INVALID_ARGUMENT;
+    dmmdev::k_gen_keys<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(index0, n, out);
+    return dmmhost::check_launch("k_gen_keys");
+}
 
 extern "C" dmm_status dmm_gen_instances(int kind, uint32_t w, uint32_t m, uint64_t seed0, uint64_t count,
                                         uint32_t* out, void* stream) {

@@ -187,6 +187,13 @@ def gen_instances(kind: int, w: int, m: int, seed0: int, count: int, stream=None
     return out
 
 
+def gen_keys(index0: int, n: int, stream=None) -> torch.Tensor:
+    """cfg5 keys: splitmix64(index0 + i) >> 32 for i < n (uint32 bits in an int32 tensor)."""
+    out = torch.empty((n,), dtype=torch.int32, device="cuda")
+    _check(lib().dmm_gen_keys(index0, n, out.data_ptr(), _stream(stream)), "gen_keys")
+    return out
+
+
 # --------------------------------------------------------------------------------------
 # Partition / integer sort (partition.hpp:436-456)
 # --------------------------------------------------------------------------------------
@@ -390,6 +397,21 @@ def permute_into(src: torch.Tensor, dst: torch.Tensor, seeds, bufs: dict, alpha:
                              bufs["reps"].data_ptr(), bufs["hist"].data_ptr(), bufs["shifts"].data_ptr(),
                              bufs["status"].data_ptr(), None, _stream(stream)), "permute")
     return None, bufs["status"]
+
+
+def multisplit(keys: torch.Tensor, nbuckets: int = 8, shift: int = 29, out=None, stream=None):
+    """Stable bucket-major partition of a flat key array by label (key >> shift) & (nbuckets-1)
+    (the local step of the global w-way partition, cfg5).  Returns (out, bucket_starts[nbuckets])."""
+    k = keys.reshape(-1)
+    if k.dtype != torch.int32 or not k.is_cuda:
+        raise TypeError("keys must be a CUDA int32 (uint32 bits) tensor")
+    n = k.numel()
+    res = out if out is not None else torch.empty_like(k)
+    starts = torch.zeros((nbuckets,), dtype=torch.int64, device=k.device)
+    ws = torch.empty((int(lib().dmm_multisplit_workspace_bytes(n, nbuckets)),), dtype=torch.uint8, device=k.device)
+    _check(lib().dmm_multisplit(k.data_ptr(), n, shift, nbuckets, res.data_ptr(), starts.data_ptr(), ws.data_ptr(),
+                                _stream(stream)), "multisplit")
+    return res, starts
 
 
 def version() -> str:
