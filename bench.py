@@ -253,17 +253,38 @@ def main():
                    out.view(count, -1)[:, :-1].to(torch.int64) & 0xFFFFFFFF).all())
 
     # ---- end to end through the public API (pinned host in/out) -------------------------
+    # chunks cycle over 3 streams: H2D of chunk i+1 || kernel of chunk i || D2H of chunk i-1
+    from paper_1507_01391_b200.pipeline import run_pipelined
     h_in = g.cpu().pin_memory()
     h_out = torch.empty_like(h_in).pin_memory()
-    d_in = torch.empty_like(g)
+
+    perm_slot_bufs = {}
+
+    def chunk_fn(din, dout, s, lo):
+        if alg == "partition_general":
+            dmm.partition_general(din, flags=flags, out=dout, stream=s, check=False)
+        elif alg == "integer_sort_general":
+            dmm.integer_sort_general(din, 1 << 32, out=dout, stream=s, check=False)
+        elif alg == "permute":
+            bufs = perm_slot_bufs.setdefault((s.cuda_stream, din.shape[0]), {})
+            if "seeds" not in bufs:
+                bufs["seeds"] = torch.arange(1 + rank * count + lo, 1 + rank * count + lo + din.shape[0],
+                                             dtype=torch.int64, device="cuda")
+            dmm.permute_into(din, dout, None, bufs, stream=s)
+        else:
+            from paper_1507_01391_b200.distributed import global_partition
+            res, _ = global_partition(din.view(-1))
+            dout.view(-1).copy_(res)
+
+    chunks = 8 if alg != "global_partition" else 1
+    slots = run_pipelined(chunk_fn, h_in, h_out, chunks=chunks)  # warm-up (allocations)
+    torch.cuda.synchronize()
     barrier()
     ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_steps = max(3, args.steps // 4)
     ee0.record(stream)
     for _ in range(e2e_steps):
-        d_in.copy_(h_in, non_blocking=True)
-        step(d_in, out)
-        h_out.copy_(out, non_blocking=True)
+        run_pipelined(chunk_fn, h_in, h_out, chunks=chunks, slots=slots)
     ee1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = ee0.elapsed_time(ee1) / e2e_steps
@@ -271,6 +292,9 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
+    if alg == "partition_general":
+        rows = torch.arange(w, dtype=torch.int32).view(1, w, 1)
+        ok = ok and bool((h_out == rows).all())
 
     if rank == 0:
         peaks, peak_kind = _peaks()

@@ -171,6 +171,8 @@ dmm_status launch_general(const GeneralArgs& a) {
         if (smem > 48 * 1024 &&
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
             return check_launch("cudaFuncSetAttribute");
+        // prefer the full 228 KB shared-memory carveout: occupancy is bounded by smem + registers
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         configured = true;
     }
     const uint64_t units = (a.count + PK - 1) / PK;

@@ -65,6 +65,8 @@ dmm_status launch_layout(const uint32_t* in, uint32_t* out, uint64_t count, int 
         if (smem > 48 * 1024 &&
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
             return check_launch("cudaFuncSetAttribute");
+        // prefer the full 228 KB shared-memory carveout: occupancy is bounded by smem + registers
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         configured = true;
     }
     if (count == 0)

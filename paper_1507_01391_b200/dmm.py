@@ -389,6 +389,7 @@ def permute_into(src: torch.Tensor, dst: torch.Tensor, seeds, bufs: dict, alpha:
     count, w, m = src.shape
     if "seeds" not in bufs or bufs["seeds"].numel() != count:
         bufs["seeds"] = torch.as_tensor(np.asarray(seeds, dtype=np.uint64).view(np.int64), device="cuda")
+    if "reps" not in bufs or bufs["reps"].shape[0] != count:
         bufs["reps"] = torch.zeros((count, 5), dtype=torch.int64, device="cuda")
         bufs["hist"] = torch.zeros((count, 64), dtype=torch.int64, device="cuda")
         bufs["shifts"] = torch.zeros((count, w), dtype=torch.int32, device="cuda")
