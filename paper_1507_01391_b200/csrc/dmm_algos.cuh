@@ -190,10 +190,12 @@ __device__ __forceinline__ void tstages_q(uint32_t (&x)[M]) {
     }
 }
 
-template <int PK, class V, int KC, int M>
+// bitonic merge levels KC .. KEND of the block sort (KEND defaults to the last level)
+template <int PK, class V, int KC, int KEND = -1, int M>
 __device__ __forceinline__ void block_merge_levels(uint32_t (&x)[M], uint32_t* buf, int lane) {
     constexpr int R = ilog2_ceil_c(V::WV), QB = ilog2_ceil_c(V::MV / V::WV), NB = 2 * R + QB;
-    if constexpr (KC <= NB) {
+    constexpr int LAST = KEND < 0 ? NB : KEND;
+    if constexpr (KC <= LAST) {
         if constexpr (KC < R + QB) {
             // the whole merge lives in the lane's registers; direction bit KC is a register bit
             if (V::active(lane))
@@ -216,7 +218,7 @@ __device__ __forceinline__ void block_merge_levels(uint32_t (&x)[M], uint32_t* b
                 flip<V::C0, V::MV>(x, f);
             }
         }
-        block_merge_levels<PK, V, KC + 1>(x, buf, lane);
+        block_merge_levels<PK, V, KC + 1, KEND>(x, buf, lane);
     }
 }
 

@@ -1,0 +1,187 @@
+// tile_sort.cu -- kernel 3 for tiles too wide for one warp's registers: the 32 x 128 uint32
+// tile of cfg3 (4096 keys) sorted by a CTA of 4 warps.  integer_sort_general on a 32 x 128
+// view reduces to partition_leaf (w <= m), whose outcome is the tile in row-major sorted
+// order (partition.hpp:156-172, sort.hpp:288-311); any conflict-free sorter of the same
+// multiset reproduces it bit for bit.
+//
+// Sorted rank e = 1024*w + 32*r + j lives in warp w, lane r, register j, i.e. the tile's
+// row-major order itself: warp w loads/stores 1024 contiguous words (lane r: 128 contiguous
+// bytes).  Bitonic levels 1..10 run inside each warp (register stages + row-bit stages
+// after a conflict-free transpose, as sort_block); level 10's direction is warp bit 0
+// (warp-uniform flip).  Levels 11 and 12 add compare-exchange stages between warps w and
+// w ^ 2^b through a lane-major shared slab (each lane touches its own bank column: no
+// conflicts), then the in-warp stages of a full-warp merge.
+#include "general_kernel.cuh"
+
+namespace dmmdev {
+
+constexpr int kTileWarps = 4;
+
+// compare-exchange with the partner warp (w ^ 2^b): lower warp keeps the minima
+template <int PK>
+__device__ __forceinline__ void cross_warp_stage(uint32_t (&x)[32], uint32_t* slabs, int warp, int lane, int b) {
+    uint32_t* mine = slabs + warp * (32 * 33);
+    const uint32_t* other = slabs + (warp ^ (1 << b)) * (32 * 33);
+    const bool lower = ((warp >> b) & 1) == 0;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+        mine[j * 33 + lane] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        uint32_t a = x[j], c = other[j * 33 + lane];
+        Key<PK>::cx(a, c);
+        x[j] = lower ? a : c;
+    }
+    __syncthreads();
+}
+
+template <int PK, int MODE>
+__global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* __restrict__ in,
+                                                               uint32_t* __restrict__ out, uint64_t count,
+                                                               uint64_t domain, dmm_general_stats* __restrict__ stats,
+                                                               uint8_t* __restrict__ status) {
+    __shared__ uint32_t smem[kTileWarps * 32 * 33];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    uint32_t* buf = smem + warp * (32 * 33);
+    const uint64_t tile0 = (uint64_t)blockIdx.x * PK;
+    const bool hasB = PK == 2 && tile0 + 1 < count;
+    constexpr int M = 128;
+
+    uint32_t x[32];
+    uint32_t bad = 0;
+    {
+        uint32_t a[32];
+        load_row<32>(in + tile0 * (32 * M) + warp * 1024 + lane * 32, a);
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+            bad |= (uint64_t)a[c] >= domain ? 1u : 0u;
+        if constexpr (PK == 2) {
+            uint32_t b[32];
+            if (hasB) {
+                load_row<32>(in + (tile0 + 1) * (32 * M) + warp * 1024 + lane * 32, b);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                    b[c] = 0;
+            }
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                bad |= (uint64_t)b[c] >= domain ? 2u : 0u;
+                x[c] = (a[c] & 0xFFFFu) | (b[c] << 16);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+                x[c] = a[c];
+        }
+    }
+
+    using V = VF<0xFFFFFFFFu, 0, 1, kWarp, 0, 32>;
+    // levels 1..9 inside the warp (ascending/descending by in-warp bits)
+    block_merge_levels<PK, V, 1, 9>(x, buf, lane);
+    // level 10: direction = warp bit 0
+    {
+        const uint32_t f = (warp & 1) ? 0xFFFFFFFFu : 0u;
+        flip<0, 32>(x, f);
+        block_merge_levels<PK, V, 10, 10>(x, buf, lane);
+        flip<0, 32>(x, f);
+    }
+    // level 11: direction = warp bit 1; cross-warp stage on warp bit 0, then the warp merge
+    {
+        const uint32_t f = (warp & 2) ? 0xFFFFFFFFu : 0u;
+        flip<0, 32>(x, f);
+        cross_warp_stage<PK>(x, smem, warp, lane, 0);
+        block_merge_levels<PK, V, 10, 10>(x, buf, lane);
+        flip<0, 32>(x, f);
+    }
+    // level 12: ascending; cross-warp stages on warp bits 1, 0, then the warp merge
+    cross_warp_stage<PK>(x, smem, warp, lane, 1);
+    cross_warp_stage<PK>(x, smem, warp, lane, 0);
+    block_merge_levels<PK, V, 10, 10>(x, buf, lane);
+
+    // tile reductions of the per-warp flags
+    __shared__ uint32_t flags_s[kTileWarps];
+    uint32_t mism = 0;
+    if constexpr (MODE == kModePartition) {
+        // row-major rank e = 1024 w + 32 r + j belongs to machine row e / 128 = 8 w + r / 4
+        const uint32_t row = 8u * warp + lane / 4;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            if constexpr (PK == 2) {
+                mism |= (x[c] & 0xFFFFu) != row ? 1u : 0u;
+                mism |= (x[c] >> 16) != row ? 2u : 0u;
+            } else {
+                mism |= x[c] != row ? 1u : 0u;
+            }
+        }
+    }
+    const uint32_t wflag = __reduce_or_sync(0xFFFFFFFFu, bad | (mism << 2));
+    if (lane == 0)
+        flags_s[warp] = wflag;
+    __syncthreads();
+    uint32_t all = 0;
+#pragma unroll
+    for (int i = 0; i < kTileWarps; ++i)
+        all |= flags_s[i];
+    const uint32_t badt = all & 3u, invalid = (all >> 2) | badt;
+
+#pragma unroll
+    for (int h = 0; h < PK; ++h) {
+        if (h == 1 && !hasB)
+            break;
+        const uint64_t k = tile0 + h;
+        uint32_t v[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+            v[c] = PK == 2 ? ((x[c] >> (16 * h)) & 0xFFFFu) : x[c];
+        store_row<32>(out + k * (32 * M) + warp * 1024 + lane * 32, v);
+        if (threadIdx.x == 0) {
+            uint8_t s = DMM_OK;
+            if (MODE == kModePartition && ((invalid >> h) & 1u))
+                s = DMM_INVALID_INSTANCE;
+            else if ((badt >> h) & 1u)
+                s = DMM_KEY_OUT_OF_RANGE;
+            if (status)
+                status[k] = s;
+            if (stats) {
+                stats[k].cleanup_retries = 0;  // w <= m: partition_leaf only, no cleanup loop
+                stats[k].sorted = 1;
+            }
+        }
+    }
+}
+
+}  // namespace dmmdev
+
+namespace dmmhost {
+
+dmm_status launch_general_m128(int mode, bool pk2, bool ext, const GeneralArgs& a) {
+    if (ext) {
+        set_error("extension kernels are only built where the reference rejects the shape");
+        return DMM_UNSUPPORTED_SHAPE;
+    }
+    if (mode == dmmdev::kModeSortAny) {
+        set_error("sort_wide_any is built for m = 32, 64");
+        return DMM_UNSUPPORTED_SHAPE;
+    }
+    const int pk = (mode == dmmdev::kModePartition || pk2) ? 2 : 1;
+    const uint64_t blocks = (a.count + pk - 1) / pk;
+    if (blocks > 0x7FFFFFFFull)
+        return DMM_INVALID_ARGUMENT;
+    const dim3 grid{unsigned(blocks)}, block{unsigned(dmmdev::kTileWarps * 32)};
+    if (mode == dmmdev::kModePartition)
+        dmmdev::k_tile_sort<2, dmmdev::kModePartition>
+            <<<grid, block, 0, a.stream>>>(a.in, a.out, a.count, a.domain, a.stats, a.status);
+    else if (pk == 2)
+        dmmdev::k_tile_sort<2, dmmdev::kModeIntegerSort>
+            <<<grid, block, 0, a.stream>>>(a.in, a.out, a.count, a.domain, a.stats, a.status);
+    else
+        dmmdev::k_tile_sort<1, dmmdev::kModeIntegerSort>
+            <<<grid, block, 0, a.stream>>>(a.in, a.out, a.count, a.domain, a.stats, a.status);
+    return check_launch("k_tile_sort");
+}
+
+}  // namespace dmmhost
