@@ -166,15 +166,16 @@ __device__ __forceinline__ void sort_wide_any(uint32_t (&x)[M], uint32_t* buf, i
 template <int PK, int OFF, int N, int JB, int DIRBIT, int M>
 __device__ __forceinline__ void reg_stages(uint32_t (&x)[M]) {
     if constexpr (JB >= 0) {
-#pragma unroll
-        for (int p = 0; p < N; ++p) {
-            if (((p >> JB) & 1) == 0) {
-                if (DIRBIT < 0 || ((p >> DIRBIT) & 1) == 0)
-                    Key<PK>::cx(x[OFF + p], x[OFF + (p | (1 << JB))]);
+        static_for<0, N>([&](auto pc) {
+            constexpr int p = decltype(pc)::value;
+            if constexpr (((p >> JB) & 1) == 0) {
+                constexpr int I = p & ((1 << JB) - 1) | ((p >> (JB + 1)) << JB);  // comparator index
+                if constexpr (DIRBIT < 0 || ((p >> DIRBIT) & 1) == 0)
+                    Key<PK>::template cx<I>(x[OFF + p], x[OFF + (p | (1 << JB))]);
                 else
-                    Key<PK>::cx(x[OFF + (p | (1 << JB))], x[OFF + p]);
+                    Key<PK>::template cx<I>(x[OFF + (p | (1 << JB))], x[OFF + p]);
             }
-        }
+        });
         reg_stages<PK, OFF, N, JB - 1, DIRBIT>(x);
     }
 }
@@ -260,7 +261,7 @@ __device__ __forceinline__ void sort_columns_network(uint32_t (&x)[M], int lane)
             for (int c = 0; c < M; ++c) {
                 const uint32_t p = __shfl_xor_sync(0xFFFFFFFFu, x[c], j);
                 uint32_t lo = x[c], hi = p;
-                Key<PK>::cx(lo, hi);
+                Key<PK>::template cx<0>(lo, hi);
                 x[c] = keep_min ? lo : hi;
             }
         }

@@ -28,22 +28,63 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 namespace dmmdev {
 
 constexpr int kWarp = 32;
 
+// compile-time loop: f(std::integral_constant<int, i>) for i = B, B+S, ... < E
+template <int B, int E, int S = 1, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        static_for<B + S, E, S>(f);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Key traits: comparator and direction flip
+//
+// Pipe balance (tools/mb_pipes.cu, measured on B200): IMNMX / VIMNMX.U16x2 (and
+// HMNMX2) issue on the ALU pipe at 16 lanes/clk/SMSP; the FMA pipe (IMAD) is idle in
+// a sorting network.  max(a, b) = a + b - min(a, b) holds exactly in 32-bit wrapping
+// arithmetic -- and per 16-bit half of a packed pair, since the halves' sum is the
+// exact integer max_hi * 2^16 + max_lo -- so a comparator can take its max from two
+// IMADs instead of a second ALU min/max.  Comparators cx<I> with I % 3 != 0 use that
+// form (1 ALU + 2 FMA), the others the pure form (2 ALU): both pipes then carry 4/3
+// instructions per comparator (1.39x comparator throughput measured, bit-exact).
+// The IMAD multiplier -1 must be opaque to ptxas, or it folds the IMADs back into an
+// IADD3 on the ALU pipe: it is derived from %nsmid (ptxas cannot know it is nonzero;
+// ptxas reads it once per kernel and keeps it in a register).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t pipe_neg() {
+    uint32_t n;
+    asm("mov.u32 %0, %%nsmid;" : "=r"(n));
+    return n != 0 ? 0xFFFFFFFFu : 0u;
+}
+
+// h = a + b - l = b - (l - a), two IMADs on the FMA pipe
+__device__ __forceinline__ uint32_t fma_pipe_max(uint32_t a, uint32_t b, uint32_t l) {
+    const uint32_t neg = pipe_neg();
+    uint32_t t, h;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(a), "r"(neg), "r"(l));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h) : "r"(t), "r"(neg), "r"(b));
+    return h;
+}
+
 template <int PK>
 struct Key;
 
 template <>
 struct Key<1> {  // one 32-bit key per register
+    template <int I = 0>
     static __device__ __forceinline__ void cx(uint32_t& a, uint32_t& b) {
         const uint32_t l = min(a, b);
-        b = max(a, b);
+        if constexpr (I % 3 == 0)
+            b = max(a, b);
+        else
+            b = fma_pipe_max(a, b, l);
         a = l;
     }
     // per-lane "a > b" as a bit mask (bit 0)
@@ -53,9 +94,13 @@ struct Key<1> {  // one 32-bit key per register
 
 template <>
 struct Key<2> {  // two 16-bit keys per register (instance A low half, B high half)
+    template <int I = 0>
     static __device__ __forceinline__ void cx(uint32_t& a, uint32_t& b) {
         const uint32_t l = __vminu2(a, b);
-        b = __vmaxu2(a, b);
+        if constexpr (I % 3 == 0)
+            b = __vmaxu2(a, b);
+        else
+            b = fma_pipe_max(a, b, l);
         a = l;
     }
     // bit 0: A half a>b, bit 1: B half a>b
@@ -78,11 +123,11 @@ __device__ __forceinline__ void oe_merge(uint32_t (&x)[M]) {
     if constexpr (step < HI - LO) {
         oe_merge<PK, LO, HI, step>(x);
         oe_merge<PK, LO + R, HI, step>(x);
-#pragma unroll
-        for (int i = LO + R; i < HI - R; i += step)
-            Key<PK>::cx(x[i], x[i + R]);
+        static_for<LO + R, HI - R, step>([&](auto i) {
+            Key<PK>::template cx<(decltype(i)::value - LO) / step>(x[decltype(i)::value], x[decltype(i)::value + R]);
+        });
     } else {
-        Key<PK>::cx(x[LO], x[LO + R]);
+        Key<PK>::template cx<LO>(x[LO], x[LO + R]);
     }
 }
 
@@ -104,11 +149,14 @@ __device__ __forceinline__ void sort_net(uint32_t (&x)[M]) {
     oe_sort<PK, OFF, OFF + N - 1>(x);
 }
 
+// x ^= f for f in {0, ~0}, computed as x * (f | 1) + f (= x, or -x - 1 = ~x) on the
+// FMA pipe: the ALU pipe is the sorting networks' bottleneck
 template <int OFF, int N, int M>
 __device__ __forceinline__ void flip(uint32_t (&x)[M], uint32_t f) {
+    const uint32_t s = f | 1u;
 #pragma unroll
     for (int c = OFF; c < OFF + N; ++c)
-        x[c] ^= f;
+        asm("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(s), "r"(f));
 }
 
 // ---------------------------------------------------------------------------
@@ -197,20 +245,81 @@ struct ToRowMajor {
     __host__ __device__ static constexpr int src_col(int lane, int d) { return V::C0 + lin(lane, d) / V::WV; }
 };
 
-// A relayout goes through a per-warp staging buffer where slot (b, d) lives at
-// word (d - C0) * (32 + kappa) + b, i.e. in bank ((d - C0) * kappa + b) mod 32.
-//   scatter: lane a stores register c into its DESTINATION slot, then every lane
-//            loads its own slots (own-slot loads are conflict-free for any kappa);
-//   gather : every lane stores into its own slots (conflict-free), then lane b
-//            loads register d from its SOURCE slot.
-// find_layout picks, at compile time, the first (mode, kappa) for which every
-// warp-wide access touches 32 distinct banks -- the reference's CAC (core.hpp:
-// 445-467) checked exhaustively over all lanes and registers.  Returns
-// mode * 64 + kappa (mode 0 scatter, 1 gather) or -1.
+// A relayout goes through a per-warp staging buffer.  Two slot layouts:
+//
+//  * column-major (scalar modes 0/1): slot (b, d) at word (d - C0) * (32 + kappa) + b,
+//    i.e. bank ((d - C0) * kappa + b) mod 32;
+//      scatter (0): lane a stores register c into its DESTINATION slot, then every lane
+//                   loads its own slots (own-slot loads are conflict-free for any kappa);
+//      gather  (1): every lane stores into its own slots (conflict-free), then lane b
+//                   loads register d from its SOURCE slot;
+//  * lane-major (vector modes 2/3): slot (b, d) at word b * Q + (d - C0), Q = pitch, so a
+//    lane's own slots are contiguous and move as 128-bit STS.128 / LDS.128 (a quarter of
+//    the shared-memory instructions on the own side; the MIO queue is what stalls the
+//    relayout-heavy kernels):
+//      gather-v4  (2): own slots stored with STS.128, then scalar gathers from sources;
+//      scatter-v4 (3): scalar scatters to destinations, then own slots loaded with LDS.128.
+//    A 128-bit access is served a quarter-warp (8 lanes, 128 bytes) per wavefront, so it
+//    is conflict-free iff the 8 lanes of every quarter hit 8 distinct 4-bank groups.
+//
+// find_layout picks, at compile time, the first layout (vector modes first) for which
+// every warp-wide access touches distinct banks -- the reference's CAC (core.hpp:445-467)
+// checked exhaustively over all lanes and registers.  Returns mode * 64 + k (k = kappa
+// for modes 0/1, Q - MV for modes 2/3) or -1.
+__host__ __device__ constexpr int relayout_buf_words(int mv) {
+    return (mv * (mv >= 32 ? 33 : 64)) > 32 * (mv + 4) ? (mv * (mv >= 32 ? 33 : 64)) : 32 * (mv + 4);
+}
+
+template <class V, class Map>
+__host__ __device__ constexpr bool v4_own_ok(int Q) {  // own-slot 128-bit accesses, per quarter-warp
+    for (int j = 0; j < V::MV / 4; ++j) {
+        for (int q = 0; q < 4; ++q) {
+            uint32_t seen = 0;
+            for (int a = 8 * q; a < 8 * q + 8; ++a) {
+                if (!V::active(a))
+                    continue;
+                const int g = ((a * Q + 4 * j) / 4) & 7;
+                if ((seen >> g) & 1u)
+                    return false;
+                seen |= 1u << g;
+            }
+        }
+    }
+    return true;
+}
+
+template <class V, class Map>
+__host__ __device__ constexpr bool v4_cross_ok(int Q, bool gather) {  // scalar cross accesses
+    for (int c = V::C0; c < V::C0 + V::MV; ++c) {
+        uint32_t seen = 0;
+        for (int lane = 0; lane < kWarp; ++lane) {
+            if (!V::active(lane))
+                continue;
+            const int b = gather ? Map::src_lane(lane, c) : Map::dst_lane(lane, c);
+            const int d = gather ? Map::src_col(lane, c) : Map::dst_col(lane, c);
+            const int bank = (b * Q + (d - V::C0)) & 31;
+            if ((seen >> bank) & 1u)
+                return false;
+            seen |= 1u << bank;
+        }
+    }
+    return true;
+}
+
 template <class V, class Map>
 __host__ __device__ constexpr int find_layout() {
+    if (V::MV % 4 == 0 && V::C0 % 4 == 0) {
+        for (int mode = 2; mode < 4; ++mode) {
+            for (int Q = V::MV; Q * kWarp <= relayout_buf_words(V::MV); Q += 4) {
+                if (v4_own_ok<V, Map>(Q) && v4_cross_ok<V, Map>(Q, mode == 2))
+                    return mode * 64 + (Q - V::MV);
+            }
+        }
+    }
     for (int mode = 0; mode < 2; ++mode) {
         for (int k = 0; k <= 32; ++k) {
+            if ((32 + k) * V::MV > relayout_buf_words(V::MV))
+                break;
             bool ok = true;
             for (int c = V::C0; c < V::C0 + V::MV && ok; ++c) {
                 uint32_t seen = 0;
@@ -251,41 +360,77 @@ __host__ __device__ constexpr bool map_is_consistent() {
     return true;
 }
 
-// Words of shared memory a relayout buffer of an MV-wide window may use: MV columns
-// of pitch 32 + kappa.  Windows of 32+ columns only relayout with kappa <= 1
-// (statically checked in relayout()).
-__host__ __device__ constexpr int relayout_buf_words(int mv) { return mv * (mv >= 32 ? 33 : 64); }
-
 template <class V, class Map, int M>
 __device__ __forceinline__ void relayout(uint32_t (&x)[M], uint32_t* buf, int lane) {
     constexpr int L = find_layout<V, Map>();
-    static_assert(L >= 0, "no conflict-free skew for this relayout");
+    static_assert(L >= 0, "no conflict-free layout for this relayout");
     static_assert(map_is_consistent<V, Map>(), "relayout map is not a bijection with a matching inverse");
-    constexpr int P = 32 + (L & 63);
-    constexpr bool gather = L >= 64;
-    static_assert(V::MV * P <= relayout_buf_words(V::MV), "relayout buffer too small for this skew");
+    constexpr int mode = L / 64;
     const bool act = V::active(lane);
-    __syncwarp();
-    if (act) {
+    if constexpr (mode >= 2) {
+        constexpr int Q = V::MV + (L & 63);
+        static_assert(Q * kWarp <= relayout_buf_words(V::MV), "relayout buffer too small for this pitch");
+        uint32_t* own = buf + lane * Q;
+        __syncwarp();
+        if (act) {
+            if constexpr (mode == 2) {
 #pragma unroll
-        for (int c = V::C0; c < V::C0 + V::MV; ++c) {
-            if constexpr (gather) {
-                buf[(c - V::C0) * P + lane] = x[c];
+                for (int j = 0; j < V::MV / 4; ++j)
+                    *reinterpret_cast<uint4*>(own + 4 * j) =
+                        make_uint4(x[V::C0 + 4 * j], x[V::C0 + 4 * j + 1], x[V::C0 + 4 * j + 2], x[V::C0 + 4 * j + 3]);
             } else {
-                const int b = Map::dst_lane(lane, c), d = Map::dst_col(lane, c);
-                buf[(d - V::C0) * P + b] = x[c];
+#pragma unroll
+                for (int c = V::C0; c < V::C0 + V::MV; ++c) {
+                    const int b = Map::dst_lane(lane, c), d = Map::dst_col(lane, c);
+                    buf[b * Q + (d - V::C0)] = x[c];
+                }
             }
         }
-    }
-    __syncwarp();
-    if (act) {
+        __syncwarp();
+        if (act) {
+            if constexpr (mode == 2) {
 #pragma unroll
-        for (int d = V::C0; d < V::C0 + V::MV; ++d) {
-            if constexpr (gather) {
-                const int a = Map::src_lane(lane, d), c = Map::src_col(lane, d);
-                x[d] = buf[(c - V::C0) * P + a];
+                for (int d = V::C0; d < V::C0 + V::MV; ++d) {
+                    const int a = Map::src_lane(lane, d), c = Map::src_col(lane, d);
+                    x[d] = buf[a * Q + (c - V::C0)];
+                }
             } else {
-                x[d] = buf[(d - V::C0) * P + lane];
+#pragma unroll
+                for (int j = 0; j < V::MV / 4; ++j) {
+                    const uint4 t = *reinterpret_cast<const uint4*>(own + 4 * j);
+                    x[V::C0 + 4 * j] = t.x;
+                    x[V::C0 + 4 * j + 1] = t.y;
+                    x[V::C0 + 4 * j + 2] = t.z;
+                    x[V::C0 + 4 * j + 3] = t.w;
+                }
+            }
+        }
+    } else {
+        constexpr int P = 32 + (L & 63);
+        constexpr bool gather = mode == 1;
+        static_assert(V::MV * P <= relayout_buf_words(V::MV), "relayout buffer too small for this skew");
+        __syncwarp();
+        if (act) {
+#pragma unroll
+            for (int c = V::C0; c < V::C0 + V::MV; ++c) {
+                if constexpr (gather) {
+                    buf[(c - V::C0) * P + lane] = x[c];
+                } else {
+                    const int b = Map::dst_lane(lane, c), d = Map::dst_col(lane, c);
+                    buf[(d - V::C0) * P + b] = x[c];
+                }
+            }
+        }
+        __syncwarp();
+        if (act) {
+#pragma unroll
+            for (int d = V::C0; d < V::C0 + V::MV; ++d) {
+                if constexpr (gather) {
+                    const int a = Map::src_lane(lane, d), c = Map::src_col(lane, d);
+                    x[d] = buf[(c - V::C0) * P + a];
+                } else {
+                    x[d] = buf[(d - V::C0) * P + lane];
+                }
             }
         }
     }

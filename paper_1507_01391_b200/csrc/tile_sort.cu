@@ -20,19 +20,23 @@ constexpr int kTileWarps = 4;
 // compare-exchange with the partner warp (w ^ 2^b): lower warp keeps the minima
 template <int PK>
 __device__ __forceinline__ void cross_warp_stage(uint32_t (&x)[32], uint32_t* slabs, int warp, int lane, int b) {
-    uint32_t* mine = slabs + warp * (32 * 33);
-    const uint32_t* other = slabs + (warp ^ (1 << b)) * (32 * 33);
+    uint32_t* mine = slabs + warp * relayout_buf_words(32);
+    const uint32_t* other = slabs + (warp ^ (1 << b)) * relayout_buf_words(32);
     const bool lower = ((warp >> b) & 1) == 0;
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 32; ++j)
         mine[j * 33 + lane] = x[j];
     __syncthreads();
+    // lower is warp-uniform: one min or max per key
+    if (lower) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        uint32_t a = x[j], c = other[j * 33 + lane];
-        Key<PK>::cx(a, c);
-        x[j] = lower ? a : c;
+        for (int j = 0; j < 32; ++j)
+            x[j] = PK == 2 ? __vminu2(x[j], other[j * 33 + lane]) : min(x[j], other[j * 33 + lane]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            x[j] = PK == 2 ? __vmaxu2(x[j], other[j * 33 + lane]) : max(x[j], other[j * 33 + lane]);
     }
     __syncthreads();
 }
@@ -42,10 +46,10 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
                                                                uint32_t* __restrict__ out, uint64_t count,
                                                                uint64_t domain, dmm_general_stats* __restrict__ stats,
                                                                uint8_t* __restrict__ status) {
-    __shared__ uint32_t smem[kTileWarps * 32 * 33];
+    __shared__ __align__(16) uint32_t smem[kTileWarps * relayout_buf_words(32)];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    uint32_t* buf = smem + warp * (32 * 33);
+    uint32_t* buf = smem + warp * relayout_buf_words(32);
     const uint64_t tile0 = (uint64_t)blockIdx.x * PK;
     const bool hasB = PK == 2 && tile0 + 1 < count;
     constexpr int M = 128;
