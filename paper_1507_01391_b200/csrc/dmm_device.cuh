@@ -308,7 +308,15 @@ __host__ __device__ constexpr bool v4_cross_ok(int Q, bool gather) {  // scalar 
 
 template <class V, class Map>
 __host__ __device__ constexpr int find_layout() {
-    if (V::MV % 4 == 0 && V::C0 % 4 == 0) {
+    // vector modes only where every quarter-warp is wholly active or wholly idle: a
+    // predicated 128-bit access with a ragged quarter was measured (ncu) to cost an extra
+    // wavefront, so partial quarters keep the scalar layouts
+    bool quarters_whole = true;
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t qm = (V::MASK >> (8 * q)) & 0xFFu;
+        quarters_whole = quarters_whole && (qm == 0u || qm == 0xFFu);
+    }
+    if (V::MV % 4 == 0 && V::C0 % 4 == 0 && quarters_whole) {
         for (int mode = 2; mode < 4; ++mode) {
             for (int Q = V::MV; Q * kWarp <= relayout_buf_words(V::MV); Q += 4) {
                 if (v4_own_ok<V, Map>(Q) && v4_cross_ok<V, Map>(Q, mode == 2))

@@ -43,8 +43,14 @@ __device__ __forceinline__ void store_row(uint32_t* __restrict__ p, const uint32
 enum : int { kModeIntegerSort = 0, kModePartition = 1, kModeSortAny = 2 };
 
 // One warp per PK instances.  Row r of instance k is at in[(k*32 + r)*M].
+// CTA shape: warps per CTA and the occupancy target handed to ptxas (register cap)
+template <int M, int PK>
+constexpr int warps_per_block() { return M >= 128 ? 4 : 8; }
+template <int M, int PK>
+constexpr int min_blocks_per_sm() { return 1; }
+
 template <int M, int PK, bool EXT, int MODE>
-__global__ void __launch_bounds__(256) k_general_sort(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+__global__ void __launch_bounds__(warps_per_block<M, PK>() * 32, min_blocks_per_sm<M, PK>()) k_general_sort(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                                                       uint64_t count, uint64_t domain, int strict, int ascending,
                                                       dmm_general_stats* __restrict__ stats,
                                                       uint8_t* __restrict__ status) {
@@ -57,33 +63,63 @@ __global__ void __launch_bounds__(256) k_general_sort(const uint32_t* __restrict
         return;
     const bool hasB = PK == 2 && inst0 + 1 < count;
 
+    // A leaf-only instance (w <= m: balance_divide_sort is partition_leaf, whose outcome
+    // is the sorted multiset whatever the starting arrangement) is loaded fully coalesced:
+    // lane l takes the 16-byte chunks l, l + 32, ... of the instance.  Otherwise lane r
+    // loads row r (the recursion's intermediate matrices depend on the arrangement).
+    constexpr bool kAnyLayout = MODE != kModeSortAny && kWarp <= M && M % 4 == 0;
+    auto load = [&](uint64_t k, uint32_t (&v)[M]) {
+        if constexpr (kAnyLayout) {
+            const uint4* q = reinterpret_cast<const uint4*>(in + k * kWarp * M);
+#pragma unroll
+            for (int i = 0; i < M / 4; ++i) {
+                const uint4 t = __ldg(q + lane + kWarp * i);
+                v[4 * i] = t.x;
+                v[4 * i + 1] = t.y;
+                v[4 * i + 2] = t.z;
+                v[4 * i + 3] = t.w;
+            }
+        } else {
+            load_row<M>(in + (k * kWarp + lane) * M, v);
+        }
+    };
+    // keys outside [0, domain): OR-accumulate (power-of-two domain, half an ALU op per
+    // key) or max-accumulate; nothing to check for domain >= 2^32
+    const bool dom32 = domain < (1ull << 32);
+    const bool dom_pow2 = (domain & (domain - 1)) == 0;
+    const uint32_t dom_mask = dom32 && dom_pow2 ? ~(uint32_t)(domain - 1) : 0u;
+    auto keys_bad = [&](const uint32_t* v, int n) -> uint32_t {
+        if (!dom32)
+            return 0u;
+        uint32_t acc = 0;
+        if (dom_pow2) {
+#pragma unroll
+            for (int c = 0; c < n; ++c)
+                acc |= v[c];
+            return (acc & dom_mask) != 0 ? 1u : 0u;
+        }
+#pragma unroll
+        for (int c = 0; c < n; ++c)
+            acc = max(acc, v[c]);
+        return acc >= (uint32_t)domain ? 1u : 0u;
+    };
+
     uint32_t x[M];
-    uint32_t bad = 0;  // bit h: half h holds a key outside [0, domain)
-    {
-        uint32_t a[M];
-        load_row<M>(in + (inst0 * kWarp + lane) * M, a);
-#pragma unroll
-        for (int c = 0; c < M; ++c)
-            bad |= (uint64_t)a[c] >= domain ? 1u : 0u;
-        if constexpr (PK == 2) {
-            uint32_t b[M];
-            if (hasB) {
-                load_row<M>(in + ((inst0 + 1) * kWarp + lane) * M, b);
-            } else {
-#pragma unroll
-                for (int c = 0; c < M; ++c)
-                    b[c] = 0;
-            }
-#pragma unroll
-            for (int c = 0; c < M; ++c) {
-                bad |= (uint64_t)b[c] >= domain ? 2u : 0u;
-                x[c] = (a[c] & 0xFFFFu) | (b[c] << 16);
-            }
+    load(inst0, x);
+    uint32_t bad = keys_bad(x, M);  // bit h: half h holds a key outside [0, domain)
+    if constexpr (PK == 2) {
+        uint32_t b[M];
+        if (hasB) {
+            load(inst0 + 1, b);
         } else {
 #pragma unroll
             for (int c = 0; c < M; ++c)
-                x[c] = a[c];
+                b[c] = 0;
         }
+        bad |= keys_bad(b, M) << 1;
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+            x[c] = __byte_perm(x[c], b[c], 0x5410);  // (a & 0xFFFF) | (b << 16)
     }
     bad = __reduce_or_sync(0xFFFFFFFFu, bad);
 
@@ -99,16 +135,13 @@ __global__ void __launch_bounds__(256) k_general_sort(const uint32_t* __restrict
     if constexpr (MODE == kModePartition) {
         // check_partition_instance (partition.hpp:112-124): labels in [0, w), m copies
         // each  <=>  (labels < w) and the sorted result has row i = i everywhere.
-        uint32_t mism = 0;
+        // OR of (key ^ lane) over the row: one LOP3 per register, both halves at once
+        const uint32_t want = PK == 2 ? (uint32_t)lane * 0x10001u : (uint32_t)lane;
+        uint32_t diff = 0;
 #pragma unroll
-        for (int c = 0; c < M; ++c) {
-            if constexpr (PK == 2) {
-                mism |= (x[c] & 0xFFFFu) != (uint32_t)lane ? 1u : 0u;
-                mism |= (x[c] >> 16) != (uint32_t)lane ? 2u : 0u;
-            } else {
-                mism |= x[c] != (uint32_t)lane ? 1u : 0u;
-            }
-        }
+        for (int c = 0; c < M; ++c)
+            diff |= x[c] ^ want;
+        const uint32_t mism = PK == 2 ? ((diff & 0xFFFFu) ? 1u : 0u) | ((diff >> 16) ? 2u : 0u) : (diff ? 1u : 0u);
         invalid = __reduce_or_sync(0xFFFFFFFFu, mism) | bad;
     }
 
@@ -117,11 +150,24 @@ __global__ void __launch_bounds__(256) k_general_sort(const uint32_t* __restrict
         if (h == 1 && !hasB)
             break;
         const uint64_t k = inst0 + h;
-        uint32_t v[M];
+        if constexpr (M % 4 == 0) {
+            // unpack one 16-byte vector at a time (register budget)
+            uint4* q = reinterpret_cast<uint4*>(out + (k * kWarp + lane) * M);
 #pragma unroll
-        for (int c = 0; c < M; ++c)
-            v[c] = PK == 2 ? ((x[c] >> (16 * h)) & 0xFFFFu) : x[c];
-        store_row<M>(out + (k * kWarp + lane) * M, v);
+            for (int i = 0; i < M / 4; ++i) {
+                uint32_t v[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    v[e] = PK == 2 ? ((x[4 * i + e] >> (16 * h)) & 0xFFFFu) : x[4 * i + e];
+                q[i] = make_uint4(v[0], v[1], v[2], v[3]);
+            }
+        } else {
+            uint32_t v[M];
+#pragma unroll
+            for (int c = 0; c < M; ++c)
+                v[c] = PK == 2 ? ((x[c] >> (16 * h)) & 0xFFFFu) : x[c];
+            store_row<M>(out + (k * kWarp + lane) * M, v);
+        }
         if (lane == 0) {
             const bool unsorted = (res.unsorted >> h) & 1u;
             uint8_t s = DMM_OK;
@@ -158,13 +204,10 @@ struct GeneralArgs {
     cudaStream_t stream;
 };
 
-template <int M>
-constexpr int warps_per_block() { return M >= 128 ? 4 : 8; }
-
 template <int M, int PK, bool EXT, int MODE>
 dmm_status launch_general(const GeneralArgs& a) {
     auto kern = dmmdev::k_general_sort<M, PK, EXT, MODE>;
-    constexpr int kWarpsPerBlock = warps_per_block<M>();
+    constexpr int kWarpsPerBlock = dmmdev::warps_per_block<M, PK>();
     const size_t smem = size_t(kWarpsPerBlock) * dmmdev::relayout_buf_words(M) * sizeof(uint32_t);
     static bool configured = false;  // per instantiation
     if (!configured) {
