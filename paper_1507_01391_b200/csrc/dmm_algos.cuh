@@ -180,6 +180,18 @@ __device__ __forceinline__ void reg_stages(uint32_t (&x)[M]) {
     }
 }
 
+// a single ascending stage jb on registers [OFF, OFF+N): pairs (p, p ^ 2^jb)
+template <int PK, int OFF, int N, int JB, int M>
+__device__ __forceinline__ void reg_stage(uint32_t (&x)[M]) {
+    static_for<0, N>([&](auto pc) {
+        constexpr int p = decltype(pc)::value;
+        if constexpr (((p >> JB) & 1) == 0) {
+            constexpr int I = p & ((1 << JB) - 1) | ((p >> (JB + 1)) << JB);
+            Key<PK>::template cx<I>(x[OFF + p], x[OFF + (p | (1 << JB))]);
+        }
+    });
+}
+
 // l-bit stages of merge level KC in the transposed layout, for every group of WV
 // registers (group QI = one value of the q bits; l bits are the group's low bits)
 template <int PK, class V, int KC, int QI, int M>

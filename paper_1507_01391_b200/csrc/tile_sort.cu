@@ -5,12 +5,18 @@
 // multiset reproduces it bit for bit.
 //
 // Sorted rank e = 1024*w + 32*r + j lives in warp w, lane r, register j, i.e. the tile's
-// row-major order itself: warp w loads/stores 1024 contiguous words (lane r: 128 contiguous
-// bytes).  Bitonic levels 1..10 run inside each warp (register stages + row-bit stages
-// after a conflict-free transpose, as sort_block); level 10's direction is warp bit 0
-// (warp-uniform flip).  Levels 11 and 12 add compare-exchange stages between warps w and
-// w ^ 2^b through a lane-major shared slab (each lane touches its own bank column: no
-// conflicts), then the in-warp stages of a full-warp merge.
+// row-major order itself: warp w stores 1024 contiguous words (lane r: 128 contiguous
+// bytes).  The starting arrangement is irrelevant to a sort, so the tile is loaded fully
+// coalesced (lane l of warp w takes the 16-byte chunks 256w + l + 32i).
+//
+// Bitonic levels 1..5 are register-local (static code).  Every later level is one "pass"
+// of the same loop: flip the keys of the lanes whose direction bit is set (lane bit for
+// in-warp levels 6..9, warp bit for 10 and 11; x ^ ~0 reverses the order), optional
+// compare-exchange stages with the partner warp (w ^ 2^b) through a lane-major shared
+// slab (each lane touches its own bank column: no conflicts), then transpose / row-bit
+// stages / transpose / register stages, all ascending, and flip back.  The passes share
+// ONE copy of the transpose and of the five single-stage bodies (runtime switch): the
+// straight-line version (64 KB of SASS) stalled on instruction fetch (ncu: no_inst 42 %).
 #include "general_kernel.cuh"
 
 namespace dmmdev {
@@ -41,6 +47,18 @@ __device__ __forceinline__ void cross_warp_stage(uint32_t (&x)[32], uint32_t* sl
     __syncthreads();
 }
 
+// one ascending stage over the 32 registers: pairs (p, p ^ 2^j), j < 5 chosen at runtime
+template <int PK>
+__device__ __forceinline__ void one_stage(uint32_t (&x)[32], int j) {
+    switch (j) {
+        case 0: reg_stage<PK, 0, 32, 0>(x); break;
+        case 1: reg_stage<PK, 0, 32, 1>(x); break;
+        case 2: reg_stage<PK, 0, 32, 2>(x); break;
+        case 3: reg_stage<PK, 0, 32, 3>(x); break;
+        default: reg_stage<PK, 0, 32, 4>(x); break;
+    }
+}
+
 template <int PK, int MODE>
 __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* __restrict__ in,
                                                                uint32_t* __restrict__ out, uint64_t count,
@@ -57,54 +75,79 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
     uint32_t x[32];
     uint32_t bad = 0;
     {
-        uint32_t a[32];
-        load_row<32>(in + tile0 * (32 * M) + warp * 1024 + lane * 32, a);
+        // coalesced chunk loads; keys outside [0, domain) flagged by OR / max accumulation
+        const bool dom32 = domain < (1ull << 32);
+        const bool dom_pow2 = (domain & (domain - 1)) == 0;
+        const uint32_t dom_mask = dom32 && dom_pow2 ? ~(uint32_t)(domain - 1) : 0u;
+        auto load = [&](uint64_t t, uint32_t (&v)[32]) -> uint32_t {
+            const uint4* q = reinterpret_cast<const uint4*>(in + t * (32 * M)) + warp * 256 + lane;
+            uint32_t acc_or = 0, acc_max = 0;
 #pragma unroll
-        for (int c = 0; c < 32; ++c)
-            bad |= (uint64_t)a[c] >= domain ? 1u : 0u;
+            for (int i = 0; i < 8; ++i) {
+                const uint4 c = __ldg(q + 32 * i);
+                v[4 * i] = c.x;
+                v[4 * i + 1] = c.y;
+                v[4 * i + 2] = c.z;
+                v[4 * i + 3] = c.w;
+            }
+            if (!dom32)
+                return 0u;
+            if (dom_pow2) {
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                    acc_or |= v[c];
+                return (acc_or & dom_mask) ? 1u : 0u;
+            }
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+                acc_max = max(acc_max, v[c]);
+            return acc_max >= (uint32_t)domain ? 1u : 0u;
+        };
+        bad = load(tile0, x);
         if constexpr (PK == 2) {
             uint32_t b[32];
             if (hasB) {
-                load_row<32>(in + (tile0 + 1) * (32 * M) + warp * 1024 + lane * 32, b);
+                bad |= load(tile0 + 1, b) << 1;
             } else {
 #pragma unroll
                 for (int c = 0; c < 32; ++c)
                     b[c] = 0;
             }
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                bad |= (uint64_t)b[c] >= domain ? 2u : 0u;
-                x[c] = (a[c] & 0xFFFFu) | (b[c] << 16);
-            }
-        } else {
-#pragma unroll
             for (int c = 0; c < 32; ++c)
-                x[c] = a[c];
+                x[c] = __byte_perm(x[c], b[c], 0x5410);  // (a & 0xFFFF) | (b << 16)
         }
     }
 
     using V = VF<0xFFFFFFFFu, 0, 1, kWarp, 0, 32>;
-    // levels 1..9 inside the warp (ascending/descending by in-warp bits)
-    block_merge_levels<PK, V, 1, 9>(x, buf, lane);
-    // level 10: direction = warp bit 0
-    {
-        const uint32_t f = (warp & 1) ? 0xFFFFFFFFu : 0u;
+    // levels 1..5: register-local, static
+    block_merge_levels<PK, V, 1, 5>(x, buf, lane);
+    // levels 6..12 as passes of one loop (see the header)
+#pragma unroll 1
+    for (int pass = 0; pass < 7; ++pass) {
+        const int level = 6 + pass;
+        uint32_t f;
+        if (level < 10)
+            f = (lane >> (level - 5)) & 1;  // in-warp level: direction = element bit `level`
+        else if (level < 12)
+            f = (warp >> (level - 10)) & 1;  // cross-warp levels: direction = warp bit
+        else
+            f = 0;
+        f = f ? 0xFFFFFFFFu : 0u;
         flip<0, 32>(x, f);
-        block_merge_levels<PK, V, 10, 10>(x, buf, lane);
+#pragma unroll 1
+        for (int b = level - 11; b >= 0; --b)  // stages on warp bits (levels 11, 12)
+            cross_warp_stage<PK>(x, smem, warp, lane, b);
+        const int row_stages = (level < 10 ? level : 10) - 6;  // row-bit stages row_stages..0
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+            transpose_blocks<V>(x, buf, lane);
+#pragma unroll 1
+            for (int j = half == 0 ? row_stages : 4; j >= 0; --j)
+                one_stage<PK>(x, j);
+        }
         flip<0, 32>(x, f);
     }
-    // level 11: direction = warp bit 1; cross-warp stage on warp bit 0, then the warp merge
-    {
-        const uint32_t f = (warp & 2) ? 0xFFFFFFFFu : 0u;
-        flip<0, 32>(x, f);
-        cross_warp_stage<PK>(x, smem, warp, lane, 0);
-        block_merge_levels<PK, V, 10, 10>(x, buf, lane);
-        flip<0, 32>(x, f);
-    }
-    // level 12: ascending; cross-warp stages on warp bits 1, 0, then the warp merge
-    cross_warp_stage<PK>(x, smem, warp, lane, 1);
-    cross_warp_stage<PK>(x, smem, warp, lane, 0);
-    block_merge_levels<PK, V, 10, 10>(x, buf, lane);
 
     // tile reductions of the per-warp flags
     __shared__ uint32_t flags_s[kTileWarps];
