@@ -47,15 +47,17 @@ __device__ __forceinline__ void cross_warp_stage(uint32_t (&x)[32], uint32_t* sl
     __syncthreads();
 }
 
-// one ascending stage over the 32 registers: pairs (p, p ^ 2^j), j < 5 chosen at runtime
+// ascending stages js..0 over the 32 registers (pairs (p, p ^ 2^j)), js < 5 chosen at
+// runtime; each case is one straight-line sequence, so register renaming only has to be
+// undone once per sequence (a per-stage switch cost 16 moves per stage)
 template <int PK>
-__device__ __forceinline__ void one_stage(uint32_t (&x)[32], int j) {
-    switch (j) {
-        case 0: reg_stage<PK, 0, 32, 0>(x); break;
-        case 1: reg_stage<PK, 0, 32, 1>(x); break;
-        case 2: reg_stage<PK, 0, 32, 2>(x); break;
-        case 3: reg_stage<PK, 0, 32, 3>(x); break;
-        default: reg_stage<PK, 0, 32, 4>(x); break;
+__device__ __forceinline__ void stages_down(uint32_t (&x)[32], int js) {
+    switch (js) {
+        case 0: reg_stages<PK, 0, 32, 0, -1>(x); break;
+        case 1: reg_stages<PK, 0, 32, 1, -1>(x); break;
+        case 2: reg_stages<PK, 0, 32, 2, -1>(x); break;
+        case 3: reg_stages<PK, 0, 32, 3, -1>(x); break;
+        default: reg_stages<PK, 0, 32, 4, -1>(x); break;
     }
 }
 
@@ -122,10 +124,9 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
     using V = VF<0xFFFFFFFFu, 0, 1, kWarp, 0, 32>;
     // levels 1..5: register-local, static
     block_merge_levels<PK, V, 1, 5>(x, buf, lane);
-    // levels 6..12 as passes of one loop (see the header)
-#pragma unroll 1
-    for (int pass = 0; pass < 7; ++pass) {
-        const int level = 6 + pass;
+    // levels 6..12 as passes of one loop (see the header); the flip that ends a pass and
+    // the one that starts the next are merged into one
+    auto dir_mask = [&](int level) -> uint32_t {
         uint32_t f;
         if (level < 10)
             f = (lane >> (level - 5)) & 1;  // in-warp level: direction = element bit `level`
@@ -133,8 +134,15 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
             f = (warp >> (level - 10)) & 1;  // cross-warp levels: direction = warp bit
         else
             f = 0;
-        f = f ? 0xFFFFFFFFu : 0u;
-        flip<0, 32>(x, f);
+        return f ? 0xFFFFFFFFu : 0u;
+    };
+    uint32_t fcur = 0;
+#pragma unroll 1
+    for (int pass = 0; pass < 7; ++pass) {
+        const int level = 6 + pass;
+        const uint32_t f = dir_mask(level);
+        flip<0, 32>(x, f ^ fcur);
+        fcur = f;
 #pragma unroll 1
         for (int b = level - 11; b >= 0; --b)  // stages on warp bits (levels 11, 12)
             cross_warp_stage<PK>(x, smem, warp, lane, b);
@@ -142,12 +150,10 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
             transpose_blocks<V>(x, buf, lane);
-#pragma unroll 1
-            for (int j = half == 0 ? row_stages : 4; j >= 0; --j)
-                one_stage<PK>(x, j);
+            stages_down<PK>(x, half == 0 ? row_stages : 4);
         }
-        flip<0, 32>(x, f);
     }
+    flip<0, 32>(x, fcur);
 
     // tile reductions of the per-warp flags
     __shared__ uint32_t flags_s[kTileWarps];
