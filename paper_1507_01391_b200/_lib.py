@@ -8,7 +8,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libdmm_b200.so")
+# DMM_B200_LIB: an alternative build of the same library (A/B timing of build variants)
+LIB_PATH = os.environ.get("DMM_B200_LIB") or os.path.join(PKG, "libdmm_b200.so")
 
 
 class GeneralStats(C.Structure):  # dmm_general_stats

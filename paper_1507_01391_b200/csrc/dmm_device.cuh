@@ -73,6 +73,11 @@ __device__ __forceinline__ uint32_t fma_pipe_max(uint32_t a, uint32_t b, uint32_
     return h;
 }
 
+#ifndef DMM_CX_PURE_EVERY
+#define DMM_CX_PURE_EVERY 3
+#endif
+constexpr int kPureEvery = DMM_CX_PURE_EVERY;
+
 template <int PK>
 struct Key;
 
@@ -81,7 +86,7 @@ struct Key<1> {  // one 32-bit key per register
     template <int I = 0>
     static __device__ __forceinline__ void cx(uint32_t& a, uint32_t& b) {
         const uint32_t l = min(a, b);
-        if constexpr (I % 3 == 0)
+        if constexpr (I % kPureEvery == 0)
             b = max(a, b);
         else
             b = fma_pipe_max(a, b, l);
@@ -97,7 +102,7 @@ struct Key<2> {  // two 16-bit keys per register (instance A low half, B high ha
     template <int I = 0>
     static __device__ __forceinline__ void cx(uint32_t& a, uint32_t& b) {
         const uint32_t l = __vminu2(a, b);
-        if constexpr (I % 3 == 0)
+        if constexpr (I % kPureEvery == 0)
             b = __vmaxu2(a, b);
         else
             b = fma_pipe_max(a, b, l);
