@@ -105,29 +105,33 @@ def cpu_baseline(cfg_name: str, seconds: float = 15.0):
     from oracle.oracle import Port, Ref
     alg, w, m, count, flags, _ = CONFIGS[cfg_name]
     note = ""
+    alg_id = ALG_ID.get(alg)
+    kind = {"partition_general": 1, "integer_sort_general": 0, "permute": 2}.get(alg)
     if cfg_name == "cfg2":
         # the reference rejects 32 x 8 (balance leftover group, partition.hpp:241-244): time the
         # closest shape it accepts, general partition 32 x 16
         m = 16
         note = "reference rejects 32x8 (ShapeViolation); timed its closest accepted general shape 32x16; "
+    if alg == "global_partition":
+        # no reference path partitions 2^32 keys (~137 GB of machine cells); its own 8-way partition
+        # of one 8 x 65536 instance (partition_short_wide, partition.hpp:178) is the stand-in
+        alg, alg_id, kind, w, m = "partition_short_wide", 3, 1, 8, 65536
+        note = "8-way partition stand-in: reference partition_short_wide on 8 x 65536 instances; "
     if not Ref.available():
         return None
     ref, port = Ref(), Port()
     import numpy as np
     nthreads = os.cpu_count() or 1
-    kind = 1 if alg == "partition_general" else 2
-    if alg == "integer_sort_general":
-        kind = 0
-    sample = 64
+    sample = 64 if w * m <= 4096 else nthreads
     # grow the sample until the run takes ~seconds/4 (bounded)
     while True:
         if kind == 0:
             inst = np.stack([port.gen_sort_u32(w, m, s) for s in range(sample)]).astype(np.uint32)
         else:
             inst = np.stack([port.gen_instance(kind, w, m, s) for s in range(sample)]).astype(np.uint32)
-        st, secs, good = ref.cpu_baseline(ALG_ID[alg], inst, seeds=np.arange(sample, dtype=np.uint64),
+        st, secs, good = ref.cpu_baseline(alg_id, inst, seeds=np.arange(sample, dtype=np.uint64),
                                           domain=1 << 32, nthreads=nthreads)
-        if secs * 4 >= seconds or sample >= (1 << 16):
+        if secs * 4 >= seconds or sample >= (1 << 16) or sample * w * m >= (1 << 26):
             break
         sample *= 2
     keys = sample * w * m
@@ -135,6 +139,18 @@ def cpu_baseline(cfg_name: str, seconds: float = 15.0):
             "sample": f"{note}{sample} instances of {w}x{m} through run_algorithm({alg}) "
                       f"(strict, auditor on, host_threads=1) on {nthreads} threads, {secs:.2f} s, "
                       f"{good}/{sample} correct"}
+
+
+def measured_traffic(cfg_name: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the config's dominant kernel,
+    from the committed ncu --set full capture (profiles/traffic.json, written by
+    profiles/ncu_summarize.py --traffic), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f).get(cfg_name)
+    except (OSError, ValueError):
+        return None
+    return t
 
 
 def run_reference(args):
@@ -301,6 +317,7 @@ def main():
         total_keys = keys_per_gpu * world
         value = total_keys / (ms_max / 1e3)
         bytes_per_launch = keys_per_gpu * 8  # algorithmic: one u32 read + one u32 write per key
+        traffic = measured_traffic(args.config)
         achieved = bytes_per_launch / (ms / 1e3) / 1e9
         line = {
             "metric": "keys/s", "value": value, "unit": "keys/s", "n_gpus": world, "steps": args.steps,
@@ -310,7 +327,9 @@ def main():
                        "keys_per_gpu": keys_per_gpu, "l2": "inputs 2x L2 (no flush needed)",
                        "parallelism": f"instances sharded over {world} GPU(s)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                         "frac": achieved / peaks["hbm_gbs"],
+                         "traffic": (traffic or {}).get("bytes_per_launch"),
+                         "traffic_source": (traffic or {}).get("source"),
                          "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
                          else "fallback 6650 GB/s"},
             "e2e": {"value": total_keys / (e2e_ms / 1e3), "unit": "keys/s",

@@ -1,5 +1,7 @@
 """Summarize an ncu --set full report: key raw metrics + per-source-line hot spots.
-usage: python profiles/ncu_summarize.py <report.ncu-rep> [top_n]"""
+usage: python profiles/ncu_summarize.py <report.ncu-rep> [top_n]
+       python profiles/ncu_summarize.py --traffic <cfg>=<report.ncu-rep> ... [--source-dir profiles/rNN]
+         -> merges {cfg: {kernel, bytes_per_launch, ...}} into profiles/traffic.json (read by bench.py)"""
 import csv
 import io
 import subprocess
@@ -67,5 +69,47 @@ def main():
     print("  stall reasons:", ", ".join(f"{k[6:]} {100 * v / tr:.0f}%" for k, v in agg.most_common(6)))
 
 
+def raw_metrics(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    return {h: (vals[i], units[i]) for i, h in enumerate(hdr)}
+
+
+def to_bytes(v, unit):
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[unit]
+    return float(v.replace(",", "")) * scale
+
+
+def traffic(args):
+    import json
+    import os
+    src_dir = None
+    if "--source-dir" in args:
+        i = args.index("--source-dir")
+        src_dir = args[i + 1]
+        args = args[:i] + args[i + 2:]
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "traffic.json")
+    try:
+        with open(path) as f:
+            out = json.load(f)
+    except OSError:
+        out = {}
+    for a in args:
+        cfg, rep = a.split("=", 1)
+        m = raw_metrics(rep)
+        rd = to_bytes(*m["dram__bytes_read.sum"])
+        wr = to_bytes(*m["dram__bytes_write.sum"])
+        out[cfg] = {"kernel": m["Kernel Name"][0][:120], "bytes_per_launch": rd + wr, "read_bytes": rd,
+                    "write_bytes": wr, "ncu_duration_us": float(m["gpu__time_duration.sum"][0].replace(",", "")),
+                    "source": os.path.join(src_dir or os.path.dirname(rep), os.path.basename(rep))}
+        print(cfg, out[cfg])
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "--traffic":
+        traffic(sys.argv[2:])
+    else:
+        main()
