@@ -33,6 +33,12 @@ struct PermArgs {
 };
 
 constexpr int kRngWords = 312;
+// warps (machines) per CTA: the kernel only synchronises warps, so small CTAs let the
+// per-warp shared-memory footprint, not the CTA granularity, set the occupancy
+#ifndef DMM_PERM_WARPS
+#define DMM_PERM_WARPS 4
+#endif
+constexpr int kPermWarps = DMM_PERM_WARPS;
 
 // Warp-shared generator: the 312-word state in smem as two 32-bit arrays (low and
 // high halves), so every warp-wide access is a unit-stride 32-bit access (no bank
@@ -214,11 +220,11 @@ __host__ __device__ constexpr int perm_stage_words() {
 }
 template <int M>
 __host__ __device__ constexpr int perm_warp_words() {  // u32 words of smem per warp
-    return 2 * kRngWords + M * 32 + perm_stage_words<M>() + M * 32;
+    return 2 * kRngWords + M * 32 + perm_stage_words<M>();
 }
 
 template <int M>
-__global__ void __launch_bounds__(128) k_permute(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+__global__ void __launch_bounds__(kPermWarps * 32) k_permute(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                                                  uint64_t count, const uint64_t* __restrict__ seeds,
                                                  const uint64_t* __restrict__ states, PermArgs a,
                                                  dmm_permute_report* __restrict__ reps, uint64_t* __restrict__ hist,
@@ -233,7 +239,8 @@ __global__ void __launch_bounds__(128) k_permute(const uint32_t* __restrict__ in
     WarpRng rng{wbase, wbase + kRngWords, 0};
     uint32_t* outs = wbase + 2 * kRngWords;     // output region, row i in bank i: outs[j*32 + i]
     uint32_t* stage = outs + M * 32;            // relayout buffer / own-bank rows A,B,H
-    uint32_t* pk = stage + perm_stage_words<M>();  // packed rows (own bank), capacity m
+    uint32_t* pk = stage + M * 32;                 // packed rows (own bank), capacity m: aliases B,
+                                                   // which is dead from packing until the finish
     uint32_t* H = stage;                           // per-colour counts, then bucket starts
     uint32_t* B = stage + M * 32;                  // colour-sorted (compacted) row
     const uint64_t k = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
@@ -292,15 +299,18 @@ __global__ void __launch_bounds__(128) k_permute(const uint32_t* __restrict__ in
 #pragma unroll
         for (int b = 0; b < M; ++b)
             H[b * 32 + lane] = 0;
+        // h(i) for the 32 source rows i: lane l evaluates h(l) once, keys fetch theirs by
+        // shuffle (one SHFL instead of a 64-bit splitmix64 per key)
+        const uint32_t h_lane = hash_eval(key, M, (uint32_t)lane);
         uint32_t col[M];
 #pragma unroll
         for (int c = 0; c < M; ++c) {
-            col[c] = 0;
-            if (x[c] != empty) {
-                const uint32_t i = x[c] / M, j = x[c] % M;
-                col[c] = (j + M - hash_eval(key, M, i)) % M;
+            const bool live = x[c] != empty;
+            const uint32_t i = live ? x[c] / M : 0u, j = x[c] % M;
+            const uint32_t hi = __shfl_sync(0xFFFFFFFFu, h_lane, (int)(i & 31u));
+            col[c] = live ? (j + M - hi) % M : 0u;
+            if (live)
                 H[col[c] * 32 + lane] += 1;
-            }
         }
         uint32_t run = 0;
         uint32_t lane_left = 0;
@@ -315,23 +325,21 @@ __global__ void __launch_bounds__(128) k_permute(const uint32_t* __restrict__ in
         for (int c = 0; c < M; ++c)
             if ((uint32_t)c >= run)
                 B[c * 32 + lane] = empty;
-        // scatter into the colour-sorted order; a label whose rank in its colour bucket is
-        // below alpha is delivered by the communication phase below
-        uint32_t rank[M];
+        // scatter into the colour-sorted order
 #pragma unroll
         for (int c = 0; c < M; ++c) {
-            rank[c] = 0xFFFFFFFFu;
             if (x[c] != empty) {
                 const uint32_t pos = H[col[c] * 32 + lane];
                 H[col[c] * 32 + lane] = pos + 1;
                 B[pos * 32 + lane] = x[c];
-                rank[c] = pos;
             }
         }
         // communication_phase permute.hpp:225-274.  Step (pass p, colour k): every row sends
         // its p-th label of colour k to out[i][j]; the output region keeps row i in bank i and
         // the colouring makes the destinations of one step distinct rows, so every step is one
         // conflict-free warp-wide store.  H holds the bucket ends now: start = end - count.
+        // A sent label's cell becomes empty in place (the compacted row keeps its holes):
+        // exactly the first min(count, alpha) cells of every colour bucket.
         for (int kc = 0; kc < M; ++kc) {
             const uint32_t end = H[kc * 32 + lane];
             const uint32_t start = kc == 0 ? 0u : H[(kc - 1) * 32 + lane];
@@ -339,17 +347,7 @@ __global__ void __launch_bounds__(128) k_permute(const uint32_t* __restrict__ in
             for (uint32_t p = 0; p < take; ++p) {
                 const uint32_t label = B[(start + p) * 32 + lane];
                 outs[(label % M) * 32 + label / M] = label;
-            }
-        }
-        // delivered cells become empty in place (the compacted row keeps its holes)
-#pragma unroll
-        for (int c = 0; c < M; ++c) {
-            const uint32_t pos = rank[c];
-            if (pos != 0xFFFFFFFFu) {
-                const uint32_t g = col[c];
-                const uint32_t start = g == 0 ? 0u : H[(g - 1) * 32 + lane];
-                if (pos - start < a.alpha)
-                    B[pos * 32 + lane] = empty;
+                B[(start + p) * 32 + lane] = empty;
             }
         }
 #pragma unroll
@@ -527,7 +525,7 @@ template <int M>
 dmm_status launch_permute(const uint32_t* in, uint32_t* out, uint64_t count, const uint64_t* seeds,
                           const uint64_t* states, const dmmdev::PermArgs& a, dmm_permute_report* reps, uint64_t* hist, uint32_t* shifts,
                           uint8_t* status, cudaStream_t s) {
-    constexpr int kWarps = 4;
+    constexpr int kWarps = dmmdev::kPermWarps;
     auto kern = dmmdev::k_permute<M>;
     const size_t smem = size_t(kWarps) * dmmdev::perm_warp_words<M>() * sizeof(uint32_t);
     static bool configured = false;
