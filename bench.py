@@ -180,6 +180,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--count", type=int, default=0, help="instances per GPU (default: the config's)")
+    ap.add_argument("--e2e-chunks", type=int, default=8, help="pipeline chunks of the end-to-end leg")
+    ap.add_argument("--e2e-streams", type=int, default=3, help="CUDA streams of the end-to-end leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -292,8 +294,8 @@ def main():
             res, _ = global_partition(din.view(-1))
             dout.view(-1).copy_(res)
 
-    chunks = 8 if alg != "global_partition" else 1
-    slots = run_pipelined(chunk_fn, h_in, h_out, chunks=chunks)  # warm-up (allocations)
+    chunks = args.e2e_chunks if alg != "global_partition" else 1
+    slots = run_pipelined(chunk_fn, h_in, h_out, chunks=chunks, nstreams=args.e2e_streams)  # warm-up
     torch.cuda.synchronize()
     barrier()
     ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
