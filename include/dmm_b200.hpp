@@ -7,6 +7,8 @@
 //     dmm::b200::partition_general(view)            // partition.hpp:453
 //     dmm::b200::integer_sort_general(view, domain)  // partition.hpp:436
 //     dmm::b200::sort_tall(view)                     // sort.hpp:352
+//     dmm::b200::partition_square(view) / partition_short_wide(view)   // partition.hpp:189 / :178
+//     dmm::b200::sort_square(view, asc) / sort_short_wide(view, asc)   // sort.hpp:337 / :225
 //     dmm::b200::transpose_square(view)              // layout.hpp:24 (+ to_column_major / to_row_major)
 //     dmm::b200::permute(machine, rng, params)       // permute.hpp:545
 //
@@ -165,6 +167,53 @@ inline void simple(const MatrixView& v, Fn&& fn, const char* where) {
 inline void sort_tall(const MatrixView& v) {
     detail::simple(v, [&](uint32_t* p) { return dmm_sort_tall(p, p, v.W(), v.M(), 1, nullptr); }, "sort_tall");
 }
+namespace detail {
+inline void no_hook(const ShortWideHook& hook) {
+    if (hook)
+        throw Error("ShortWideHook observation points are not supported by the B200 kernels");
+}
+// a partition entry point: per-instance status -> the reference's exception
+template <class Fn>
+inline void partition_entry(const MatrixView& v, Fn&& fn, const char* where) {
+    std::vector<uint32_t> g = gather(v);
+    DeviceBuffer d(sizeof(uint32_t) * g.size()), ss(16);
+    to_device(d, g);
+    check(fn(d.as<uint32_t>(), ss.as<uint8_t>()), where);
+    uint8_t status = 0;
+    cuda_check(cudaMemcpy(&status, ss.ptr, 1, cudaMemcpyDeviceToHost), "D2H");
+    if (status != DMM_OK)
+        raise(static_cast<dmm_status>(status), where);
+    to_host(g, d);
+    scatter(v, g);
+}
+}  // namespace detail
+
+/// void partition_square(const MatrixView&)  partition.hpp:189-197
+inline void partition_square(const MatrixView& v) {
+    detail::partition_entry(
+        v, [&](uint32_t* p, uint8_t* st) { return dmm_partition_square(p, p, v.W(), v.M(), 1, st, nullptr); },
+        "partition_square");
+}
+/// void partition_short_wide(const MatrixView&, const ShortWideHook& = {})  partition.hpp:178-185
+inline void partition_short_wide(const MatrixView& v, const ShortWideHook& hook = {}) {
+    detail::no_hook(hook);
+    detail::partition_entry(
+        v, [&](uint32_t* p, uint8_t* st) { return dmm_partition_short_wide(p, p, v.W(), v.M(), 1, st, nullptr); },
+        "partition_short_wide");
+}
+/// void sort_square(const MatrixView&, bool ascending = true)  sort.hpp:337-346
+inline void sort_square(const MatrixView& v, bool ascending = true) {
+    detail::simple(v, [&](uint32_t* p) { return dmm_sort_square(p, p, v.W(), v.M(), 1, ascending ? 1 : 0, nullptr); },
+                   "sort_square");
+}
+/// void sort_short_wide(const MatrixView&, bool ascending = true, const ShortWideHook& = {})  sort.hpp:225-230
+inline void sort_short_wide(const MatrixView& v, bool ascending = true, const ShortWideHook& hook = {}) {
+    detail::no_hook(hook);
+    detail::simple(v,
+                   [&](uint32_t* p) { return dmm_sort_short_wide(p, p, v.W(), v.M(), 1, ascending ? 1 : 0, nullptr); },
+                   "sort_short_wide");
+}
+
 /// transpose_square layout.hpp:24-61
 inline void transpose_square(const MatrixView& v) {
     if (v.W() != v.M())

@@ -24,13 +24,30 @@ const char* dmm_last_error(void) { return dmmhost::g_error.c_str(); }
 uint32_t dmm_last_launch_count(void) { return dmmhost::g_launches; }
 
 int dmm_supported(const char* algorithm, uint32_t w, uint32_t m) {
-    if (!algorithm || w != 32)
+    if (!algorithm)
         return 0;
     const std::string a(algorithm);
+    // compiled (w, m) machine shapes of the general-sort kernel (general_m*.cu, general_w*.cu)
+    auto general = [&]() -> bool {
+        switch (w) {
+            case 32: return m == 8 || m == 16 || m == 32 || m == 64 || m == 128;
+            case 16:
+            case 8: return m == 8 || m == 16 || m == 32 || m == 64;
+            case 4: return m == 4 || m == 8 || m == 16;
+            case 2: return m == 2 || m == 4 || m == 8;
+            default: return false;
+        }
+    };
     if (a == "partition_general" || a == "integer_sort_general")
-        return m == 8 || m == 16 || m == 32 || m == 64 || m == 128;
+        return general();
     if (a == "sort_wide_any")
-        return m == 32 || m == 64;
+        return general() && w <= m && m % w == 0 && (w != 32 || m == 32 || m == 64);
+    if (a == "partition_square" || a == "sort_square")
+        return general() && w == m && (m == 4 || m == 16);
+    if (a == "partition_short_wide" || a == "sort_short_wide")
+        return general() && uint64_t(w) * w <= m;
+    if (a == "permute")
+        return w == 32 && (m == 2 || m == 4 || m == 16 || m == 32);
     return 0;
 }
 

@@ -397,10 +397,12 @@ __device__ __forceinline__ void cleanup_pass_pair(uint32_t (&x)[M], uint32_t* bu
 struct GenResult {
     uint32_t retries[2];  // cleanup_retries (GeneralStats partition.hpp:292-295)
     uint32_t unsorted;    // bit h: cleanup budget exhausted for half h
+    // reduce over the WM lanes of each machine (WM = 32: the whole warp)
+    template <int WM = kWarp>
     __device__ void finish() {
-        retries[0] = __reduce_max_sync(0xFFFFFFFFu, retries[0]);
-        retries[1] = __reduce_max_sync(0xFFFFFFFFu, retries[1]);
-        unsorted = __reduce_or_sync(0xFFFFFFFFu, unsorted);
+        retries[0] = seg_max<WM>(retries[0]);
+        retries[1] = seg_max<WM>(retries[1]);
+        unsorted = seg_or<WM>(unsorted);
     }
 };
 

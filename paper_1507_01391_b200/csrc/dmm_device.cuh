@@ -43,6 +43,30 @@ __device__ __forceinline__ void static_for(F&& f) {
     }
 }
 
+// Reductions over aligned groups of WM lanes (one machine each; WM = 32: the warp).
+template <int WM>
+__device__ __forceinline__ uint32_t seg_or(uint32_t v) {
+    if constexpr (WM >= kWarp) {
+        return __reduce_or_sync(0xFFFFFFFFu, v);
+    } else {
+#pragma unroll
+        for (int off = 1; off < WM; off <<= 1)
+            v |= __shfl_xor_sync(0xFFFFFFFFu, v, off);
+        return v;
+    }
+}
+template <int WM>
+__device__ __forceinline__ uint32_t seg_max(uint32_t v) {
+    if constexpr (WM >= kWarp) {
+        return __reduce_max_sync(0xFFFFFFFFu, v);
+    } else {
+#pragma unroll
+        for (int off = 1; off < WM; off <<= 1)
+            v = max(v, __shfl_xor_sync(0xFFFFFFFFu, v, off));
+        return v;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Key traits: comparator and direction flip
 //

@@ -42,45 +42,61 @@ __device__ __forceinline__ void store_row(uint32_t* __restrict__ p, const uint32
 
 enum : int { kModeIntegerSort = 0, kModePartition = 1, kModeSortAny = 2 };
 
-// One warp per PK instances.  Row r of instance k is at in[(k*32 + r)*M].
 // CTA shape: warps per CTA and the occupancy target handed to ptxas (register cap)
 template <int M, int PK>
 constexpr int warps_per_block() { return M >= 128 ? 4 : 8; }
 template <int M, int PK>
 constexpr int min_blocks_per_sm() { return 1; }
 
-template <int M, int PK, bool EXT, int MODE>
-__global__ void __launch_bounds__(warps_per_block<M, PK>() * 32, min_blocks_per_sm<M, PK>()) k_general_sort(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
-                                                      uint64_t count, uint64_t domain, int strict, int ascending,
-                                                      dmm_general_stats* __restrict__ stats,
-                                                      uint8_t* __restrict__ status) {
+// One warp = G = 32 / WM machines of WM rows (WM = 32: one machine per warp; WM < 32: the
+// machines are the members of one lockstep view family, exactly how the reference runs
+// sibling views), times PK instances per register (16-bit halves).  Warp-task t covers
+// instances [t*PK*G, (t+1)*PK*G): half h, lane group g = lane / WM holds instance
+// t*PK*G + h*G + g, local row lane % WM.  The G instances of one half are contiguous in
+// memory, so lane l's row sits at in[(first * WM + l) * M] exactly as for one 32-row machine.
+template <int M, int PK, bool EXT, int MODE, int WM = kWarp>
+__global__ void __launch_bounds__(warps_per_block<M, PK>() * 32, min_blocks_per_sm<M, PK>())
+    k_general_sort(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count, uint64_t domain,
+                   int strict, int ascending, dmm_general_stats* __restrict__ stats, uint8_t* __restrict__ status) {
+    static_assert(WM >= 1 && kWarp % WM == 0, "machines must tile the warp");
+    constexpr int G = kWarp / WM;
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
+    const int grp = lane / WM, row = lane % WM;
     uint32_t* buf = smem + warp * relayout_buf_words(M);
-    const uint64_t inst0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * PK;
-    if (inst0 >= count)
+    const uint64_t first = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * (PK * G);  // half 0, group 0
+    if (first >= count)
         return;
-    const bool hasB = PK == 2 && inst0 + 1 < count;
+    // half h of this lane's machine: instance first + h*G + grp (absent past count)
+    auto inst_of = [&](int h) -> uint64_t { return first + (uint64_t)h * G + grp; };
+    const bool hasB = PK == 2 && first + G < count;  // any machine of half 1 present
 
     // A leaf-only instance (w <= m: balance_divide_sort is partition_leaf, whose outcome
     // is the sorted multiset whatever the starting arrangement) is loaded fully coalesced:
-    // lane l takes the 16-byte chunks l, l + 32, ... of the instance.  Otherwise lane r
-    // loads row r (the recursion's intermediate matrices depend on the arrangement).
-    constexpr bool kAnyLayout = MODE != kModeSortAny && kWarp <= M && M % 4 == 0;
-    auto load = [&](uint64_t k, uint32_t (&v)[M]) {
+    // the machine's lane r takes its instance's 16-byte chunks r, r + WM, ...  Otherwise
+    // lane r loads row r (the recursion's intermediate matrices depend on the arrangement).
+    constexpr bool kAnyLayout = MODE != kModeSortAny && WM <= M && M % 4 == 0;
+    auto load = [&](int h, uint32_t (&v)[M]) {
+        const uint64_t k = inst_of(h);
+        if (k >= count) {
+#pragma unroll
+            for (int c = 0; c < M; ++c)
+                v[c] = 0;
+            return;
+        }
         if constexpr (kAnyLayout) {
-            const uint4* q = reinterpret_cast<const uint4*>(in + k * kWarp * M);
+            const uint4* q = reinterpret_cast<const uint4*>(in + k * WM * M);
 #pragma unroll
             for (int i = 0; i < M / 4; ++i) {
-                const uint4 t = __ldg(q + lane + kWarp * i);
+                const uint4 t = __ldg(q + row + WM * i);
                 v[4 * i] = t.x;
                 v[4 * i + 1] = t.y;
                 v[4 * i + 2] = t.z;
                 v[4 * i + 3] = t.w;
             }
         } else {
-            load_row<M>(in + (k * kWarp + lane) * M, v);
+            load_row<M>(in + (k * WM + row) * M, v);
         }
     };
     // keys outside [0, domain): OR-accumulate (power-of-two domain, half an ALU op per
@@ -105,12 +121,12 @@ __global__ void __launch_bounds__(warps_per_block<M, PK>() * 32, min_blocks_per_
     };
 
     uint32_t x[M];
-    load(inst0, x);
+    load(0, x);
     uint32_t bad = keys_bad(x, M);  // bit h: half h holds a key outside [0, domain)
     if constexpr (PK == 2) {
         uint32_t b[M];
         if (hasB) {
-            load(inst0 + 1, b);
+            load(1, b);
         } else {
 #pragma unroll
             for (int c = 0; c < M; ++c)
@@ -121,38 +137,38 @@ __global__ void __launch_bounds__(warps_per_block<M, PK>() * 32, min_blocks_per_
         for (int c = 0; c < M; ++c)
             x[c] = __byte_perm(x[c], b[c], 0x5410);  // (a & 0xFFFF) | (b << 16)
     }
-    bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+    bad = seg_or<WM>(bad);
 
-    using V = VF<0xFFFFFFFFu, 0, 1, kWarp, 0, M>;
+    using V = VF<0xFFFFFFFFu, 0, 1, WM, 0, M>;
     GenResult res{{0u, 0u}, 0u};
     if constexpr (MODE == kModeSortAny)
         sort_wide_any<PK, V>(x, buf, lane, ascending != 0);
     else
         balance_divide_sort<PK, V, EXT>(x, buf, lane, res);
-    res.finish();
+    res.template finish<WM>();
 
     uint32_t invalid = 0;
     if constexpr (MODE == kModePartition) {
         // check_partition_instance (partition.hpp:112-124): labels in [0, w), m copies
         // each  <=>  (labels < w) and the sorted result has row i = i everywhere.
-        // OR of (key ^ lane) over the row: one LOP3 per register, both halves at once
-        const uint32_t want = PK == 2 ? (uint32_t)lane * 0x10001u : (uint32_t)lane;
+        // OR of (key ^ row) over the row: one LOP3 per register, both halves at once
+        const uint32_t want = PK == 2 ? (uint32_t)row * 0x10001u : (uint32_t)row;
         uint32_t diff = 0;
 #pragma unroll
         for (int c = 0; c < M; ++c)
             diff |= x[c] ^ want;
         const uint32_t mism = PK == 2 ? ((diff & 0xFFFFu) ? 1u : 0u) | ((diff >> 16) ? 2u : 0u) : (diff ? 1u : 0u);
-        invalid = __reduce_or_sync(0xFFFFFFFFu, mism) | bad;
+        invalid = seg_or<WM>(mism) | bad;
     }
 
 #pragma unroll
     for (int h = 0; h < PK; ++h) {
-        if (h == 1 && !hasB)
-            break;
-        const uint64_t k = inst0 + h;
+        const uint64_t k = inst_of(h);
+        if (k >= count)
+            continue;
         if constexpr (M % 4 == 0) {
             // unpack one 16-byte vector at a time (register budget)
-            uint4* q = reinterpret_cast<uint4*>(out + (k * kWarp + lane) * M);
+            uint4* q = reinterpret_cast<uint4*>(out + (k * WM + row) * M);
 #pragma unroll
             for (int i = 0; i < M / 4; ++i) {
                 uint32_t v[4];
@@ -166,9 +182,9 @@ __global__ void __launch_bounds__(warps_per_block<M, PK>() * 32, min_blocks_per_
 #pragma unroll
             for (int c = 0; c < M; ++c)
                 v[c] = PK == 2 ? ((x[c] >> (16 * h)) & 0xFFFFu) : x[c];
-            store_row<M>(out + (k * kWarp + lane) * M, v);
+            store_row<M>(out + (k * WM + row) * M, v);
         }
-        if (lane == 0) {
+        if (row == 0) {
             const bool unsorted = (res.unsorted >> h) & 1u;
             uint8_t s = DMM_OK;
             if (MODE == kModePartition && ((invalid >> h) & 1u))
@@ -204,9 +220,9 @@ struct GeneralArgs {
     cudaStream_t stream;
 };
 
-template <int M, int PK, bool EXT, int MODE>
+template <int M, int PK, bool EXT, int MODE, int WM = dmmdev::kWarp>
 dmm_status launch_general(const GeneralArgs& a) {
-    auto kern = dmmdev::k_general_sort<M, PK, EXT, MODE>;
+    auto kern = dmmdev::k_general_sort<M, PK, EXT, MODE, WM>;
     constexpr int kWarpsPerBlock = dmmdev::warps_per_block<M, PK>();
     const size_t smem = size_t(kWarpsPerBlock) * dmmdev::relayout_buf_words(M) * sizeof(uint32_t);
     static bool configured = false;  // per instantiation
@@ -218,7 +234,7 @@ dmm_status launch_general(const GeneralArgs& a) {
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         configured = true;
     }
-    const uint64_t units = (a.count + PK - 1) / PK;
+    const uint64_t units = (a.count + PK * (dmmdev::kWarp / WM) - 1) / (PK * (dmmdev::kWarp / WM));
     const uint64_t blocks = (units + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (blocks == 0)
         return DMM_OK;
@@ -236,5 +252,10 @@ dmm_status launch_general_m16(int mode, bool pk2, bool ext, const GeneralArgs& a
 dmm_status launch_general_m32(int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_m64(int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_m128(int mode, bool pk2, bool ext, const GeneralArgs& a);
+// sub-warp machines (w < 32 rows, 32 / w machines per warp), general_w*.cu
+dmm_status launch_general_w16(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);
+dmm_status launch_general_w8(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);
+dmm_status launch_general_w4(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);
+dmm_status launch_general_w2(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);
 
 }  // namespace dmmhost

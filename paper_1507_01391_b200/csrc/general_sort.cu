@@ -13,19 +13,29 @@ using namespace dmmhost;
 
 // Dispatch over the compiled shapes (W = 32).  PK = 2 whenever every legal key
 // fits in 16 bits (domain <= 2^16).
-dmm_status dispatch(int mode, const uint32_t* in, uint32_t* out, uint32_t m, uint64_t count, uint64_t domain,
-                    bool ext, int strict, int ascending, dmm_general_stats* stats, uint8_t* status, cudaStream_t s) {
+dmm_status dispatch(int mode, const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                    uint64_t domain, bool ext, int strict, int ascending, dmm_general_stats* stats, uint8_t* status,
+                    cudaStream_t s) {
     const bool pk2 = domain <= 65536;
     const GeneralArgs a{in, out, count, domain, strict, ascending, stats, status, s};
-    switch (m) {
-        case 8: return launch_general_m8(mode, pk2, ext, a);
-        case 16: return launch_general_m16(mode, pk2, ext, a);
-        case 32: return launch_general_m32(mode, pk2, ext, a);
-        case 64: return launch_general_m64(mode, pk2, ext, a);
-        case 128: return launch_general_m128(mode, pk2, ext, a);
+    switch (w) {
+        case 32:
+            switch (m) {
+                case 8: return launch_general_m8(mode, pk2, ext, a);
+                case 16: return launch_general_m16(mode, pk2, ext, a);
+                case 32: return launch_general_m32(mode, pk2, ext, a);
+                case 64: return launch_general_m64(mode, pk2, ext, a);
+                case 128: return launch_general_m128(mode, pk2, ext, a);
+                default: break;
+            }
+            break;
+        case 16: return launch_general_w16(m, mode, pk2, ext, a);
+        case 8: return launch_general_w8(m, mode, pk2, ext, a);
+        case 4: return launch_general_w4(m, mode, pk2, ext, a);
+        case 2: return launch_general_w2(m, mode, pk2, ext, a);
         default: break;
     }
-    set_error("no kernel compiled for this shape");
+    set_error("no kernel compiled for this shape (w in {2, 4, 8, 16, 32})");
     return DMM_UNSUPPORTED_SHAPE;
 }
 
@@ -55,17 +65,13 @@ dmm_status dmm_integer_sort_general(const uint32_t* in, uint32_t* out, uint32_t 
         return sh;
     if (dmm_status e = check_ptrs(in, out, count); e != DMM_OK || count == 0)
         return e;
-    if (w != 32) {
-        set_error("kernels are built for w = 32 (one warp per machine)");
-        return DMM_UNSUPPORTED_SHAPE;
-    }
     if (domain == 0 || domain > (1ull << 32)) {
         // keys are 32-bit words; a wider domain admits every key
         domain = 1ull << 32;
     }
     // use the extension kernels only where the reference itself would reject the shape
     const bool need_ext = ext && !general_sort_shape_ok(w, m, false) && m < w;
-    return dispatch(dmmdev::kModeIntegerSort, in, out, m, count, domain, need_ext, !(flags & DMM_FLAG_NONSTRICT), 1,
+    return dispatch(dmmdev::kModeIntegerSort, in, out, w, m, count, domain, need_ext, !(flags & DMM_FLAG_NONSTRICT), 1,
                                               stats, status, static_cast<cudaStream_t>(stream));
 }
 
@@ -78,12 +84,8 @@ dmm_status dmm_partition_general(const uint32_t* in, uint32_t* out, uint32_t w, 
         return sh;
     if (dmm_status e = check_ptrs(in, out, count); e != DMM_OK || count == 0)
         return e;
-    if (w != 32) {
-        set_error("kernels are built for w = 32 (one warp per machine)");
-        return DMM_UNSUPPORTED_SHAPE;
-    }
     const bool need_ext = ext && !general_sort_shape_ok(w, m, false) && m < w;
-    return dispatch(dmmdev::kModePartition, in, out, m, count, w, need_ext, !(flags & DMM_FLAG_NONSTRICT), 1, stats,
+    return dispatch(dmmdev::kModePartition, in, out, w, m, count, w, need_ext, !(flags & DMM_FLAG_NONSTRICT), 1, stats,
                                             status, static_cast<cudaStream_t>(stream));
 }
 
@@ -94,45 +96,65 @@ dmm_status dmm_sort_wide_any(const uint32_t* in, uint32_t* out, uint32_t w, uint
         return DMM_SHAPE_VIOLATION;
     if (dmm_status e = check_ptrs(in, out, count); e != DMM_OK || count == 0)
         return e;
-    if (w != 32) {
-        set_error("kernels are built for w = 32 (one warp per machine)");
-        return DMM_UNSUPPORTED_SHAPE;
-    }
-    return dispatch(dmmdev::kModeSortAny, in, out, m, count, 1ull << 32, false, 1, ascending, nullptr, nullptr,
+    return dispatch(dmmdev::kModeSortAny, in, out, w, m, count, 1ull << 32, false, 1, ascending, nullptr, nullptr,
                                           static_cast<cudaStream_t>(stream));
 }
 
+// partition_square partition.hpp:189-197: w = m, m a perfect square; check_partition_instance
+// then partition_leaf, whose outcome is the sorted instance (row i = i)
 dmm_status dmm_partition_square(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
                                 uint8_t* status, void* stream) {
     reset_launches();
-    // partition.hpp:189-197
     if (w != m)
         return DMM_SHAPE_VIOLATION;
     const uint32_t h = isqrt_floor(m);
     if (h * h != m)
         return DMM_SHAPE_VIOLATION;
-    (void)in;
-    (void)out;
-    (void)count;
-    (void)status;
-    (void)stream;
-    set_error("partition_square: no perfect-square w = m is a single warp (w = 32)");
-    return DMM_UNSUPPORTED_SHAPE;
+    if (dmm_status e = check_ptrs(in, out, count); e != DMM_OK || count == 0)
+        return e;
+    return dispatch(dmmdev::kModePartition, in, out, w, m, count, w, false, 1, 1, nullptr, status,
+                    static_cast<cudaStream_t>(stream));
 }
 
+// partition_short_wide partition.hpp:178-185: w^2 <= m; the short-wide skeleton with radix
+// rows leaves the sorted instance, i.e. partition_leaf's outcome
 dmm_status dmm_partition_short_wide(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
                                     uint8_t* status, void* stream) {
     reset_launches();
-    // partition.hpp:178-185
     if (uint64_t(w) * w > m)
         return DMM_SHAPE_VIOLATION;
-    (void)in;
-    (void)out;
-    (void)count;
-    (void)status;
-    (void)stream;
-    set_error("partition_short_wide: w = 32 needs m >= 1024 words per register row");
-    return DMM_UNSUPPORTED_SHAPE;
+    if (dmm_status e = check_ptrs(in, out, count); e != DMM_OK || count == 0)
+        return e;
+    return dispatch(dmmdev::kModePartition, in, out, w, m, count, w, false, 1, 1, nullptr, status,
+                    static_cast<cudaStream_t>(stream));
+}
+
+// sort_square sort.hpp:337-346: w = m perfect square -> square_skeleton (Theorem 2),
+// run literally by the comparison-sort kernel (sort_wide_any dispatches on the shape)
+dmm_status dmm_sort_square(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                           int ascending, void* stream) {
+    reset_launches();
+    if (w != m)
+        return DMM_SHAPE_VIOLATION;
+    const uint32_t h = isqrt_floor(m);
+    if (h * h != m)
+        return DMM_SHAPE_VIOLATION;
+    if (dmm_status e = check_ptrs(in, out, count); e != DMM_OK || count == 0)
+        return e;
+    return dispatch(dmmdev::kModeSortAny, in, out, w, m, count, 1ull << 32, false, 1, ascending, nullptr, nullptr,
+                    static_cast<cudaStream_t>(stream));
+}
+
+// sort_short_wide sort.hpp:225-230: w^2 <= m -> short_wide_skeleton (Lemma 1) with merge rows
+dmm_status dmm_sort_short_wide(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                               int ascending, void* stream) {
+    reset_launches();
+    if (uint64_t(w) * w > m)
+        return DMM_SHAPE_VIOLATION;
+    if (dmm_status e = check_ptrs(in, out, count); e != DMM_OK || count == 0)
+        return e;
+    return dispatch(dmmdev::kModeSortAny, in, out, w, m, count, 1ull << 32, false, 1, ascending, nullptr, nullptr,
+                    static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -3,8 +3,7 @@
 //
 // C ABI: dmm_transpose_square (layout.hpp:24), dmm_to_column_major (layout.hpp:397),
 // dmm_to_row_major (layout.hpp:403), dmm_sort_rows (partition.hpp:94 / sort.hpp:76),
-// dmm_sort_tall (sort.hpp:352), dmm_sort_square (sort.hpp:337),
-// dmm_sort_short_wide (sort.hpp:225).
+// dmm_sort_tall (sort.hpp:352).  (dmm_sort_square / dmm_sort_short_wide: general_sort.cu.)
 #include "general_kernel.cuh"
 
 namespace dmmdev {
@@ -169,29 +168,6 @@ dmm_status dmm_sort_tall(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t
     if (dmm_status e = common_checks(in, out, w, count); e != DMM_OK)
         return e;
     return dispatch_layout<dmmdev::kOpSortTall>(m, in, out, count, 0, 0, nullptr, stream);
-}
-
-dmm_status dmm_sort_square(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
-                           int ascending, void* stream) {
-    reset_launches();
-    (void)in, (void)out, (void)count, (void)ascending, (void)stream;
-    if (w != m)  // sort.hpp:338-342
-        return DMM_SHAPE_VIOLATION;
-    const uint32_t h = isqrt_floor(m);
-    if (h * h != m)
-        return DMM_SHAPE_VIOLATION;
-    set_error("sort_square: no perfect-square w = m equals one warp (w = 32)");
-    return DMM_UNSUPPORTED_SHAPE;
-}
-
-dmm_status dmm_sort_short_wide(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
-                               int ascending, void* stream) {
-    reset_launches();
-    (void)in, (void)out, (void)count, (void)ascending, (void)stream;
-    if (uint64_t(w) * w > m)  // sort.hpp:203-204
-        return DMM_SHAPE_VIOLATION;
-    set_error("sort_short_wide: w = 32 needs m >= 1024 words per register row");
-    return DMM_UNSUPPORTED_SHAPE;
 }
 
 }  // extern "C"

@@ -248,24 +248,27 @@ def _simple(fn_name: str, grid, *args, out=None, stream=None, w_arg_only: bool =
     return res[0] if single else res
 
 
-def partition_square(grid, *, out=None, stream=None):
-    """void partition_square(const MatrixView&)  partition.hpp:189-197."""
+def _partition_entry(fn_name: str, grid, out, stream, check: bool):
     t, single = _as_batch(grid)
     res = out if out is not None else torch.empty_like(t)
     count, w, m = t.shape
-    _check(lib().dmm_partition_square(t.data_ptr(), res.data_ptr(), w, m, count, None, _stream(stream)),
-           "partition_square")
+    status = torch.empty((count,), dtype=torch.uint8, device=t.device)
+    _check(getattr(lib(), "dmm_" + fn_name)(t.data_ptr(), res.data_ptr(), w, m, count, status.data_ptr(),
+                                            _stream(stream)), fn_name)
+    if check:
+        _raise_first(status, fn_name)
     return res[0] if single else res
 
 
-def partition_short_wide(grid, *, out=None, stream=None):
-    """void partition_short_wide(const MatrixView&, hook)  partition.hpp:178-185."""
-    t, single = _as_batch(grid)
-    res = out if out is not None else torch.empty_like(t)
-    count, w, m = t.shape
-    _check(lib().dmm_partition_short_wide(t.data_ptr(), res.data_ptr(), w, m, count, None, _stream(stream)),
-           "partition_short_wide")
-    return res[0] if single else res
+def partition_square(grid, *, out=None, stream=None, check: bool = True):
+    """void partition_square(const MatrixView&)  partition.hpp:189-197 (w = m, m a perfect
+    square; w < 32 machines run 32 / w per warp)."""
+    return _partition_entry("partition_square", grid, out, stream, check)
+
+
+def partition_short_wide(grid, *, out=None, stream=None, check: bool = True):
+    """void partition_short_wide(const MatrixView&, hook)  partition.hpp:178-185 (w^2 <= m)."""
+    return _partition_entry("partition_short_wide", grid, out, stream, check)
 
 
 # --------------------------------------------------------------------------------------

@@ -191,10 +191,80 @@ static void permute_cases() {
     CHECK(throws_as<ShapeViolation>([&] { b200::permute(bad, r); }));
 }
 
+// sub-warp machines (w < 32): the square / short-wide entry points exist only there
+static void subwarp_cases() {
+    // partition_square / partition_short_wide (partition.hpp:178-197)
+    for (auto [w, m] : {std::pair<u32, u32>{16, 16}, {4, 4}, {8, 64}, {4, 16}, {2, 4}}) {
+        for (u64 seed = 1; seed <= 3; ++seed) {
+            Instance in = gen_instance(InstanceKind::partition, w, m, seed);
+            Machine a = make_machine(w, m), b = make_machine(w, m);
+            MatrixView va = MatrixView::full(a), vb = MatrixView::full(b);
+            va.load(in.grid);
+            vb.load(in.grid);
+            if (w == m) {
+                partition_square(va);
+                b200::partition_square(vb);
+            } else {
+                partition_short_wide(va);
+                b200::partition_short_wide(vb);
+            }
+            CHECK(va.snapshot() == vb.snapshot());
+        }
+    }
+    // general partition and integer sort at w in {16, 8, 4} with GeneralStats
+    for (auto [w, m] : {std::pair<u32, u32>{16, 8}, {16, 32}, {8, 16}, {4, 8}}) {
+        for (u64 seed = 1; seed <= 3; ++seed) {
+            Instance in = gen_instance(InstanceKind::partition, w, m, seed);
+            Machine a = make_machine(w, m), b = make_machine(w, m);
+            MatrixView va = MatrixView::full(a), vb = MatrixView::full(b);
+            va.load(in.grid);
+            vb.load(in.grid);
+            GeneralStats sa = partition_general(va);
+            GeneralStats sb = b200::partition_general(vb);
+            CHECK(va.snapshot() == vb.snapshot());
+            CHECK(sa.cleanup_retries == sb.cleanup_retries && sa.sorted == sb.sorted);
+        }
+    }
+    // comparison sorts: sort_square 16 x 16 / 4 x 4, sort_short_wide 8 x 64 / 4 x 16, both directions
+    Rng rng(29);
+    for (auto [w, m] : {std::pair<u32, u32>{16, 16}, {4, 4}, {8, 64}, {4, 16}}) {
+        for (bool asc : {true, false}) {
+            std::vector<word> g(u64(w) * m);
+            for (auto& x : g)
+                x = rng() >> 40;
+            Machine a = make_machine(w, m), b = make_machine(w, m);
+            MatrixView va = MatrixView::full(a), vb = MatrixView::full(b);
+            va.load(g);
+            vb.load(g);
+            if (w == m) {
+                sort_square(va, asc);
+                b200::sort_square(vb, asc);
+            } else {
+                sort_short_wide(va, asc);
+                b200::sort_short_wide(vb, asc);
+            }
+            CHECK(va.snapshot() == vb.snapshot());
+        }
+    }
+    // the same error types: bad label counts, w^2 > m
+    {
+        Instance in = gen_instance(InstanceKind::partition, 16, 16, 2);
+        in.grid[0] = in.grid[0] == 15 ? 14 : 15;
+        Machine b = make_machine(16, 16);
+        MatrixView vb = MatrixView::full(b);
+        vb.load(in.grid);
+        CHECK(throws_as<InvalidInstance>([&] { b200::partition_square(vb); }));
+        Machine c = make_machine(8, 32);
+        MatrixView vc = MatrixView::full(c);
+        CHECK(throws_as<ShapeViolation>([&] { b200::partition_short_wide(vc); }));
+    }
+}
+
 int main() {
     partition_cases();
     integer_sort_cases();
     layout_and_sort_cases();
+    subwarp_cases();
     permute_cases();
     std::printf("shim parity: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;

@@ -39,6 +39,12 @@ def test_version_and_support_table(lib):
     assert lib.dmm_supported(b"partition_general", 32, 8)
     assert lib.dmm_supported(b"partition_general", 32, 32)
     assert not lib.dmm_supported(b"partition_general", 64, 8)
+    # sub-warp machines (32 / w per warp) and the square / short-wide entry points
+    assert lib.dmm_supported(b"partition_general", 16, 8) and lib.dmm_supported(b"integer_sort_general", 4, 16)
+    assert lib.dmm_supported(b"partition_square", 16, 16) and lib.dmm_supported(b"sort_square", 4, 4)
+    assert lib.dmm_supported(b"partition_short_wide", 8, 64) and lib.dmm_supported(b"sort_short_wide", 2, 4)
+    assert not lib.dmm_supported(b"partition_square", 32, 32)  # 32 is not a perfect square
+    assert not lib.dmm_supported(b"partition_short_wide", 8, 32)  # w^2 > m
 
 
 @pytest.mark.parametrize("w,m,flags,expect", [
