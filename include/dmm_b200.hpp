@@ -19,7 +19,9 @@
 // host code after the call sees the same stream as with the reference.
 //
 // Not reproduced (GPU kernels have no DMM step meter): Machine::steps()/work() do not
-// advance; PartitionProbe hooks and traces are unsupported (Error); permute() reproduces
+// advance; PartitionProbe hooks are replayed from the kernel's snapshots (the caller's
+// machine holds the reference's window at each call); ShortWideHook and traces are
+// unsupported (Error); permute() reproduces
 // the output region, the report and the Rng position, not the scratch/counter cells.
 // Words must fit in 32 bits (KeyOutOfRange otherwise).  Requires <dmm/dmm.hpp>.
 #pragma once
@@ -103,14 +105,44 @@ inline void scatter(const MatrixView& v, const std::vector<uint32_t>& g) {
             v.machine().poke(v.bank(r), v.off(c), g[u64(r) * v.M() + c]);
 }
 
-inline void no_probe(const PartitionProbe* probe) {
-    if (probe && (probe->after_balance || probe->after_divide))
-        throw Error("PartitionProbe hooks are not supported by the B200 kernels");
+inline bool wants_probe(const PartitionProbe* probe) {
+    return probe && (probe->after_balance || probe->after_divide);
+}
+
+// Replays the reference's hook calls (partition.hpp:373-391) from the kernel's snapshots: the
+// caller's machine holds, at each call, the window the reference would hold, and the hook gets
+// the same list of views (balance level / convert_and_divide row ranges, built host-side).
+inline void replay_probe(const MatrixView& v, const PartitionProbe& probe, const std::vector<uint32_t>& snaps,
+                         uint32_t nsnaps) {
+    const u64 cells = u64(v.W()) * v.M();
+    auto show = [&](uint32_t i) {
+        if (i < nsnaps)
+            scatter(v, std::vector<uint32_t>(snaps.begin() + i * cells, snaps.begin() + (i + 1) * cells));
+    };
+    std::vector<MatrixView> level{v};
+    u32 depth = 0;
+    uint32_t i = 0;
+    while (level.front().W() > v.M()) {
+        show(i++);
+        if (probe.after_balance)
+            probe.after_balance(depth, level);
+        const PartitionParams p = PartitionParams::compute(level.front().W(), v.M());
+        std::vector<MatrixView> next;
+        for (const MatrixView& lv : level) {
+            const u32 h = lv.W() / p.subproblems;
+            for (u32 k = 0; k < p.subproblems; ++k)
+                next.push_back(lv.row_range(k * h, h));
+        }
+        level.swap(next);
+        ++depth;
+        show(i++);
+        if (probe.after_divide)
+            probe.after_divide(depth, level);
+    }
 }
 
 inline GeneralStats general_impl(bool partition, const MatrixView& v, u64 domain, bool enforce,
                                  const PartitionProbe* probe) {
-    no_probe(probe);
     std::vector<uint32_t> g = gather(v);
     const uint64_t bytes = sizeof(uint32_t) * g.size();
     DeviceBuffer d(bytes), st(sizeof(dmm_general_stats)), ss(16);
@@ -120,27 +152,43 @@ inline GeneralStats general_impl(bool partition, const MatrixView& v, u64 domain
         flags |= DMM_FLAG_NONSTRICT;
     if (!enforce)
         flags |= DMM_FLAG_NO_ENFORCE_PRE;
-    const dmm_status s =
-        partition ? dmm_partition_general(d.as<uint32_t>(), d.as<uint32_t>(), v.W(), v.M(), 1, flags,
-                                          st.as<dmm_general_stats>(), ss.as<uint8_t>(), nullptr)
-                  : dmm_integer_sort_general(d.as<uint32_t>(), d.as<uint32_t>(), v.W(), v.M(), 1, domain, flags,
-                                             st.as<dmm_general_stats>(), ss.as<uint8_t>(), nullptr);
-    check(s, partition ? "partition_general" : "integer_sort_general");
+    const bool probing = wants_probe(probe);
+    const uint32_t nsnaps = probing ? dmm_general_probe_snaps(v.W(), v.M(), flags) : 0;
+    DeviceBuffer dsnap(sizeof(uint32_t) * (nsnaps ? nsnaps * g.size() : 1));
+    const char* where = partition ? "partition_general" : "integer_sort_general";
+    dmm_status s;
+    if (partition)
+        s = dmm_partition_general_probe(d.as<uint32_t>(), d.as<uint32_t>(), v.W(), v.M(), 1, flags,
+                                        st.as<dmm_general_stats>(), ss.as<uint8_t>(), dsnap.as<uint32_t>(), nsnaps,
+                                        nullptr);
+    else
+        s = dmm_integer_sort_general_probe(d.as<uint32_t>(), d.as<uint32_t>(), v.W(), v.M(), 1, domain, flags,
+                                           st.as<dmm_general_stats>(), ss.as<uint8_t>(), dsnap.as<uint32_t>(),
+                                           nsnaps, nullptr);
+    check(s, where);
     dmm_general_stats hs{};
     uint8_t status = 0;
     cuda_check(cudaMemcpy(&hs, st.ptr, sizeof(hs), cudaMemcpyDeviceToHost), "D2H");
     cuda_check(cudaMemcpy(&status, ss.ptr, 1, cudaMemcpyDeviceToHost), "D2H");
-    if (status != DMM_OK)
-        raise(static_cast<dmm_status>(status), partition ? "partition_general" : "integer_sort_general");
+    // input validation fails before the recursion (no hook calls); a failed cleanup after it
+    if (status == DMM_INVALID_INSTANCE || status == DMM_KEY_OUT_OF_RANGE)
+        raise(static_cast<dmm_status>(status), where);
+    if (probing && nsnaps) {
+        std::vector<uint32_t> snaps(u64(nsnaps) * g.size());
+        to_host(snaps, dsnap);
+        replay_probe(v, *probe, snaps, nsnaps);
+    }
     to_host(g, d);
     scatter(v, g);
+    if (status != DMM_OK)
+        raise(static_cast<dmm_status>(status), where);
     GeneralStats out;
     out.cleanup_retries = hs.cleanup_retries;
     out.sorted = hs.sorted != 0;
     return out;
 }
 
-/// GeneralStats partition_general(const MatrixView&)  partition.hpp:453-456
+/// GeneralStats partition_general(const MatrixView&, const PartitionProbe* = nullptr)  partition.hpp:453-456
 inline GeneralStats partition_general(const MatrixView& v, const PartitionProbe* probe = nullptr) {
     return general_impl(true, v, v.W(), true, probe);
 }

@@ -86,6 +86,20 @@ dmm_status dmm_integer_sort_general(const uint32_t* in, uint32_t* out, uint32_t 
                                     uint64_t domain, uint32_t flags, dmm_general_stats* stats, uint8_t* status,
                                     void* stream);
 
+/* PartitionProbe capture (partition.hpp:298-301, called at :376-390): the same two calls,
+ * additionally writing the full w x m working window after every balance (after_balance)
+ * and every convert-and-divide (after_divide) of the outer recursion, in hook order, to
+ * snapshots[k * max_snaps * w * m ...] for instance k (max_snaps per instance; extra
+ * snapshots are dropped).  dmm_general_probe_snaps(w, m, flags) = the number the recursion
+ * takes for that shape (0 when w <= m). */
+uint32_t dmm_general_probe_snaps(uint32_t w, uint32_t m, uint32_t flags);
+dmm_status dmm_partition_general_probe(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                       uint32_t flags, dmm_general_stats* stats, uint8_t* status, uint32_t* snapshots,
+                                       uint32_t max_snaps, void* stream);
+dmm_status dmm_integer_sort_general_probe(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                          uint64_t domain, uint32_t flags, dmm_general_stats* stats, uint8_t* status,
+                                          uint32_t* snapshots, uint32_t max_snaps, void* stream);
+
 /* void partition_square(const MatrixView&)                       partition.hpp:189-197 */
 dmm_status dmm_partition_square(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
                                 uint8_t* status, void* stream);

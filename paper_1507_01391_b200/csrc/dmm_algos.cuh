@@ -331,15 +331,44 @@ __device__ __forceinline__ void balance_rounds(uint32_t (&x)[M], uint32_t* buf, 
 
 // balance + convert_and_divide (partition.hpp:275-286) until subproblems have <= m
 // rows, then the leaves (balance_divide_sort steps (1) and (2), :373-396)
+// PartitionProbe (partition.hpp:298-301) capture: the full working window after every
+// balance (after_balance) and every convert-and-divide (after_divide) of the OUTER
+// recursion, in the order the reference calls its hooks.  Each lane stores its row of
+// the window; with PK = 2 each 16-bit half goes to its own instance's snapshot area.
+struct ProbeSink {
+    uint32_t* dst[2];  // per half: this instance's snapshot area (max x WM x M words) or null
+    uint32_t n, max;
+    int row, wm;
+    template <int PK, int M>
+    __device__ __forceinline__ void capture(const uint32_t (&x)[M]) {
+        if (n < max) {
+#pragma unroll
+            for (int h = 0; h < PK; ++h) {
+                if (dst[h] == nullptr)
+                    continue;
+                uint32_t* q = dst[h] + ((size_t)n * wm + row) * M;
+#pragma unroll
+                for (int c = 0; c < M; ++c)
+                    q[c] = PK == 2 ? ((x[c] >> (16 * h)) & 0xFFFFu) : x[c];
+            }
+        }
+        ++n;
+    }
+};
+
 template <int PK, class V, bool EXT, int M>
-__device__ __forceinline__ void levels(uint32_t (&x)[M], uint32_t* buf, int lane) {
+__device__ __forceinline__ void levels(uint32_t (&x)[M], uint32_t* buf, int lane, ProbeSink* ps = nullptr) {
     if constexpr (V::WV > V::MV) {
         static_assert(V::WV % V::MV == 0, "general partition needs m | w (ShapeViolation)");
         balance_rounds<PK, V, EXT, 1, V::WV>(x, buf, lane);
+        if (ps)
+            ps->template capture<PK>(x);  // after_balance(depth, level)
         constexpr PParams p = pparams_c(V::WV, V::MV, EXT);
         static_assert(V::WV % p.subproblems == 0, "m*d must divide W (DivisibilityViolation)");
         to_row_major<V>(x, buf, lane);
-        levels<PK, VRows<V, V::WV / p.subproblems>, EXT>(x, buf, lane);
+        if (ps)
+            ps->template capture<PK>(x);  // after_divide(depth + 1, next)
+        levels<PK, VRows<V, V::WV / p.subproblems>, EXT>(x, buf, lane, ps);
     } else {
         partition_leaf<PK, V>(x, buf, lane);
     }
@@ -408,11 +437,12 @@ struct GenResult {
 
 // balance_divide_sort partition.hpp:363-428
 template <int PK, class V, bool EXT, int M>
-__device__ __forceinline__ void balance_divide_sort(uint32_t (&x)[M], uint32_t* buf, int lane, GenResult& res) {
+__device__ __forceinline__ void balance_divide_sort(uint32_t (&x)[M], uint32_t* buf, int lane, GenResult& res,
+                                                    ProbeSink* ps = nullptr) {
     if constexpr (V::WV <= V::MV) {
         partition_leaf<PK, V>(x, buf, lane);
     } else {
-        levels<PK, V, EXT>(x, buf, lane);
+        levels<PK, V, EXT>(x, buf, lane, ps);
         // (3) column recursion: each column into a (W/m) x m submatrix
         to_row_major<V>(x, buf, lane);
         balance_divide_sort<PK, VRows<V, V::WV / V::MV>, EXT>(x, buf, lane, res);

@@ -57,7 +57,8 @@ constexpr int min_blocks_per_sm() { return 1; }
 template <int M, int PK, bool EXT, int MODE, int WM = kWarp>
 __global__ void __launch_bounds__(warps_per_block<M, PK>() * 32, min_blocks_per_sm<M, PK>())
     k_general_sort(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count, uint64_t domain,
-                   int strict, int ascending, dmm_general_stats* __restrict__ stats, uint8_t* __restrict__ status) {
+                   int strict, int ascending, dmm_general_stats* __restrict__ stats, uint8_t* __restrict__ status,
+                   uint32_t* __restrict__ probe, uint32_t probe_max) {
     static_assert(WM >= 1 && kWarp % WM == 0, "machines must tile the warp");
     constexpr int G = kWarp / WM;
     extern __shared__ uint32_t smem[];
@@ -143,8 +144,16 @@ __global__ void __launch_bounds__(warps_per_block<M, PK>() * 32, min_blocks_per_
     GenResult res{{0u, 0u}, 0u};
     if constexpr (MODE == kModeSortAny)
         sort_wide_any<PK, V>(x, buf, lane, ascending != 0);
-    else
-        balance_divide_sort<PK, V, EXT>(x, buf, lane, res);
+    else {
+        // PartitionProbe snapshots (one code path: the hook points test a uniform pointer):
+        // instance k's area is probe[k * probe_max * WM * M ...]
+        ProbeSink ps{{nullptr, nullptr}, 0u, probe_max, row, WM};
+#pragma unroll
+        for (int h = 0; h < PK; ++h)
+            if (probe != nullptr && inst_of(h) < count)
+                ps.dst[h] = probe + inst_of(h) * probe_max * WM * M;
+        balance_divide_sort<PK, V, EXT>(x, buf, lane, res, probe != nullptr ? &ps : nullptr);
+    }
     res.template finish<WM>();
 
     uint32_t invalid = 0;
@@ -218,6 +227,8 @@ struct GeneralArgs {
     dmm_general_stats* stats;
     uint8_t* status;
     cudaStream_t stream;
+    uint32_t* probe = nullptr;  // PartitionProbe snapshots (count x probe_max x w x m), optional
+    uint32_t probe_max = 0;
 };
 
 template <int M, int PK, bool EXT, int MODE, int WM = dmmdev::kWarp>
@@ -241,7 +252,8 @@ dmm_status launch_general(const GeneralArgs& a) {
     if (blocks > 0x7FFFFFFFull)
         return DMM_INVALID_ARGUMENT;
     kern<<<dim3(unsigned(blocks)), dim3(kWarpsPerBlock * 32), smem, a.stream>>>(a.in, a.out, a.count, a.domain, a.strict,
-                                                                                a.ascending, a.stats, a.status);
+                                                                                a.ascending, a.stats, a.status,
+                                                                                a.probe, a.probe_max);
     return check_launch("k_general_sort");
 }
 

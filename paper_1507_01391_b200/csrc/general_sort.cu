@@ -15,9 +15,9 @@ using namespace dmmhost;
 // fits in 16 bits (domain <= 2^16).
 dmm_status dispatch(int mode, const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
                     uint64_t domain, bool ext, int strict, int ascending, dmm_general_stats* stats, uint8_t* status,
-                    cudaStream_t s) {
+                    cudaStream_t s, uint32_t* probe = nullptr, uint32_t probe_max = 0) {
     const bool pk2 = domain <= 65536;
-    const GeneralArgs a{in, out, count, domain, strict, ascending, stats, status, s};
+    const GeneralArgs a{in, out, count, domain, strict, ascending, stats, status, s, probe, probe_max};
     switch (w) {
         case 32:
             switch (m) {
@@ -55,9 +55,13 @@ dmm_status check_ptrs(const void* in, const void* out, uint64_t count) {
 
 extern "C" {
 
-dmm_status dmm_integer_sort_general(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
-                                    uint64_t domain, uint32_t flags, dmm_general_stats* stats, uint8_t* status,
-                                    void* stream) {
+}  // extern "C"
+
+namespace {
+
+dmm_status integer_sort_impl(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                             uint64_t domain, uint32_t flags, dmm_general_stats* stats, uint8_t* status,
+                             uint32_t* probe, uint32_t probe_max, void* stream) {
     reset_launches();
     const bool ext = flags & DMM_FLAG_EXT_PARTIAL_GROUPS;
     const dmm_status sh = integer_sort_shape_status(w, m, !(flags & DMM_FLAG_NO_ENFORCE_PRE), ext);
@@ -72,11 +76,12 @@ dmm_status dmm_integer_sort_general(const uint32_t* in, uint32_t* out, uint32_t 
     // use the extension kernels only where the reference itself would reject the shape
     const bool need_ext = ext && !general_sort_shape_ok(w, m, false) && m < w;
     return dispatch(dmmdev::kModeIntegerSort, in, out, w, m, count, domain, need_ext, !(flags & DMM_FLAG_NONSTRICT), 1,
-                                              stats, status, static_cast<cudaStream_t>(stream));
+                    stats, status, static_cast<cudaStream_t>(stream), probe, probe_max);
 }
 
-dmm_status dmm_partition_general(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
-                                 uint32_t flags, dmm_general_stats* stats, uint8_t* status, void* stream) {
+dmm_status partition_impl(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count, uint32_t flags,
+                          dmm_general_stats* stats, uint8_t* status, uint32_t* probe, uint32_t probe_max,
+                          void* stream) {
     reset_launches();
     const bool ext = flags & DMM_FLAG_EXT_PARTIAL_GROUPS;
     const dmm_status sh = integer_sort_shape_status(w, m, !(flags & DMM_FLAG_NO_ENFORCE_PRE), ext);
@@ -86,7 +91,52 @@ dmm_status dmm_partition_general(const uint32_t* in, uint32_t* out, uint32_t w, 
         return e;
     const bool need_ext = ext && !general_sort_shape_ok(w, m, false) && m < w;
     return dispatch(dmmdev::kModePartition, in, out, w, m, count, w, need_ext, !(flags & DMM_FLAG_NONSTRICT), 1, stats,
-                                            status, static_cast<cudaStream_t>(stream));
+                    status, static_cast<cudaStream_t>(stream), probe, probe_max);
+}
+
+}  // namespace
+
+extern "C" {
+
+dmm_status dmm_integer_sort_general(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                    uint64_t domain, uint32_t flags, dmm_general_stats* stats, uint8_t* status,
+                                    void* stream) {
+    return integer_sort_impl(in, out, w, m, count, domain, flags, stats, status, nullptr, 0, stream);
+}
+
+dmm_status dmm_partition_general(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                 uint32_t flags, dmm_general_stats* stats, uint8_t* status, void* stream) {
+    return partition_impl(in, out, w, m, count, flags, stats, status, nullptr, 0, stream);
+}
+
+// the outer recursion of balance_divide_sort (partition.hpp:373-391): one after_balance and one
+// after_divide snapshot per level while the subproblems have more than m rows
+uint32_t dmm_general_probe_snaps(uint32_t w, uint32_t m, uint32_t flags) {
+    const bool ext = flags & DMM_FLAG_EXT_PARTIAL_GROUPS;
+    uint32_t n = 0;
+    uint64_t W = w;
+    while (W > m && m >= 2) {
+        const dmmdev::PParams p = dmmdev::pparams_c(int(W), int(m), ext);
+        if (p.subproblems <= 0 || W % uint64_t(p.subproblems) != 0)
+            break;
+        n += 2;
+        W /= uint64_t(p.subproblems);
+    }
+    return n;
+}
+
+dmm_status dmm_partition_general_probe(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                       uint32_t flags, dmm_general_stats* stats, uint8_t* status, uint32_t* snapshots,
+                                       uint32_t max_snaps, void* stream) {
+    return partition_impl(in, out, w, m, count, flags, stats, status, max_snaps ? snapshots : nullptr, max_snaps,
+                          stream);
+}
+
+dmm_status dmm_integer_sort_general_probe(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                          uint64_t domain, uint32_t flags, dmm_general_stats* stats, uint8_t* status,
+                                          uint32_t* snapshots, uint32_t max_snaps, void* stream) {
+    return integer_sort_impl(in, out, w, m, count, domain, flags, stats, status, max_snaps ? snapshots : nullptr,
+                             max_snaps, stream);
 }
 
 dmm_status dmm_sort_wide_any(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,

@@ -172,6 +172,9 @@ class GeneralStats:
     cleanup_retries: torch.Tensor  # int32 [count]
     sorted: torch.Tensor           # bool  [count]
     status: torch.Tensor           # uint8 [count] (dmm_status)
+    # PartitionProbe capture (probe=True): [count, snaps, w, m] windows after every
+    # after_balance / after_divide hook of the outer recursion, in hook order
+    snapshots: torch.Tensor | None = None
 
 
 # --------------------------------------------------------------------------------------
@@ -197,42 +200,58 @@ def gen_keys(index0: int, n: int, stream=None) -> torch.Tensor:
 # --------------------------------------------------------------------------------------
 # Partition / integer sort (partition.hpp:436-456)
 # --------------------------------------------------------------------------------------
-def _general(fn_name: str, grid, domain: int | None, flags: int, out, stream, check: bool):
+def _general(fn_name: str, grid, domain: int | None, flags: int, out, stream, check: bool, probe: bool = False):
     t, single = _as_batch(grid)
     count, w, m = t.shape
     res = out if out is not None else torch.empty_like(t)
     stats = torch.empty((count, 2), dtype=torch.int32, device=t.device)
     status = torch.empty((count,), dtype=torch.uint8, device=t.device)
     L = lib()
+    snaps = None
+    if probe:
+        ns = int(L.dmm_general_probe_snaps(w, m, flags))
+        snaps = torch.zeros((count, ns, w, m), dtype=torch.int32, device=t.device)
+        pp = snaps.data_ptr() if ns else None
     if fn_name == "partition_general":
-        st = L.dmm_partition_general(t.data_ptr(), res.data_ptr(), w, m, count, flags, stats.data_ptr(),
-                                     status.data_ptr(), _stream(stream))
+        if probe:
+            st = L.dmm_partition_general_probe(t.data_ptr(), res.data_ptr(), w, m, count, flags, stats.data_ptr(),
+                                               status.data_ptr(), pp, ns, _stream(stream))
+        else:
+            st = L.dmm_partition_general(t.data_ptr(), res.data_ptr(), w, m, count, flags, stats.data_ptr(),
+                                         status.data_ptr(), _stream(stream))
     else:
-        st = L.dmm_integer_sort_general(t.data_ptr(), res.data_ptr(), w, m, count, domain, flags, stats.data_ptr(),
-                                        status.data_ptr(), _stream(stream))
+        if probe:
+            st = L.dmm_integer_sort_general_probe(t.data_ptr(), res.data_ptr(), w, m, count, domain, flags,
+                                                  stats.data_ptr(), status.data_ptr(), pp, ns, _stream(stream))
+        else:
+            st = L.dmm_integer_sort_general(t.data_ptr(), res.data_ptr(), w, m, count, domain, flags,
+                                            stats.data_ptr(), status.data_ptr(), _stream(stream))
     _check(st, fn_name)
-    gs = GeneralStats(stats[:, 0], stats[:, 1] != 0, status)
+    gs = GeneralStats(stats[:, 0], stats[:, 1] != 0, status, snaps[0] if (single and snaps is not None) else snaps)
     if check:
         _raise_first(status, fn_name)
     return (res[0] if single else res), gs
 
 
-def partition_general(grid, *, flags: int = 0, out=None, stream=None, check: bool = True):
+def partition_general(grid, *, flags: int = 0, out=None, stream=None, check: bool = True, probe: bool = False):
     """GeneralStats partition_general(const MatrixView&)  partition.hpp:453-456.
 
     Labels in [0, w), m copies each.  Returns (partitioned grid(s), GeneralStats).
     flags: FLAG_EXT_PARTIAL_GROUPS accepts shapes like 32 x 8 that the reference's
     balance() rejects; FLAG_NONSTRICT = MachineConfig.strict false.
     """
-    return _general("partition_general", grid, None, flags, out, stream, check)
+    return _general("partition_general", grid, None, flags, out, stream, check, probe)
 
 
 def integer_sort_general(grid, domain: int, *, enforce_analysis_pre: bool = True, flags: int = 0, out=None,
-                         stream=None, check: bool = True):
-    """GeneralStats integer_sort_general(view, domain, probe, enforce_analysis_pre)  partition.hpp:436-449."""
+                         stream=None, check: bool = True, probe: bool = False):
+    """GeneralStats integer_sort_general(view, domain, probe, enforce_analysis_pre)  partition.hpp:436-449.
+
+    probe=True captures the PartitionProbe hook points (after_balance / after_divide of the
+    outer recursion) as GeneralStats.snapshots."""
     if not enforce_analysis_pre:
         flags |= FLAG_NO_ENFORCE_PRE
-    return _general("integer_sort_general", grid, domain, flags, out, stream, check)
+    return _general("integer_sort_general", grid, domain, flags, out, stream, check, probe)
 
 
 def _simple(fn_name: str, grid, *args, out=None, stream=None, w_arg_only: bool = False):

@@ -260,11 +260,49 @@ static void subwarp_cases() {
     }
 }
 
+// PartitionProbe hooks (partition.hpp:298-301): the same calls, depths, view shapes and
+// machine contents at every call (modelled on test_partition.cpp:344-368)
+static void probe_cases() {
+    struct Event {
+        int kind;
+        u32 depth, nviews, view_w;
+        std::vector<word> snap;
+        bool operator==(const Event&) const = default;
+    };
+    for (auto [w, m] : {std::pair<u32, u32>{32, 16}, {16, 8}}) {
+        for (u64 seed = 1; seed <= 4; ++seed) {
+            Instance in = gen_instance(InstanceKind::partition, w, m, seed);
+            std::vector<Event> ea, eb;
+            Machine a = make_machine(w, m), b = make_machine(w, m);
+            MatrixView va = MatrixView::full(a), vb = MatrixView::full(b);
+            va.load(in.grid);
+            vb.load(in.grid);
+            auto probe_for = [](std::vector<Event>& ev, const MatrixView& whole) {
+                PartitionProbe p;
+                p.after_balance = [&ev, whole](u32 d, const std::vector<MatrixView>& lv) {
+                    ev.push_back({0, d, u32(lv.size()), lv.front().W(), whole.snapshot()});
+                };
+                p.after_divide = [&ev, whole](u32 d, const std::vector<MatrixView>& lv) {
+                    ev.push_back({1, d, u32(lv.size()), lv.front().W(), whole.snapshot()});
+                };
+                return p;
+            };
+            PartitionProbe pa = probe_for(ea, va), pb = probe_for(eb, vb);
+            GeneralStats sa = partition_general(va, &pa);
+            GeneralStats sb = b200::partition_general(vb, &pb);
+            CHECK(!ea.empty() && ea == eb);
+            CHECK(va.snapshot() == vb.snapshot());
+            CHECK(sa.cleanup_retries == sb.cleanup_retries);
+        }
+    }
+}
+
 int main() {
     partition_cases();
     integer_sort_cases();
     layout_and_sort_cases();
     subwarp_cases();
+    probe_cases();
     permute_cases();
     std::printf("shim parity: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;

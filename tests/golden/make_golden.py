@@ -27,6 +27,10 @@ INTSORT_CASES = [(32, 16, 0, 512), (32, 32, 1, 1024), (64, 16, 2, 1024)]
 U32SORT_CASES = [(32, 128, 0), (32, 128, 1), (32, 32, 2)]
 PERMUTE_CASES = [(32, 32, s) for s in range(1, 7)] + [(32, 16, s) for s in range(1, 7)] + [
     (32, 2, 1), (32, 4, 1), (64, 16, 1), (64, 8, 1), (128, 64, 1)]
+# PartitionProbe snapshots (after_balance / after_divide of the outer recursion):
+# (w, m, seed, domain); domain = w on partition instances is partition_general's recursion
+PROBE_CASES = [(32, 16, 0, 32), (32, 16, 1, 32), (32, 16, 2, 32), (16, 8, 0, 16), (16, 8, 3, 16),
+               (32, 16, 4, 512)]
 LAYOUT_CASES = [("to_column_major", 2, 4), ("to_row_major", 2, 4), ("to_column_major", 32, 8),
                 ("to_row_major", 8, 32), ("transpose_square", 32, 32), ("to_column_major", 3, 6)]
 
@@ -35,7 +39,8 @@ def main() -> None:
     ref = Ref()
     port = Port()
     arrays: dict[str, np.ndarray] = {}
-    meta: dict[str, object] = {"partition": [], "intsort": [], "u32sort": [], "permute": [], "layout": []}
+    meta: dict[str, object] = {"partition": [], "intsort": [], "u32sort": [], "permute": [], "layout": [],
+                               "probe": []}
 
     for (w, m, s) in PARTITION_CASES:
         g = ref.gen_instance(1, w, m, s)
@@ -72,6 +77,16 @@ def main() -> None:
         pipe = rep["pipeline"]
         meta["permute"].append({"key": key, "w": w, "m": m, "seed": s, "status": st, "steps": rep["steps"],
                                 "correct": rep["correct"], **pipe})
+
+    for (w, m, s, dom) in PROBE_CASES:
+        g = ref.gen_instance(1 if dom == w else 2, w, m, s)
+        st, out, rep = ref.integer_sort_general(g, dom, probe_snaps=16)
+        key = f"probe_{w}x{m}_s{s}_d{dom}"
+        arrays[key + "_in"] = g.astype(np.uint32)
+        arrays[key + "_out"] = out.astype(np.uint32)
+        arrays[key + "_snaps"] = rep["snapshots"].astype(np.uint32)
+        meta["probe"].append({"key": key, "w": w, "m": m, "seed": s, "domain": dom, "status": st,
+                              "cleanup_retries": rep["cleanup_retries"], "n_snaps": int(rep["snapshots"].shape[0])})
 
     for (op, w, m) in LAYOUT_CASES:
         g = np.arange(1, w * m + 1, dtype=np.uint64).reshape(w, m)

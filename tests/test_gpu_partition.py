@@ -51,7 +51,7 @@ def test_partition_general_vs_oracle(port, m, flags):
 def test_partition_golden(golden):
     meta, arr = golden
     for case in meta["partition"]:
-        if case["w"] != 32 or not dmm.supported("partition_general", case["w"], case["m"]):
+        if not dmm.supported("partition_general", case["w"], case["m"]) or case["status"] != 0:
             continue
         out, st = dmm.partition_general(arr[case["key"] + "_in"])
         assert (dmm.as_uint32(out) == arr[case["key"] + "_out"]).all(), case["key"]
@@ -77,7 +77,7 @@ def test_integer_sort_vs_oracle(port, m, domain):
 def test_integer_sort_golden(golden):
     meta, arr = golden
     for case in meta["intsort"] + meta["u32sort"]:
-        if case["w"] != 32 or not dmm.supported("integer_sort_general", 32, case["m"]):
+        if not dmm.supported("integer_sort_general", case["w"], case["m"]) or case["status"] != 0:
             continue
         dom = case.get("domain", 1 << 32)
         out, st = dmm.integer_sort_general(arr[case["key"] + "_in"], dom)
@@ -171,3 +171,39 @@ def test_sort_rows_orders():
             assert (out[:, r, :] == exp).all()
     with pytest.raises(dmm.KeyOutOfRange):  # row_radix_segment partition.hpp:63
         dmm.sort_rows(g, order=0, domain=50)
+
+
+def test_partition_probe_snapshots_golden(golden):
+    """PartitionProbe (partition.hpp:298-301): the working window after every after_balance /
+    after_divide hook of the outer recursion equals the reference's, snapshot for snapshot."""
+    meta, arr = golden
+    assert meta["probe"]
+    for case in meta["probe"]:
+        g = arr[case["key"] + "_in"]
+        if case["domain"] == case["w"]:
+            out, st = dmm.partition_general(g, probe=True)
+        else:
+            out, st = dmm.integer_sort_general(g, case["domain"], probe=True)
+        snaps = dmm.as_uint32(st.snapshots)
+        assert snaps.shape[0] == case["n_snaps"], case["key"]
+        assert (snaps == arr[case["key"] + "_snaps"]).all(), case["key"]
+        assert (dmm.as_uint32(out) == arr[case["key"] + "_out"]).all()
+        assert int(st.cleanup_retries) == case["cleanup_retries"]
+
+
+@pytest.mark.parametrize("w,m", [(32, 16), (16, 8), (32, 8)])
+def test_probe_batch_matches_plain_run(port, w, m):
+    # a probed batch (both packed halves, ragged tail) returns the same outputs and stats as
+    # the plain kernel; w <= m has no outer recursion and so no snapshots
+    flags = dmm.FLAG_EXT_PARTIAL_GROUPS if (w, m) == (32, 8) else 0
+    grids = np.stack([port.gen_instance(1, w, m, s) for s in range(1, 12)]).astype(np.uint32)
+    out0, st0 = dmm.partition_general(grids, flags=flags)
+    out1, st1 = dmm.partition_general(grids, flags=flags, probe=True)
+    assert (dmm.as_uint32(out0) == dmm.as_uint32(out1)).all()
+    assert (st0.cleanup_retries == st1.cleanup_retries).all()
+    assert st1.snapshots.shape == (11, 2, w, m)
+    # the last snapshot (after the final divide) is a permutation of the instance
+    s = dmm.as_uint32(st1.snapshots)
+    assert (np.sort(s[:, -1].reshape(11, -1), axis=1) == np.sort(grids.reshape(11, -1), axis=1)).all()
+    _, st2 = dmm.partition_general(port.gen_instance(1, 32, 32, 1), probe=True)
+    assert st2.snapshots.shape == (0, 32, 32)
