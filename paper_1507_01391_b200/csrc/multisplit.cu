@@ -3,20 +3,23 @@
 // label = (key >> shift) & (nbuckets - 1), bucket-major output, per-bucket counts.
 //
 // Three passes, no shared-memory data movement at all (so nothing to conflict on):
-//   1. k_ms_count: each warp owns a tile of 32 x R keys (coalesced 128-byte rows); per row
-//      of 32 keys, log2(nbuckets) ballots give every bucket's lane mask, popc counts it;
+//   1. k_ms_count: each warp owns a tile of kMsRows rows of 128 keys; lane l loads keys
+//      4l..4l+3 of a row with one 16-byte load (512 coalesced bytes per warp load); per
+//      row and sub-position j, log2(nbuckets) ballots give every bucket's lane mask and
+//      popc counts it;
 //   2. k_ms_scan_*: exclusive scan of the per-tile counts, bucket-major (two levels);
 //   3. k_ms_scatter: the warp re-reads its tile; a key's destination is
-//      offset[bucket][tile] + keys of its bucket in earlier rows + popc(mask & lanes below),
-//      i.e. stable by (tile, row, lane) = source order.  One warp store writes at most
-//      nbuckets contiguous runs.
+//      offset[bucket][tile] + keys of its bucket in earlier rows + keys of its bucket held
+//      by lower lanes in this row + its own earlier keys of the same bucket, i.e. stable by
+//      source index.  A warp store writes at most nbuckets contiguous runs.
 // The cross-GPU exchange (bucket j -> rank owning j) is an NCCL all-to-all in
 // paper_1507_01391_b200/distributed.py.
 #include "capi_common.h"
 
 namespace dmmdev {
 
-constexpr int kMsRows = 32;  // rows of 32 keys per warp tile (1024 keys)
+constexpr int kMsRows = 32;    // rows of 128 keys per warp tile
+constexpr int kMsTile = kMsRows * 128;  // keys per warp tile
 
 template <int LB>
 __device__ __forceinline__ void bucket_masks(uint32_t label, uint32_t (&mk)[1 << LB]) {
@@ -34,6 +37,54 @@ __device__ __forceinline__ void bucket_masks(uint32_t label, uint32_t (&mk)[1 <<
     }
 }
 
+// lane l's 4 keys of row r of a tile: indices base + 128 r + 4 l + (0..3); vectorised when the
+// whole row is in range (n need not be a multiple of 4)
+__device__ __forceinline__ void load_row4(const uint32_t* __restrict__ keys, uint64_t n, uint64_t i0,
+                                          uint32_t (&k)[4], uint32_t& valid) {
+    if (i0 + 4 <= n && (i0 & 3) == 0) {
+        const uint4 t = __ldg(reinterpret_cast<const uint4*>(keys + i0));
+        k[0] = t.x;
+        k[1] = t.y;
+        k[2] = t.z;
+        k[3] = t.w;
+        valid = 0xFu;
+    } else {
+        valid = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool v = i0 + j < n;
+            k[j] = v ? __ldg(keys + i0 + j) : 0u;
+            valid |= v ? (1u << j) : 0u;
+        }
+    }
+}
+
+// Per-lane bucket counters packed 8 bits per bucket: P[h] holds buckets 4h..4h+3 (a lane
+// sees at most 4 keys per row, so a row's counts and their warp prefix sums stay < 256).
+template <int NB>
+struct Packed {
+    static constexpr int H = (NB + 3) / 4;
+    uint32_t p[H];
+    __device__ __forceinline__ void clear() {
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+            p[h] = 0;
+    }
+    __device__ __forceinline__ void add(uint32_t label) {  // count one key of bucket `label`
+        const uint32_t inc = 1u << (8 * (label & 3));
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+            p[h] += (label >> 2) == (uint32_t)h ? inc : 0u;
+    }
+    __device__ __forceinline__ uint32_t get(uint32_t b) const {
+        uint32_t v = 0;
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+            v = (b >> 2) == (uint32_t)h ? p[h] : v;
+        return (v >> (8 * (b & 3))) & 0xFFu;
+    }
+};
+
 template <int LB>
 __global__ void __launch_bounds__(256) k_ms_count(const uint32_t* __restrict__ keys, uint64_t n, uint32_t shift,
                                                   uint32_t* __restrict__ tile_counts, uint64_t ntiles) {
@@ -42,32 +93,36 @@ __global__ void __launch_bounds__(256) k_ms_count(const uint32_t* __restrict__ k
     const uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (tile >= ntiles)
         return;
-    uint32_t cnt[NB];
-#pragma unroll
-    for (int b = 0; b < NB; ++b)
-        cnt[b] = 0;
-    const uint64_t base = tile * kMsRows * 32;
-#pragma unroll 4
+    // per-lane counts over the whole tile: kMsRows * 4 = 128 keys per lane < 256
+    Packed<NB> c;
+    c.clear();
+    const uint64_t base = tile * kMsTile;
+#pragma unroll 8
     for (int r = 0; r < kMsRows; ++r) {
-        const uint64_t i = base + (uint64_t)r * 32 + lane;
-        const bool valid = i < n;
-        const uint32_t key = valid ? __ldg(keys + i) : 0u;
-        const uint32_t label = (key >> shift) & (NB - 1);
-        uint32_t mk[NB];
-        bucket_masks<LB>(label, mk);
-        const uint32_t vm = __ballot_sync(0xFFFFFFFFu, valid);
+        uint32_t k[4], valid;
+        load_row4(keys, n, base + (uint64_t)r * 128 + 4 * lane, k, valid);
 #pragma unroll
-        for (int b = 0; b < NB; ++b)
-            cnt[b] += __popc(mk[b] & vm);
+        for (int j = 0; j < 4; ++j)
+            if ((valid >> j) & 1u)
+                c.add((k[j] >> shift) & (NB - 1));
     }
-    if (lane < NB) {
-        uint32_t v = 0;
+    // lane b < NB reports bucket b: reduce every bucket over the warp (16-bit halves, < 2^13)
+    uint32_t mine = 0;
 #pragma unroll
-        for (int b = 0; b < NB; ++b)
-            if (b == lane)
-                v = cnt[b];
-        tile_counts[(uint64_t)lane * ntiles + tile] = v;  // bucket-major
+    for (int h = 0; h < Packed<NB>::H; ++h) {
+        uint32_t lo = c.p[h] & 0x00FF00FFu, hi = (c.p[h] >> 8) & 0x00FF00FFu;  // buckets (4h, 4h+2), (4h+1, 4h+3)
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            lo += __shfl_xor_sync(0xFFFFFFFFu, lo, o);
+            hi += __shfl_xor_sync(0xFFFFFFFFu, hi, o);
+        }
+        if ((lane >> 2) == h) {
+            const uint32_t q = lane & 3;
+            mine = ((q & 1) ? hi : lo) >> (16 * (q >> 1)) & 0xFFFFu;
+        }
     }
+    if (lane < NB)
+        tile_counts[(uint64_t)lane * ntiles + tile] = mine;  // bucket-major
 }
 
 // exclusive scan of a bucket-major count array (NB * ntiles entries) in two levels
@@ -147,35 +202,59 @@ __global__ void __launch_bounds__(256) k_ms_scatter(const uint32_t* __restrict__
                                                     const uint64_t* __restrict__ offsets, uint64_t ntiles,
                                                     uint32_t* __restrict__ out) {
     constexpr int NB = 1 << LB;
+    constexpr int H = Packed<NB>::H;
     const int lane = threadIdx.x & 31;
     const uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (tile >= ntiles)
         return;
-    uint64_t pos[NB];
-#pragma unroll
-    for (int b = 0; b < NB; ++b)
-        pos[b] = offsets[(uint64_t)b * ntiles + tile];
-    const uint32_t below = (1u << lane) - 1u;
-    const uint64_t base = tile * kMsRows * 32;
-#pragma unroll 4
+    // lane b < NB holds the running output position of bucket b
+    uint64_t pos = lane < NB ? offsets[(uint64_t)lane * ntiles + tile] : 0;
+    const uint64_t base = tile * kMsTile;
+#pragma unroll 2
     for (int r = 0; r < kMsRows; ++r) {
-        const uint64_t i = base + (uint64_t)r * 32 + lane;
-        const bool valid = i < n;
-        const uint32_t key = valid ? __ldg(keys + i) : 0u;
-        const uint32_t label = (key >> shift) & (NB - 1);
-        uint32_t mk[NB];
-        bucket_masks<LB>(label, mk);
-        const uint32_t vm = __ballot_sync(0xFFFFFFFFu, valid);
-        uint64_t dst = 0;
+        uint32_t k[4], valid, label[4];
+        load_row4(keys, n, base + (uint64_t)r * 128 + 4 * lane, k, valid);
+        Packed<NB> own;  // this lane's keys per bucket
+        own.clear();
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-            const uint32_t m = mk[b] & vm;
-            if ((uint32_t)b == label)
-                dst = pos[b] + __popc(m & below);
-            pos[b] += __popc(m);
+        for (int j = 0; j < 4; ++j) {
+            label[j] = (k[j] >> shift) & (NB - 1);
+            if ((valid >> j) & 1u)
+                own.add(label[j]);
         }
-        if (valid)
-            out[dst] = key;
+        // exclusive warp prefix of the packed counts: keys of each bucket in lower lanes
+        Packed<NB> lower;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            uint32_t x = own.p[h];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+                if (lane >= o)
+                    x += y;
+            }
+            lower.p[h] = x - own.p[h];
+        }
+        // row totals (inclusive prefix of lane 31) -> bucket b's lane advances pos after the row
+        uint32_t row_total = 0;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            const uint32_t t = __shfl_sync(0xFFFFFFFFu, lower.p[h] + own.p[h], 31);
+            if ((lane >> 2) == h)
+                row_total = (t >> (8 * (lane & 3))) & 0xFFu;
+        }
+        Packed<NB> seen;  // own earlier keys per bucket
+        seen.clear();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t b = label[j];
+            const uint64_t p0 = __shfl_sync(0xFFFFFFFFu, pos, (int)b);
+            if ((valid >> j) & 1u) {
+                out[p0 + lower.get(b) + seen.get(b)] = k[j];
+                seen.add(b);
+            }
+        }
+        pos += row_total;
     }
 }
 
@@ -188,7 +267,7 @@ template <int LB>
 dmm_status run_multisplit(const uint32_t* keys, uint64_t n, uint32_t shift, uint32_t* out, uint64_t* starts,
                           void* workspace, cudaStream_t s) {
     constexpr int NB = 1 << LB;
-    const uint64_t ntiles = (n + dmmdev::kMsRows * 32 - 1) / (dmmdev::kMsRows * 32);
+    const uint64_t ntiles = (n + dmmdev::kMsTile - 1) / dmmdev::kMsTile;
     const uint64_t total = ntiles * NB;
     const uint64_t nblocks = (total + dmmdev::kScanBlock - 1) / dmmdev::kScanBlock;
     uint32_t* tile_counts = static_cast<uint32_t*>(workspace);
@@ -228,7 +307,7 @@ dmm_status run_multisplit(const uint32_t* keys, uint64_t n, uint32_t shift, uint
 extern "C" {
 
 uint64_t dmm_multisplit_workspace_bytes(uint64_t n, uint32_t nbuckets) {
-    const uint64_t ntiles = (n + dmmdev::kMsRows * 32 - 1) / (dmmdev::kMsRows * 32);
+    const uint64_t ntiles = (n + dmmdev::kMsTile - 1) / dmmdev::kMsTile;
     const uint64_t total = ntiles * nbuckets;
     const uint64_t nblocks = (total + dmmdev::kScanBlock - 1) / dmmdev::kScanBlock;
     return ((total * 4 + 255) & ~uint64_t(255)) + ((total + 31) & ~uint64_t(31)) * 8 + nblocks * 8 + 256;
