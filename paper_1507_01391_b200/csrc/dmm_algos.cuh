@@ -312,7 +312,7 @@ __device__ __forceinline__ void balance_rounds(uint32_t (&x)[M], uint32_t* buf, 
         static_assert(!(g < V::MV && g * g > V::MV) || (EXT && V::MV % g == 0),
                       "balance leftover group fits neither the square nor short-wide case (ShapeViolation)");
         static_assert(NSUBS % g == 0, "balance needs g | nsubs");
-        using A = VF<V::MASK, V::LO, V::ST * SUB_H, g, V::C0, V::MV>;
+        using A = VF<V::MASK, V::LO, V::ST * SUB_H, g, V::C0, V::MV, V::WRAP>;
         if constexpr (g == V::MV) {
             partition_leaf<PK, A>(x, buf, lane);
             transpose_square<A>(x, buf, lane);
@@ -405,18 +405,40 @@ __device__ __forceinline__ uint32_t scan_sorted(const uint32_t (&x)[M], int lane
     return Key<PK>::kAll & ~bad;
 }
 
-// cleanup_pass_pair partition.hpp:341-361 over a family of aligned contiguous views
-template <int PK, class V, int M>
+// cleanup_pass_pair partition.hpp:341-361 over a family of aligned contiguous views.
+// TAG != 0: a key bit no key of this sort uses (keys < TAG's bit in every packed half).
+// Then the two m/2-row end blocks run fused with the m/2-shifted blocks: the view family
+// shifted by m/2 wraps around each view, so its last block is (bottom end block, top end
+// block); the top block's keys carry TAG, which sorts them after every bottom key, so the
+// fused sort leaves each end block exactly its own sorted keys (the reference's separate
+// sorts, in lockstep with the shifted blocks) -- one leaf sort instead of two.
+template <int PK, class V, uint32_t TAG = 0u, int M>
 __device__ __forceinline__ void cleanup_pass_pair(uint32_t (&x)[M], uint32_t* buf, int lane) {
     static_assert(V::MASK == 0xFFFFFFFFu && V::ST == 1 && V::LO == 0 && kWarp % V::WV == 0,
                   "cleanup on aligned contiguous views");
     partition_leaf<PK, VRows<V, V::MV>>(x, buf, lane);  // aligned m x m blocks
     if constexpr (V::WV > V::MV && V::MV >= 2) {
         constexpr int H = V::MV / 2;
-        using Edge = VF<edge_mask(V::WV, H), 0, 1, H, V::C0, V::MV>;
-        using Mid = VF<mid_mask(V::WV, H), H, 1, V::MV, V::C0, V::MV>;
-        partition_leaf<PK, Edge>(x, buf, lane);  // the two m/2-row end blocks of every view
-        partition_leaf<PK, Mid>(x, buf, lane);   // the m/2-shifted m-row blocks
+        if constexpr (TAG != 0u) {
+            using Shifted = VF<0xFFFFFFFFu, H, 1, V::MV, V::C0, V::MV, V::WV>;
+            const bool top = V::local(lane) < H;
+            if (top) {
+#pragma unroll
+                for (int c = V::C0; c < V::C0 + V::MV; ++c)
+                    x[c] |= TAG;
+            }
+            partition_leaf<PK, Shifted>(x, buf, lane);
+            if (top) {
+#pragma unroll
+                for (int c = V::C0; c < V::C0 + V::MV; ++c)
+                    x[c] &= ~TAG;
+            }
+        } else {
+            using Edge = VF<edge_mask(V::WV, H), 0, 1, H, V::C0, V::MV>;
+            using Mid = VF<mid_mask(V::WV, H), H, 1, V::MV, V::C0, V::MV>;
+            partition_leaf<PK, Edge>(x, buf, lane);  // the two m/2-row end blocks of every view
+            partition_leaf<PK, Mid>(x, buf, lane);   // the m/2-shifted m-row blocks
+        }
     }
 }
 
@@ -436,7 +458,7 @@ struct GenResult {
 };
 
 // balance_divide_sort partition.hpp:363-428
-template <int PK, class V, bool EXT, int M>
+template <int PK, class V, bool EXT, uint32_t TAG = 0u, int M>
 __device__ __forceinline__ void balance_divide_sort(uint32_t (&x)[M], uint32_t* buf, int lane, GenResult& res,
                                                     ProbeSink* ps = nullptr) {
     if constexpr (V::WV <= V::MV) {
@@ -445,7 +467,7 @@ __device__ __forceinline__ void balance_divide_sort(uint32_t (&x)[M], uint32_t* 
         levels<PK, V, EXT>(x, buf, lane, ps);
         // (3) column recursion: each column into a (W/m) x m submatrix
         to_row_major<V>(x, buf, lane);
-        balance_divide_sort<PK, VRows<V, V::WV / V::MV>, EXT>(x, buf, lane, res);
+        balance_divide_sort<PK, VRows<V, V::WV / V::MV>, EXT, TAG>(x, buf, lane, res);
         to_column_major<V>(x, buf, lane);
         // (4) shifted square cleanup with a checked postcondition
         constexpr int budget = ilog2_ceil_c(V::WV);
@@ -453,7 +475,7 @@ __device__ __forceinline__ void balance_divide_sort(uint32_t (&x)[M], uint32_t* 
         int passes = 0;
 #pragma unroll 1
         for (;;) {
-            cleanup_pass_pair<PK, V>(x, buf, lane);
+            cleanup_pass_pair<PK, V, TAG>(x, buf, lane);
             const uint32_t ok = scan_sorted<PK, V>(x, lane);
             const uint32_t fresh = ok & ~done;
             if (fresh & 1u)

@@ -191,23 +191,31 @@ __device__ __forceinline__ void flip(uint32_t (&x)[M], uint32_t f) {
 // ---------------------------------------------------------------------------
 // View families
 // ---------------------------------------------------------------------------
-template <uint32_t MASK_, int LO_, int ST_, int WV_, int C0_, int MV_>
+// WRAP: lanes are numbered cyclically inside aligned groups of WRAP lanes, so a family
+// offset by LO can wrap around its group (the m/2-shifted cleanup blocks with the two
+// end blocks fused, cleanup_pass_pair below).  With WRAP = 32 and LO <= every active lane
+// this is the plain affine family.
+template <uint32_t MASK_, int LO_, int ST_, int WV_, int C0_, int MV_, int WRAP_ = 32>
 struct VF {
     static constexpr uint32_t MASK = MASK_;
-    static constexpr int LO = LO_, ST = ST_, WV = WV_, C0 = C0_, MV = MV_;
-    static_assert(WV >= 1 && MV >= 1 && ST >= 1, "bad view family");
+    static constexpr int LO = LO_, ST = ST_, WV = WV_, C0 = C0_, MV = MV_, WRAP = WRAP_;
+    static_assert(WV >= 1 && MV >= 1 && ST >= 1 && WRAP >= 1 && 32 % WRAP == 0, "bad view family");
     __host__ __device__ static constexpr bool active(int lane) { return ((MASK >> lane) & 1u) != 0; }
-    __host__ __device__ static constexpr int local(int lane) { return ((lane - LO) / ST) % WV; }
-    __host__ __device__ static constexpr int base(int lane) { return lane - ST * local(lane); }
-    __host__ __device__ static constexpr int lane_of(int lane, int k) { return base(lane) + ST * k; }
+    __host__ __device__ static constexpr int group0(int lane) { return (lane / WRAP) * WRAP; }
+    __host__ __device__ static constexpr int local(int lane) {
+        return ((((lane - group0(lane) - LO) % WRAP + WRAP) % WRAP) / ST) % WV;
+    }
+    __host__ __device__ static constexpr int lane_of(int lane, int k) {
+        return group0(lane) + (((lane - group0(lane) - ST * local(lane) + ST * k) % WRAP + WRAP) % WRAP);
+    }
 };
 
 // aligned row groups of height H inside every view of V (row_range in lockstep; H | WV)
 template <class V, int H>
-using VRows = VF<V::MASK, V::LO, V::ST, H, V::C0, V::MV>;
+using VRows = VF<V::MASK, V::LO, V::ST, H, V::C0, V::MV, V::WRAP>;
 // column window [C0+lo, C0+lo+n) (col_window, view.hpp:83)
 template <class V, int lo, int n>
-using VCols = VF<V::MASK, V::LO, V::ST, V::WV, V::C0 + lo, n>;
+using VCols = VF<V::MASK, V::LO, V::ST, V::WV, V::C0 + lo, n, V::WRAP>;
 
 __host__ __device__ constexpr uint32_t lane_range_mask(int lo, int hi) {
     uint32_t m = 0;

@@ -152,7 +152,10 @@ __global__ void __launch_bounds__(warps_per_block<M, PK>() * 32, min_blocks_per_
         for (int h = 0; h < PK; ++h)
             if (probe != nullptr && inst_of(h) < count)
                 ps.dst[h] = probe + inst_of(h) * probe_max * WM * M;
-        balance_divide_sort<PK, V, EXT>(x, buf, lane, res, probe != nullptr ? &ps : nullptr);
+        // partition labels are < w <= 32: the top key bit of every half is free for the fused
+        // cleanup (cleanup_pass_pair); integer keys may use every bit
+        constexpr uint32_t kTag = MODE == kModePartition ? (PK == 2 ? 0x80008000u : 0x80000000u) : 0u;
+        balance_divide_sort<PK, V, EXT, kTag>(x, buf, lane, res, probe != nullptr ? &ps : nullptr);
     }
     res.template finish<WM>();
 

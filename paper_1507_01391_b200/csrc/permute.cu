@@ -200,7 +200,7 @@ __device__ __forceinline__ bool finish_packed(uint32_t (&y)[WP], uint32_t* buf, 
                                               int lane, uint32_t empty, uint32_t& retries) {
     using V = VF<0xFFFFFFFFu, 0, 1, kWarp, 0, WP>;
     GenResult res{{0u, 0u}, 0u};
-    balance_divide_sort<1, V, false>(y, buf, lane, res);
+    balance_divide_sort<1, V, false, 0x80000000u>(y, buf, lane, res);  // packed labels <= n < 2^31
     res.finish();
     if (res.unsorted & 1u)
         return false;
