@@ -30,6 +30,9 @@ int dmm_supported(const char* algorithm, uint32_t w, uint32_t m) {
     // compiled (w, m) machine shapes of the general-sort kernel (general_m*.cu, general_w*.cu)
     auto general = [&]() -> bool {
         switch (w) {
+            case 256: return m == 16;
+            case 128: return m == 32 || m == 64;
+            case 64: return m == 8 || m == 16 || m == 32 || m == 64;
             case 32: return m == 8 || m == 16 || m == 32 || m == 64 || m == 128;
             case 16:
             case 8: return m == 8 || m == 16 || m == 32 || m == 64;
@@ -43,7 +46,7 @@ int dmm_supported(const char* algorithm, uint32_t w, uint32_t m) {
     if (a == "sort_wide_any")
         return general() && w <= m && m % w == 0 && (w != 32 || m == 32 || m == 64);
     if (a == "partition_square" || a == "sort_square")
-        return general() && w == m && (m == 4 || m == 16);
+        return general() && w == m && (m == 4 || m == 16 || m == 64);
     if (a == "partition_short_wide" || a == "sort_short_wide")
         return general() && uint64_t(w) * w <= m;
     if (a == "permute")

@@ -312,7 +312,7 @@ __device__ __forceinline__ void balance_rounds(uint32_t (&x)[M], uint32_t* buf, 
         static_assert(!(g < V::MV && g * g > V::MV) || (EXT && V::MV % g == 0),
                       "balance leftover group fits neither the square nor short-wide case (ShapeViolation)");
         static_assert(NSUBS % g == 0, "balance needs g | nsubs");
-        using A = VF<V::MASK, V::LO, V::ST * SUB_H, g, V::C0, V::MV, V::WRAP>;
+        using A = VF<V::MASK, V::LO, V::ST * SUB_H, g, V::C0, V::MV, V::WRAP, V::ROWS>;
         if constexpr (g == V::MV) {
             partition_leaf<PK, A>(x, buf, lane);
             transpose_square<A>(x, buf, lane);
@@ -384,24 +384,95 @@ __host__ __device__ constexpr uint32_t edge_mask(int WV, int H) {
 }
 __host__ __device__ constexpr uint32_t mid_mask(int WV, int H) { return ~edge_mask(WV, H); }
 
+// ---------------------------------------------------------------------------
+// Machine-wide primitives for multi-warp machines (ROWS = 64..256 rows = threads of one
+// CTA).  `scratch` is machine shared memory that is free at the call (the relayout buffer
+// between relayouts); every call begins and ends with a machine barrier.
+// ---------------------------------------------------------------------------
+// OR of v over aligned groups of G rows (G >= 32: warp reduction + one word per warp)
+template <int ROWS, int G>
+__device__ __forceinline__ uint32_t group_or(uint32_t v, int row, uint32_t* scratch) {
+    if constexpr (G <= 32) {
+#pragma unroll
+        for (int off = 1; off < G; off <<= 1)
+            v |= __shfl_xor_sync(0xFFFFFFFFu, v, off);
+        return v;
+    } else {
+        v = __reduce_or_sync(0xFFFFFFFFu, v);
+        __syncthreads();
+        if ((row & 31) == 0)
+            scratch[row >> 5] = v;
+        __syncthreads();
+        uint32_t r = 0;
+        const int w0 = (row / G) * (G / 32);
+#pragma unroll
+        for (int w = 0; w < G / 32; ++w)
+            r |= scratch[w0 + w];
+        __syncthreads();
+        return r;
+    }
+}
+template <int ROWS, int G>
+__device__ __forceinline__ uint32_t group_max(uint32_t v, int row, uint32_t* scratch) {
+    if constexpr (G <= 32) {
+#pragma unroll
+        for (int off = 1; off < G; off <<= 1)
+            v = max(v, __shfl_xor_sync(0xFFFFFFFFu, v, off));
+        return v;
+    } else {
+        v = __reduce_max_sync(0xFFFFFFFFu, v);
+        __syncthreads();
+        if ((row & 31) == 0)
+            scratch[row >> 5] = v;
+        __syncthreads();
+        uint32_t r = 0;
+        const int w0 = (row / G) * (G / 32);
+#pragma unroll
+        for (int w = 0; w < G / 32; ++w)
+            r = max(r, scratch[w0 + w]);
+        __syncthreads();
+        return r;
+    }
+}
+// the successor row's value (row + 1; the last row gets its own)
+template <int ROWS>
+__device__ __forceinline__ uint32_t next_row_value(uint32_t v, int row, uint32_t* scratch) {
+    if constexpr (ROWS == 32) {
+        return __shfl_down_sync(0xFFFFFFFFu, v, 1);
+    } else {
+        __syncthreads();
+        scratch[row] = v;
+        __syncthreads();
+        const uint32_t r = scratch[row + 1 < ROWS ? row + 1 : row];
+        __syncthreads();
+        return r;
+    }
+}
+// every row of the machine agrees (the cleanup loop's exit)
+template <int ROWS>
+__device__ __forceinline__ bool machine_all(bool p) {
+    if constexpr (ROWS == 32)
+        return __all_sync(0xFFFFFFFFu, p);
+    else
+        return __syncthreads_and(p ? 1 : 0) != 0;
+}
+
 // scan_sorted partition.hpp:308-337 over a family of aligned contiguous views: each
 // lane returns its view's verdict (bit h set = half h sorted row-major).  The
 // reference's tree_reduce_sum + broadcast of the verdict is a butterfly OR inside
 // each group of WV lanes.
 template <int PK, class V, int M>
-__device__ __forceinline__ uint32_t scan_sorted(const uint32_t (&x)[M], int lane) {
-    static_assert(V::MASK == 0xFFFFFFFFu && V::ST == 1 && V::LO == 0 && kWarp % V::WV == 0,
+__device__ __forceinline__ uint32_t scan_sorted(const uint32_t (&x)[M], uint32_t* buf, int lane) {
+    static_assert(V::MASK == 0xFFFFFFFFu && V::ST == 1 && V::LO == 0 && V::ROWS % V::WV == 0,
                   "scan_sorted on aligned contiguous views");
     uint32_t bad = 0;
 #pragma unroll
     for (int c = V::C0 + 1; c < V::C0 + V::MV; ++c)
         bad |= Key<PK>::gt(x[c - 1], x[c]);
-    const uint32_t next_first = __shfl_down_sync(0xFFFFFFFFu, x[V::C0], 1);
+    const uint32_t next_first = next_row_value<V::ROWS>(x[V::C0], lane, buf);
     if (V::local(lane) + 1 < V::WV)
         bad |= Key<PK>::gt(x[V::C0 + V::MV - 1], next_first);
-#pragma unroll
-    for (int off = 1; off < V::WV; off <<= 1)
-        bad |= __shfl_xor_sync(0xFFFFFFFFu, bad, off);
+    bad = group_or<V::ROWS, V::WV>(bad, lane, buf);
     return Key<PK>::kAll & ~bad;
 }
 
@@ -414,13 +485,13 @@ __device__ __forceinline__ uint32_t scan_sorted(const uint32_t (&x)[M], int lane
 // sorts, in lockstep with the shifted blocks) -- one leaf sort instead of two.
 template <int PK, class V, uint32_t TAG = 0u, int M>
 __device__ __forceinline__ void cleanup_pass_pair(uint32_t (&x)[M], uint32_t* buf, int lane) {
-    static_assert(V::MASK == 0xFFFFFFFFu && V::ST == 1 && V::LO == 0 && kWarp % V::WV == 0,
+    static_assert(V::MASK == 0xFFFFFFFFu && V::ST == 1 && V::LO == 0 && V::ROWS % V::WV == 0,
                   "cleanup on aligned contiguous views");
     partition_leaf<PK, VRows<V, V::MV>>(x, buf, lane);  // aligned m x m blocks
     if constexpr (V::WV > V::MV && V::MV >= 2) {
         constexpr int H = V::MV / 2;
         if constexpr (TAG != 0u) {
-            using Shifted = VF<0xFFFFFFFFu, H, 1, V::MV, V::C0, V::MV, V::WV>;
+            using Shifted = VF<0xFFFFFFFFu, H, 1, V::MV, V::C0, V::MV, V::WV, V::ROWS>;
             const bool top = V::local(lane) < H;
             if (top) {
 #pragma unroll
@@ -434,6 +505,7 @@ __device__ __forceinline__ void cleanup_pass_pair(uint32_t (&x)[M], uint32_t* bu
                     x[c] &= ~TAG;
             }
         } else {
+            static_assert(V::ROWS == 32, "multi-warp machines run the fused cleanup (a free tag bit)");
             using Edge = VF<edge_mask(V::WV, H), 0, 1, H, V::C0, V::MV>;
             using Mid = VF<mid_mask(V::WV, H), H, 1, V::MV, V::C0, V::MV>;
             partition_leaf<PK, Edge>(x, buf, lane);  // the two m/2-row end blocks of every view
@@ -454,6 +526,13 @@ struct GenResult {
         retries[0] = seg_max<WM>(retries[0]);
         retries[1] = seg_max<WM>(retries[1]);
         unsorted = seg_or<WM>(unsorted);
+    }
+    // multi-warp machine of ROWS rows (scratch: free machine shared memory)
+    template <int ROWS>
+    __device__ void finish_machine(int row, uint32_t* scratch) {
+        retries[0] = group_max<ROWS, ROWS>(retries[0], row, scratch);
+        retries[1] = group_max<ROWS, ROWS>(retries[1], row, scratch);
+        unsorted = group_or<ROWS, ROWS>(unsorted, row, scratch);
     }
 };
 
@@ -476,14 +555,14 @@ __device__ __forceinline__ void balance_divide_sort(uint32_t (&x)[M], uint32_t* 
 #pragma unroll 1
         for (;;) {
             cleanup_pass_pair<PK, V, TAG>(x, buf, lane);
-            const uint32_t ok = scan_sorted<PK, V>(x, lane);
+            const uint32_t ok = scan_sorted<PK, V>(x, buf, lane);
             const uint32_t fresh = ok & ~done;
             if (fresh & 1u)
                 res.retries[0] = max(res.retries[0], (uint32_t)passes);
             if (fresh & 2u)
                 res.retries[1] = max(res.retries[1], (uint32_t)passes);
             done |= ok;
-            if (__all_sync(0xFFFFFFFFu, done == Key<PK>::kAll) || passes == budget)
+            if (machine_all<V::ROWS>(done == Key<PK>::kAll) || passes == budget)
                 break;
             ++passes;
         }

@@ -191,16 +191,21 @@ __device__ __forceinline__ void flip(uint32_t (&x)[M], uint32_t f) {
 // ---------------------------------------------------------------------------
 // View families
 // ---------------------------------------------------------------------------
-// WRAP: lanes are numbered cyclically inside aligned groups of WRAP lanes, so a family
+// WRAP: rows are numbered cyclically inside aligned groups of WRAP rows, so a family
 // offset by LO can wrap around its group (the m/2-shifted cleanup blocks with the two
-// end blocks fused, cleanup_pass_pair below).  With WRAP = 32 and LO <= every active lane
-// this is the plain affine family.
-template <uint32_t MASK_, int LO_, int ST_, int WV_, int C0_, int MV_, int WRAP_ = 32>
+// end blocks fused, cleanup_pass_pair).  With WRAP = ROWS and LO <= every active row this
+// is the plain affine family.  ROWS: rows of the machine = threads holding one row each
+// (32: one warp, the `lane` arguments below are lanes; 64..256: ROWS / 32 warps of one CTA,
+// the `lane` arguments are thread indices = rows; MASK must then be full).
+template <uint32_t MASK_, int LO_, int ST_, int WV_, int C0_, int MV_, int WRAP_ = 32, int ROWS_ = 32>
 struct VF {
     static constexpr uint32_t MASK = MASK_;
-    static constexpr int LO = LO_, ST = ST_, WV = WV_, C0 = C0_, MV = MV_, WRAP = WRAP_;
-    static_assert(WV >= 1 && MV >= 1 && ST >= 1 && WRAP >= 1 && 32 % WRAP == 0, "bad view family");
-    __host__ __device__ static constexpr bool active(int lane) { return ((MASK >> lane) & 1u) != 0; }
+    static constexpr int LO = LO_, ST = ST_, WV = WV_, C0 = C0_, MV = MV_, WRAP = WRAP_, ROWS = ROWS_;
+    static_assert(WV >= 1 && MV >= 1 && ST >= 1 && WRAP >= 1 && ROWS % WRAP == 0, "bad view family");
+    static_assert(ROWS == 32 || (ROWS % 32 == 0 && MASK == 0xFFFFFFFFu), "multi-warp machines use full families");
+    __host__ __device__ static constexpr bool active(int lane) {
+        return ROWS == 32 ? ((MASK >> lane) & 1u) != 0 : (lane >= 0 && lane < ROWS);
+    }
     __host__ __device__ static constexpr int group0(int lane) { return (lane / WRAP) * WRAP; }
     __host__ __device__ static constexpr int local(int lane) {
         return ((((lane - group0(lane) - LO) % WRAP + WRAP) % WRAP) / ST) % WV;
@@ -210,12 +215,21 @@ struct VF {
     }
 };
 
+// synchronise the threads of one machine (one warp, or the CTA for multi-warp machines)
+template <class V>
+__device__ __forceinline__ void machine_sync() {
+    if constexpr (V::ROWS == 32)
+        __syncwarp();
+    else
+        __syncthreads();
+}
+
 // aligned row groups of height H inside every view of V (row_range in lockstep; H | WV)
 template <class V, int H>
-using VRows = VF<V::MASK, V::LO, V::ST, H, V::C0, V::MV, V::WRAP>;
+using VRows = VF<V::MASK, V::LO, V::ST, H, V::C0, V::MV, V::WRAP, V::ROWS>;
 // column window [C0+lo, C0+lo+n) (col_window, view.hpp:83)
 template <class V, int lo, int n>
-using VCols = VF<V::MASK, V::LO, V::ST, V::WV, V::C0 + lo, n, V::WRAP>;
+using VCols = VF<V::MASK, V::LO, V::ST, V::WV, V::C0 + lo, n, V::WRAP, V::ROWS>;
 
 __host__ __device__ constexpr uint32_t lane_range_mask(int lo, int hi) {
     uint32_t m = 0;
@@ -310,7 +324,7 @@ __host__ __device__ constexpr int relayout_buf_words(int mv) {
 template <class V, class Map>
 __host__ __device__ constexpr bool v4_own_ok(int Q) {  // own-slot 128-bit accesses, per quarter-warp
     for (int j = 0; j < V::MV / 4; ++j) {
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < V::ROWS / 8; ++q) {
             uint32_t seen = 0;
             for (int a = 8 * q; a < 8 * q + 8; ++a) {
                 if (!V::active(a))
@@ -328,19 +342,27 @@ __host__ __device__ constexpr bool v4_own_ok(int Q) {  // own-slot 128-bit acces
 template <class V, class Map>
 __host__ __device__ constexpr bool v4_cross_ok(int Q, bool gather) {  // scalar cross accesses
     for (int c = V::C0; c < V::C0 + V::MV; ++c) {
-        uint32_t seen = 0;
-        for (int lane = 0; lane < kWarp; ++lane) {
-            if (!V::active(lane))
-                continue;
-            const int b = gather ? Map::src_lane(lane, c) : Map::dst_lane(lane, c);
-            const int d = gather ? Map::src_col(lane, c) : Map::dst_col(lane, c);
-            const int bank = (b * Q + (d - V::C0)) & 31;
-            if ((seen >> bank) & 1u)
-                return false;
-            seen |= 1u << bank;
+        for (int w = 0; w < V::ROWS / 32; ++w) {  // one warp-wide instruction per warp
+            uint32_t seen = 0;
+            for (int lane = 32 * w; lane < 32 * w + 32; ++lane) {
+                if (!V::active(lane))
+                    continue;
+                const int b = gather ? Map::src_lane(lane, c) : Map::dst_lane(lane, c);
+                const int d = gather ? Map::src_col(lane, c) : Map::dst_col(lane, c);
+                const int bank = (b * Q + (d - V::C0)) & 31;
+                if ((seen >> bank) & 1u)
+                    return false;
+                seen |= 1u << bank;
+            }
         }
     }
     return true;
+}
+
+// staging words per machine row-group of 32 (the buffer of a machine is ROWS / 32 of these)
+template <class V>
+__host__ __device__ constexpr int relayout_words() {
+    return relayout_buf_words(V::MV) * (V::ROWS / 32);
 }
 
 template <class V, class Map>
@@ -355,7 +377,7 @@ __host__ __device__ constexpr int find_layout() {
     }
     if (V::MV % 4 == 0 && V::C0 % 4 == 0 && quarters_whole) {
         for (int mode = 2; mode < 4; ++mode) {
-            for (int Q = V::MV; Q * kWarp <= relayout_buf_words(V::MV); Q += 4) {
+            for (int Q = V::MV; Q * V::ROWS <= relayout_words<V>(); Q += 4) {
                 if (v4_own_ok<V, Map>(Q) && v4_cross_ok<V, Map>(Q, mode == 2))
                     return mode * 64 + (Q - V::MV);
             }
@@ -363,22 +385,24 @@ __host__ __device__ constexpr int find_layout() {
     }
     for (int mode = 0; mode < 2; ++mode) {
         for (int k = 0; k <= 32; ++k) {
-            if ((32 + k) * V::MV > relayout_buf_words(V::MV))
+            if ((V::ROWS + k) * V::MV > relayout_words<V>())
                 break;
             bool ok = true;
             for (int c = V::C0; c < V::C0 + V::MV && ok; ++c) {
-                uint32_t seen = 0;
-                for (int lane = 0; lane < kWarp; ++lane) {
-                    if (!V::active(lane))
-                        continue;
-                    const int b = mode == 0 ? Map::dst_lane(lane, c) : Map::src_lane(lane, c);
-                    const int d = mode == 0 ? Map::dst_col(lane, c) : Map::src_col(lane, c);
-                    const int bank = ((d - V::C0) * k + b) & 31;
-                    if ((seen >> bank) & 1u) {
-                        ok = false;
-                        break;
+                for (int w = 0; w < V::ROWS / 32 && ok; ++w) {
+                    uint32_t seen = 0;
+                    for (int lane = 32 * w; lane < 32 * w + 32; ++lane) {
+                        if (!V::active(lane))
+                            continue;
+                        const int b = mode == 0 ? Map::dst_lane(lane, c) : Map::src_lane(lane, c);
+                        const int d = mode == 0 ? Map::dst_col(lane, c) : Map::src_col(lane, c);
+                        const int bank = ((d - V::C0) * k + b) & 31;
+                        if ((seen >> bank) & 1u) {
+                            ok = false;
+                            break;
+                        }
+                        seen |= 1u << bank;
                     }
-                    seen |= 1u << bank;
                 }
             }
             if (ok)
@@ -391,12 +415,12 @@ __host__ __device__ constexpr int find_layout() {
 // Bijectivity / inverse consistency of a map on the active cells (static self-check).
 template <class V, class Map>
 __host__ __device__ constexpr bool map_is_consistent() {
-    for (int lane = 0; lane < kWarp; ++lane) {
+    for (int lane = 0; lane < V::ROWS; ++lane) {
         if (!V::active(lane))
             continue;
         for (int c = V::C0; c < V::C0 + V::MV; ++c) {
             const int b = Map::dst_lane(lane, c), d = Map::dst_col(lane, c);
-            if (b < 0 || b >= kWarp || !V::active(b) || d < V::C0 || d >= V::C0 + V::MV)
+            if (b < 0 || b >= V::ROWS || !V::active(b) || d < V::C0 || d >= V::C0 + V::MV)
                 return false;
             if (Map::src_lane(b, d) != lane || Map::src_col(b, d) != c)
                 return false;
@@ -414,9 +438,9 @@ __device__ __forceinline__ void relayout(uint32_t (&x)[M], uint32_t* buf, int la
     const bool act = V::active(lane);
     if constexpr (mode >= 2) {
         constexpr int Q = V::MV + (L & 63);
-        static_assert(Q * kWarp <= relayout_buf_words(V::MV), "relayout buffer too small for this pitch");
+        static_assert(Q * V::ROWS <= relayout_words<V>(), "relayout buffer too small for this pitch");
         uint32_t* own = buf + lane * Q;
-        __syncwarp();
+        machine_sync<V>();
         if (act) {
             if constexpr (mode == 2) {
 #pragma unroll
@@ -431,7 +455,7 @@ __device__ __forceinline__ void relayout(uint32_t (&x)[M], uint32_t* buf, int la
                 }
             }
         }
-        __syncwarp();
+        machine_sync<V>();
         if (act) {
             if constexpr (mode == 2) {
 #pragma unroll
@@ -451,10 +475,10 @@ __device__ __forceinline__ void relayout(uint32_t (&x)[M], uint32_t* buf, int la
             }
         }
     } else {
-        constexpr int P = 32 + (L & 63);
+        constexpr int P = V::ROWS + (L & 63);
         constexpr bool gather = mode == 1;
-        static_assert(V::MV * P <= relayout_buf_words(V::MV), "relayout buffer too small for this skew");
-        __syncwarp();
+        static_assert(V::MV * P <= relayout_words<V>(), "relayout buffer too small for this skew");
+        machine_sync<V>();
         if (act) {
 #pragma unroll
             for (int c = V::C0; c < V::C0 + V::MV; ++c) {
@@ -466,7 +490,7 @@ __device__ __forceinline__ void relayout(uint32_t (&x)[M], uint32_t* buf, int la
                 }
             }
         }
-        __syncwarp();
+        machine_sync<V>();
         if (act) {
 #pragma unroll
             for (int d = V::C0; d < V::C0 + V::MV; ++d) {

@@ -43,10 +43,13 @@ __device__ __forceinline__ void store_row(uint32_t* __restrict__ p, const uint32
 enum : int { kModeIntegerSort = 0, kModePartition = 1, kModeSortAny = 2 };
 
 // CTA shape: warps per CTA and the occupancy target handed to ptxas (register cap)
-template <int M, int PK>
-constexpr int warps_per_block() { return M >= 128 ? 4 : 8; }
+template <int M, int PK, int WM = kWarp>
+constexpr int warps_per_block() { return WM > kWarp ? WM / kWarp : (M >= 128 ? 4 : 8); }
 template <int M, int PK>
 constexpr int min_blocks_per_sm() { return 1; }
+// shared-memory words per warp (WM <= 32) or per machine (WM > 32: one machine per CTA)
+template <int M, int WM>
+constexpr int staging_words() { return relayout_buf_words(M) * (WM > kWarp ? WM / kWarp : 1); }
 
 // One warp = G = 32 / WM machines of WM rows (WM = 32: one machine per warp; WM < 32: the
 // machines are the members of one lockstep view family, exactly how the reference runs
@@ -54,19 +57,25 @@ constexpr int min_blocks_per_sm() { return 1; }
 // instances [t*PK*G, (t+1)*PK*G): half h, lane group g = lane / WM holds instance
 // t*PK*G + h*G + g, local row lane % WM.  The G instances of one half are contiguous in
 // memory, so lane l's row sits at in[(first * WM + l) * M] exactly as for one 32-row machine.
+//
+// WM > 32 (64, 128, 256): one machine per CTA of WM / 32 warps; thread t holds row t, the
+// algorithms get the row index where they take a lane, relayouts go through the CTA's
+// staging buffer between CTA barriers, and per-machine reductions combine the warps.
 template <int M, int PK, bool EXT, int MODE, int WM = kWarp>
-__global__ void __launch_bounds__(warps_per_block<M, PK>() * 32, min_blocks_per_sm<M, PK>())
+__global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_per_sm<M, PK>())
     k_general_sort(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count, uint64_t domain,
                    int strict, int ascending, dmm_general_stats* __restrict__ stats, uint8_t* __restrict__ status,
                    uint32_t* __restrict__ probe, uint32_t probe_max) {
-    static_assert(WM >= 1 && kWarp % WM == 0, "machines must tile the warp");
-    constexpr int G = kWarp / WM;
+    static_assert(WM >= 1 && (kWarp % WM == 0 || WM % kWarp == 0), "machines must tile the warp or the CTA");
+    constexpr bool kMulti = WM > kWarp;
+    constexpr int G = kMulti ? 1 : kWarp / WM;
     extern __shared__ uint32_t smem[];
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int grp = lane / WM, row = lane % WM;
-    uint32_t* buf = smem + warp * relayout_buf_words(M);
-    const uint64_t first = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * (PK * G);  // half 0, group 0
+    const int lane = kMulti ? (int)threadIdx.x : (int)(threadIdx.x & 31);  // the machine row index space
+    const int warp = kMulti ? 0 : (int)(threadIdx.x >> 5);
+    const int grp = kMulti ? 0 : lane / WM, row = kMulti ? lane : lane % WM;
+    uint32_t* buf = smem + warp * staging_words<M, WM>();
+    const uint64_t first = kMulti ? (uint64_t)blockIdx.x * PK
+                                  : ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * (PK * G);  // half 0, group 0
     if (first >= count)
         return;
     // half h of this lane's machine: instance first + h*G + grp (absent past count)
@@ -138,9 +147,15 @@ __global__ void __launch_bounds__(warps_per_block<M, PK>() * 32, min_blocks_per_
         for (int c = 0; c < M; ++c)
             x[c] = __byte_perm(x[c], b[c], 0x5410);  // (a & 0xFFFF) | (b << 16)
     }
-    bad = seg_or<WM>(bad);
+    auto machine_or = [&](uint32_t v) -> uint32_t {
+        if constexpr (kMulti)
+            return group_or<WM, WM>(v, row, buf);
+        else
+            return seg_or<WM>(v);
+    };
+    bad = machine_or(bad);
 
-    using V = VF<0xFFFFFFFFu, 0, 1, WM, 0, M>;
+    using V = VF<0xFFFFFFFFu, 0, 1, WM, 0, M, (kMulti ? WM : 32), (kMulti ? WM : 32)>;
     GenResult res{{0u, 0u}, 0u};
     if constexpr (MODE == kModeSortAny)
         sort_wide_any<PK, V>(x, buf, lane, ascending != 0);
@@ -154,10 +169,16 @@ __global__ void __launch_bounds__(warps_per_block<M, PK>() * 32, min_blocks_per_
                 ps.dst[h] = probe + inst_of(h) * probe_max * WM * M;
         // partition labels are < w <= 32: the top key bit of every half is free for the fused
         // cleanup (cleanup_pass_pair); integer keys may use every bit
-        constexpr uint32_t kTag = MODE == kModePartition ? (PK == 2 ? 0x80008000u : 0x80000000u) : 0u;
+        // (multi-warp machines always run the fused cleanup: their integer sorts need a
+        // domain below the tag bit, checked by the host)
+        constexpr uint32_t kTag =
+            (MODE == kModePartition || kMulti) ? (PK == 2 ? 0x80008000u : 0x80000000u) : 0u;
         balance_divide_sort<PK, V, EXT, kTag>(x, buf, lane, res, probe != nullptr ? &ps : nullptr);
     }
-    res.template finish<WM>();
+    if constexpr (kMulti)
+        res.template finish_machine<WM>(row, buf);
+    else
+        res.template finish<WM>();
 
     uint32_t invalid = 0;
     if constexpr (MODE == kModePartition) {
@@ -170,7 +191,7 @@ __global__ void __launch_bounds__(warps_per_block<M, PK>() * 32, min_blocks_per_
         for (int c = 0; c < M; ++c)
             diff |= x[c] ^ want;
         const uint32_t mism = PK == 2 ? ((diff & 0xFFFFu) ? 1u : 0u) | ((diff >> 16) ? 2u : 0u) : (diff ? 1u : 0u);
-        invalid = seg_or<WM>(mism) | bad;
+        invalid = machine_or(mism) | bad;
     }
 
 #pragma unroll
@@ -237,8 +258,9 @@ struct GeneralArgs {
 template <int M, int PK, bool EXT, int MODE, int WM = dmmdev::kWarp>
 dmm_status launch_general(const GeneralArgs& a) {
     auto kern = dmmdev::k_general_sort<M, PK, EXT, MODE, WM>;
-    constexpr int kWarpsPerBlock = dmmdev::warps_per_block<M, PK>();
-    const size_t smem = size_t(kWarpsPerBlock) * dmmdev::relayout_buf_words(M) * sizeof(uint32_t);
+    constexpr int kWarpsPerBlock = dmmdev::warps_per_block<M, PK, WM>();
+    constexpr bool kMulti = WM > dmmdev::kWarp;
+    const size_t smem = size_t(kMulti ? 1 : kWarpsPerBlock) * dmmdev::staging_words<M, WM>() * sizeof(uint32_t);
     static bool configured = false;  // per instantiation
     if (!configured) {
         if (smem > 48 * 1024 &&
@@ -248,8 +270,9 @@ dmm_status launch_general(const GeneralArgs& a) {
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         configured = true;
     }
-    const uint64_t units = (a.count + PK * (dmmdev::kWarp / WM) - 1) / (PK * (dmmdev::kWarp / WM));
-    const uint64_t blocks = (units + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    constexpr int kPerWarp = kMulti ? 1 : dmmdev::kWarp / WM;  // machines per warp
+    const uint64_t units = (a.count + PK * kPerWarp - 1) / (PK * kPerWarp);  // warp-tasks / machines
+    const uint64_t blocks = kMulti ? units : (units + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (blocks == 0)
         return DMM_OK;
     if (blocks > 0x7FFFFFFFull)
@@ -267,6 +290,10 @@ dmm_status launch_general_m16(int mode, bool pk2, bool ext, const GeneralArgs& a
 dmm_status launch_general_m32(int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_m64(int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_m128(int mode, bool pk2, bool ext, const GeneralArgs& a);
+// multi-warp machines (w = 64, 128, 256 rows, one per CTA), general_tall*.cu
+dmm_status launch_general_tall64(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);
+dmm_status launch_general_tall128(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);
+dmm_status launch_general_tall256(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);
 // sub-warp machines (w < 32 rows, 32 / w machines per warp), general_w*.cu
 dmm_status launch_general_w16(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_w8(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);

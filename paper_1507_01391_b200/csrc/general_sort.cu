@@ -29,13 +29,16 @@ dmm_status dispatch(int mode, const uint32_t* in, uint32_t* out, uint32_t w, uin
                 default: break;
             }
             break;
+        case 64: return launch_general_tall64(m, mode, pk2, ext, a);
+        case 128: return launch_general_tall128(m, mode, pk2, ext, a);
+        case 256: return launch_general_tall256(m, mode, pk2, ext, a);
         case 16: return launch_general_w16(m, mode, pk2, ext, a);
         case 8: return launch_general_w8(m, mode, pk2, ext, a);
         case 4: return launch_general_w4(m, mode, pk2, ext, a);
         case 2: return launch_general_w2(m, mode, pk2, ext, a);
         default: break;
     }
-    set_error("no kernel compiled for this shape (w in {2, 4, 8, 16, 32})");
+    set_error("no kernel compiled for this shape (w in {2, 4, 8, 16, 32, 64, 128, 256})");
     return DMM_UNSUPPORTED_SHAPE;
 }
 

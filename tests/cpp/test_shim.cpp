@@ -193,8 +193,8 @@ static void permute_cases() {
 
 // sub-warp machines (w < 32): the square / short-wide entry points exist only there
 static void subwarp_cases() {
-    // partition_square / partition_short_wide (partition.hpp:178-197)
-    for (auto [w, m] : {std::pair<u32, u32>{16, 16}, {4, 4}, {8, 64}, {4, 16}, {2, 4}}) {
+    // partition_square / partition_short_wide (partition.hpp:178-197); 64 x 64 is a two-warp machine
+    for (auto [w, m] : {std::pair<u32, u32>{16, 16}, {4, 4}, {64, 64}, {8, 64}, {4, 16}, {2, 4}}) {
         for (u64 seed = 1; seed <= 3; ++seed) {
             Instance in = gen_instance(InstanceKind::partition, w, m, seed);
             Machine a = make_machine(w, m), b = make_machine(w, m);
@@ -212,7 +212,7 @@ static void subwarp_cases() {
         }
     }
     // general partition and integer sort at w in {16, 8, 4} with GeneralStats
-    for (auto [w, m] : {std::pair<u32, u32>{16, 8}, {16, 32}, {8, 16}, {4, 8}}) {
+    for (auto [w, m] : {std::pair<u32, u32>{16, 8}, {16, 32}, {8, 16}, {4, 8}, {64, 8}, {128, 64}}) {
         for (u64 seed = 1; seed <= 3; ++seed) {
             Instance in = gen_instance(InstanceKind::partition, w, m, seed);
             Machine a = make_machine(w, m), b = make_machine(w, m);
@@ -227,7 +227,7 @@ static void subwarp_cases() {
     }
     // comparison sorts: sort_square 16 x 16 / 4 x 4, sort_short_wide 8 x 64 / 4 x 16, both directions
     Rng rng(29);
-    for (auto [w, m] : {std::pair<u32, u32>{16, 16}, {4, 4}, {8, 64}, {4, 16}}) {
+    for (auto [w, m] : {std::pair<u32, u32>{16, 16}, {4, 4}, {64, 64}, {8, 64}, {4, 16}}) {
         for (bool asc : {true, false}) {
             std::vector<word> g(u64(w) * m);
             for (auto& x : g)
@@ -269,7 +269,7 @@ static void probe_cases() {
         std::vector<word> snap;
         bool operator==(const Event&) const = default;
     };
-    for (auto [w, m] : {std::pair<u32, u32>{32, 16}, {16, 8}}) {
+    for (auto [w, m] : {std::pair<u32, u32>{32, 16}, {16, 8}, {64, 16}, {256, 16}}) {
         for (u64 seed = 1; seed <= 4; ++seed) {
             Instance in = gen_instance(InstanceKind::partition, w, m, seed);
             std::vector<Event> ea, eb;

@@ -38,7 +38,8 @@ def test_version_and_support_table(lib):
     assert b"sm_100a" in lib.dmm_version()
     assert lib.dmm_supported(b"partition_general", 32, 8)
     assert lib.dmm_supported(b"partition_general", 32, 32)
-    assert not lib.dmm_supported(b"partition_general", 64, 8)
+    assert lib.dmm_supported(b"partition_general", 64, 8) and lib.dmm_supported(b"partition_general", 256, 16)
+    assert not lib.dmm_supported(b"partition_general", 512, 16) and not lib.dmm_supported(b"partition_general", 128, 16)
     # sub-warp machines (32 / w per warp) and the square / short-wide entry points
     assert lib.dmm_supported(b"partition_general", 16, 8) and lib.dmm_supported(b"integer_sort_general", 4, 16)
     assert lib.dmm_supported(b"partition_square", 16, 16) and lib.dmm_supported(b"sort_square", 4, 4)
