@@ -49,6 +49,9 @@ int dmm_supported(const char* algorithm, uint32_t w, uint32_t m) {
         return general() && w == m && (m == 4 || m == 16 || m == 64);
     if (a == "partition_short_wide" || a == "sort_short_wide")
         return general() && uint64_t(w) * w <= m;
+    if (a == "sort_tall")
+        return w >= m && m > 0 && w % m == 0 &&
+               ((w == 32 && m <= 32) || (w == 64 && m >= 8 && m <= 32) || (w == 128 && (m == 16 || m == 32)));
     if (a == "permute")
         return w == 32 && (m == 2 || m == 4 || m == 16 || m == 32);
     return 0;

@@ -259,43 +259,63 @@ __device__ __forceinline__ void partition_leaf(uint32_t (&x)[M], uint32_t* buf, 
 // sort_columns_network sort.hpp:115-156: every column sorted ascending across the
 // rows.  The reference drives a Batcher comparator network between row pairs; on
 // the warp the network runs across lanes with shuffles (no shared memory, so no
-// bank to conflict on).  Outcome: the unique ascending column.
-template <int PK, int M>
-__device__ __forceinline__ void sort_columns_network(uint32_t (&x)[M], int lane) {
+// bank to conflict on).  Partners in another warp (row distance >= 32 on a multi-warp
+// machine) exchange through the machine's staging buffer: each warp writes and reads 32
+// consecutive rows of a column (row ^ j keeps the bank), so those steps are conflict-free
+// too.  Outcome: the unique ascending column.
+template <int PK, class V, int M>
+__device__ __forceinline__ void sort_columns_network(uint32_t (&x)[M], uint32_t* buf, int lane) {
+    constexpr int R = V::ROWS;
 #pragma unroll
-    for (int k = 2; k <= kWarp; k <<= 1) {
+    for (int k = 2; k <= R; k <<= 1) {
 #pragma unroll
         for (int j = k >> 1; j >= 1; j >>= 1) {
-            const bool up = (lane & k) == 0 || k == kWarp;
+            const bool up = (lane & k) == 0 || k == R;
             const bool lower = (lane & j) == 0;
             const bool keep_min = lower == up;
+            if (j < kWarp) {
 #pragma unroll
-            for (int c = 0; c < M; ++c) {
-                const uint32_t p = __shfl_xor_sync(0xFFFFFFFFu, x[c], j);
-                uint32_t lo = x[c], hi = p;
-                Key<PK>::template cx<0>(lo, hi);
-                x[c] = keep_min ? lo : hi;
+                for (int c = 0; c < M; ++c) {
+                    const uint32_t p = __shfl_xor_sync(0xFFFFFFFFu, x[c], j);
+                    uint32_t lo = x[c], hi = p;
+                    Key<PK>::template cx<0>(lo, hi);
+                    x[c] = keep_min ? lo : hi;
+                }
+            } else {
+                __syncthreads();
+#pragma unroll
+                for (int c = 0; c < M; ++c)
+                    buf[c * R + lane] = x[c];
+                __syncthreads();
+#pragma unroll
+                for (int c = 0; c < M; ++c) {
+                    const uint32_t p = buf[c * R + (lane ^ j)];
+                    x[c] = keep_min ? min(x[c], p) : max(x[c], p);
+                }
             }
         }
     }
+    if constexpr (R > kWarp)
+        __syncthreads();  // the buffer is free again for the next relayout
 }
 
-// sort_tall sort.hpp:352-374 on the full warp view (w = 32 >= m, m | w)
+// sort_tall sort.hpp:352-374 on the full machine view (w >= m, m | w)
 template <int PK, class V, int M>
 __device__ __forceinline__ void sort_tall(uint32_t (&x)[M], uint32_t* buf, int lane) {
-    static_assert(V::MASK == 0xFFFFFFFFu && V::ST == 1 && V::WV == kWarp && V::C0 == 0 && V::MV == M,
-                  "sort_tall on the full warp view");
+    static_assert(V::MASK == 0xFFFFFFFFu && V::ST == 1 && V::WV == V::ROWS && V::C0 == 0 && V::MV == M,
+                  "sort_tall on the full machine view");
     static_assert(V::WV >= V::MV && V::WV % V::MV == 0, "sort_tall needs w >= m and m | w (ShapeViolation)");
+    static_assert(PK == 1 || V::ROWS == kWarp, "packed keys only on one-warp machines");
     if constexpr (V::WV == V::MV) {
         sort_wide_any<PK, V>(x, buf, lane, true);
     } else {
         row_sort<PK, V>(x, lane, true);
-        sort_columns_network<PK>(x, lane);
+        sort_columns_network<PK, V>(x, buf, lane);
         to_row_major<V>(x, buf, lane);
-        sort_columns_network<PK>(x, lane);
+        sort_columns_network<PK, V>(x, buf, lane);
         using B = VRows<V, V::MV>;  // m x m blocks, alternating direction per block
         sort_wide_any<PK, B>(x, buf, lane, ((lane / V::MV) % 2) == 0);
-        sort_columns_network<PK>(x, lane);
+        sort_columns_network<PK, V>(x, buf, lane);
         row_sort<PK, V>(x, lane, true);
     }
 }

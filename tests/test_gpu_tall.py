@@ -97,3 +97,14 @@ def test_tall_probe_matches_reference(ref):
         assert snaps.shape[0] == rep["snapshots"].shape[0]
         assert (snaps == rep["snapshots"].astype(np.uint32)).all()
         assert (dmm.as_uint32(out) == exp.astype(np.uint32)).all()
+
+
+@pytest.mark.parametrize("w,m", [(64, 8), (64, 16), (64, 32), (128, 16), (128, 32)])
+def test_sort_tall_multiwarp(port, w, m):
+    # sort_tall sort.hpp:352-374 (Theorem 3); 128 x 32 is the reference's own test shape
+    rng = np.random.default_rng(w * m)
+    g = rng.integers(0, 2 ** 32, size=(3, w, m), dtype=np.uint64).astype(np.uint32)
+    out = dmm.as_uint32(dmm.sort_tall(g))
+    for k in range(3):
+        st, exp = port.simple("sort_tall", g[k])
+        assert st == 0 and (out[k] == exp).all(), (w, m, k)
