@@ -40,9 +40,13 @@ CONFIGS = {
     "cfg5": ("global_partition", 1, 1 << 26, 8, 0,
              "global 8-way partition of 2^32 uint32 keys across 8 GPUs: 2^29 keys per GPU (label = key >> 29), "
              "local stable multisplit + NCCL all-to-all"),
-    "cfg4": ("permute", 32, 32, 1 << 18, 0,
-             "randomized permutation w=32, n=1024 per instance (32x32: the reference rejects n=8192 at w=32), "
-             "seeded Rng per instance, 2^18 instances"),
+    "cfg4": ("permute", 128, 64, 1 << 18, 0,
+             "randomized permutation n=8192 per instance as the reference's accepted 128x64 machine "
+             "(it rejects n=8192 at w=32: 32x256 fails m | w), 4 warps per machine, seeded Rng per instance, "
+             "2^18 instances"),
+    "cfg4s": ("permute", 32, 32, 1 << 18, 0,
+              "randomized permutation w=32, n=1024 per instance (one-warp stand-in), seeded Rng per instance, "
+              "2^18 instances"),
 }
 ALG_ID = {"partition_general": 5, "integer_sort_general": 6, "permute": 7}
 

@@ -53,7 +53,8 @@ int dmm_supported(const char* algorithm, uint32_t w, uint32_t m) {
         return w >= m && m > 0 && w % m == 0 &&
                ((w == 32 && m <= 32) || (w == 64 && m >= 8 && m <= 32) || (w == 128 && (m == 16 || m == 32)));
     if (a == "permute")
-        return w == 32 && (m == 2 || m == 4 || m == 16 || m == 32);
+        return (w == 32 && (m == 2 || m == 4 || m == 16 || m == 32)) || (w == 64 && (m == 8 || m == 16)) ||
+               (w == 128 && m == 64);
     return 0;
 }
 

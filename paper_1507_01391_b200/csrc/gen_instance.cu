@@ -6,7 +6,7 @@
 // x_i = Rng(splitmix64(seed))() >> 32.
 //
 // One thread per instance; the generator state (312 words) and the grid being
-// shuffled live in that thread's local memory.  This is set-up work (the bench
+// shuffled live in that thread's local memory (in global memory above 4096 cells).  This is set-up work (the bench
 // generates its synthetic inputs with it outside the timed region), not the hot path.
 #include "capi_common.h"
 #include "dmm_rng.cuh"
@@ -31,6 +31,17 @@ __global__ void k_gen_instances(int kind, uint32_t w, uint32_t m, uint64_t seed0
         return;
     }
     rng.seed(splitmix64(seed ^ ((uint64_t)w << 32) ^ m));
+    if (n > kMaxGenN) {  // large instances (e.g. permute 128 x 64): shuffle in place in global memory
+        for (uint32_t i = 0; i < n; ++i)
+            dst[i] = kind == 1 ? i / m : i;
+        for (uint32_t i = n; i > 1; --i) {
+            const uint32_t j = (uint32_t)rng.below(i);
+            const uint32_t t = dst[i - 1];
+            dst[i - 1] = dst[j];
+            dst[j] = t;
+        }
+        return;
+    }
     uint32_t g[kMaxGenN];
     for (uint32_t i = 0; i < n; ++i)
         g[i] = kind == 1 ? i / m : i;  // partition: labels 0..w-1, m copies each; permute: iota
@@ -70,8 +81,8 @@ extern "C" dmm_status dmm_gen_instances(int kind, uint32_t w, uint32_t m, uint64
         return DMM_SHAPE_VIOLATION;  // instance.hpp:49-50
     if (kind < 0 || kind > 2 || !out)
         return DMM_INVALID_ARGUMENT;
-    if (uint64_t(w) * m > dmmdev::kMaxGenN) {
-        dmmhost::set_error("dmm_gen_instances: w*m above 4096");
+    if (uint64_t(w) * m > (1u << 20)) {
+        dmmhost::set_error("dmm_gen_instances: w*m above 2^20");
         return DMM_UNSUPPORTED_SHAPE;
     }
     if (count == 0)

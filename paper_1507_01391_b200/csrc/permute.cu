@@ -40,10 +40,75 @@ constexpr int kRngWords = 312;
 #endif
 constexpr int kPermWarps = DMM_PERM_WARPS;
 
-// Warp-shared generator: the 312-word state in smem as two 32-bit arrays (low and
+// Collective primitives of one machine of R rows: one warp (R = 32: shuffles and warp
+// votes) or one CTA of R / 32 warps (R > 32: a machine barrier and an exchange array `xch`
+// of R words + a reduction scratch `red` of R / 32 words in shared memory).
+template <int R>
+struct Mach {
+    uint32_t* xch;
+    uint32_t* red;
+    int row;
+    __device__ __forceinline__ void sync() const {
+        if constexpr (R == kWarp)
+            __syncwarp();
+        else
+            __syncthreads();
+    }
+    // value of v held by row src (every row calls)
+    __device__ __forceinline__ uint32_t shfl(uint32_t v, int src) const {
+        if constexpr (R == kWarp) {
+            return __shfl_sync(0xFFFFFFFFu, v, src);
+        } else {
+            __syncthreads();
+            xch[row] = v;
+            __syncthreads();
+            const uint32_t r = xch[src];
+            __syncthreads();
+            return r;
+        }
+    }
+    __device__ __forceinline__ uint32_t or_all(uint32_t v) const {
+        if constexpr (R == kWarp)
+            return __reduce_or_sync(0xFFFFFFFFu, v);
+        else
+            return group_or<R, R>(v, row, red);
+    }
+    __device__ __forceinline__ uint32_t max_all(uint32_t v) const {
+        if constexpr (R == kWarp)
+            return __reduce_max_sync(0xFFFFFFFFu, v);
+        else
+            return group_max<R, R>(v, row, red);
+    }
+    __device__ __forceinline__ uint32_t add_all(uint32_t v) const {
+        if constexpr (R == kWarp) {
+            return __reduce_add_sync(0xFFFFFFFFu, v);
+        } else {
+            v = __reduce_add_sync(0xFFFFFFFFu, v);
+            __syncthreads();
+            if ((row & 31) == 0)
+                red[row >> 5] = v;
+            __syncthreads();
+            uint32_t r = 0;
+#pragma unroll
+            for (int w = 0; w < R / 32; ++w)
+                r += red[w];
+            __syncthreads();
+            return r;
+        }
+    }
+    __device__ __forceinline__ bool any(bool p) const {
+        if constexpr (R == kWarp)
+            return __any_sync(0xFFFFFFFFu, p);
+        else
+            return __syncthreads_or(p ? 1 : 0) != 0;
+    }
+};
+
+// Machine-shared generator: the 312-word state in smem as two 32-bit arrays (low and
 // high halves), so every warp-wide access is a unit-stride 32-bit access (no bank
 // conflicts); `base` = index of the first draw the current state generation serves.
-struct WarpRng {
+template <int R>
+struct MachRng {
     uint32_t* lo;
     uint32_t* hi;
     int64_t base;
@@ -53,8 +118,8 @@ struct WarpRng {
         lo[i] = (uint32_t)v;
         hi[i] = (uint32_t)(v >> 32);
     }
-    __device__ void seed(uint64_t s, int lane) {
-        if (lane == 0) {
+    __device__ void seed(uint64_t s, const Mach<R>& mc) {
+        if (mc.row == 0) {
             uint64_t v = s;
             put(0, v);
             for (int i = 1; i < kRngWords; ++i) {
@@ -62,72 +127,73 @@ struct WarpRng {
                 put(i, v);
             }
         }
-        __syncwarp();
-        twist(lane);
+        mc.sync();
+        twist(mc);
         base = 0;
     }
     // mersenne twist of all 312 words: [0,156) from old words; [156,311) from new [0,155)
     // and old words; 311 from new 155 and new 0
-    __device__ void twist(int lane) {
+    __device__ void twist(const Mach<R>& mc) {
         constexpr uint64_t MA = 0xB5026F5AA96619E9ULL;
-        uint64_t v[5];
+        constexpr int T = (156 + R - 1) / R;
+        uint64_t v[T];
 #pragma unroll
-        for (int t = 0; t < 5; ++t) {
-            const int i = lane + 32 * t;
+        for (int t = 0; t < T; ++t) {
+            const int i = mc.row + R * t;
             if (i < 156) {
                 // (mt[i] & UM) | (mt[i+1] & LM): the high 33 bits of mt[i], the low 31 of mt[i+1]
                 const uint64_t x = ((uint64_t)hi[i] << 32) | (lo[i] & 0x80000000u) | (lo[i + 1] & 0x7FFFFFFFu);
                 v[t] = get(i + 156) ^ (x >> 1) ^ ((x & 1) ? MA : 0);
             }
         }
-        __syncwarp();
+        mc.sync();
 #pragma unroll
-        for (int t = 0; t < 5; ++t) {
-            const int i = lane + 32 * t;
+        for (int t = 0; t < T; ++t) {
+            const int i = mc.row + R * t;
             if (i < 156)
                 put(i, v[t]);
         }
-        __syncwarp();
+        mc.sync();
 #pragma unroll
-        for (int t = 0; t < 5; ++t) {
-            const int i = 156 + lane + 32 * t;
+        for (int t = 0; t < T; ++t) {
+            const int i = 156 + mc.row + R * t;
             if (i < 311) {
                 const uint64_t x = ((uint64_t)hi[i] << 32) | (lo[i] & 0x80000000u) | (lo[i + 1] & 0x7FFFFFFFu);
                 v[t] = get(i - 156) ^ (x >> 1) ^ ((x & 1) ? MA : 0);
             }
         }
-        __syncwarp();
+        mc.sync();
 #pragma unroll
-        for (int t = 0; t < 5; ++t) {
-            const int i = 156 + lane + 32 * t;
+        for (int t = 0; t < T; ++t) {
+            const int i = 156 + mc.row + R * t;
             if (i < 311)
                 put(i, v[t]);
         }
-        __syncwarp();
-        if (lane == 0) {
+        mc.sync();
+        if (mc.row == 0) {
             const uint64_t x = ((uint64_t)hi[311] << 32) | (lo[311] & 0x80000000u) | (lo[0] & 0x7FFFFFFFu);
             put(311, get(155) ^ (x >> 1) ^ ((x & 1) ? MA : 0));
         }
-        __syncwarp();
+        mc.sync();
     }
     // load an engine mid-stream: the 312 state words and the position p of the next draw
     // (libstdc++'s mersenne_twister_engine layout _M_x[], _M_p): draw d reads word p + d
-    __device__ void load(const uint64_t* state, int lane) {
-        for (int i = lane; i < kRngWords; i += 32)
+    __device__ void load(const uint64_t* state, const Mach<R>& mc) {
+        for (int i = mc.row; i < kRngWords; i += R)
             put(i, state[i]);
         const uint64_t p = state[kRngWords];
-        __syncwarp();
+        mc.sync();
         if (p >= (uint64_t)kRngWords) {
-            twist(lane);
+            twist(mc);
             base = 0;
         } else {
             base = -(int64_t)p;
         }
     }
-    // make draw d (warp-uniform) addressable; advances generations as needed
-    __device__ void advance_to(uint32_t d, int lane) {
+    // make draw d (machine-uniform) addressable; advances generations as needed
+    __device__ void advance_to(uint32_t d, const Mach<R>& mc) {
         while ((int64_t)d >= base + kRngWords) {
-            twist(lane);
+            twist(mc);
             base += kRngWords;
         }
     }
@@ -138,150 +204,176 @@ __device__ __forceinline__ uint32_t hash_eval(uint64_t key, uint32_t m, uint32_t
     return (uint32_t)(splitmix64(key ^ ((uint64_t)i * 0x9e3779b97f4a7c15ULL)) % m);
 }
 
-// Three-phase delivery (permute.hpp:452-529) of one lane's lexicographically sorted packed
-// row (own bank of q: q[c*32 + lane], c < WP; empty labels at the tail) into the output
-// region (row i in bank i: outs[j*32 + i]).
-template <int M>
-__device__ __forceinline__ void three_phase_delivery(const uint32_t* q, int wp, uint32_t* outs, int lane,
+// Three-phase delivery (permute.hpp:452-529) of one row's lexicographically sorted packed
+// row (own bank of q: q[c*R + row], c < WP; empty labels at the tail) into the output
+// region (row i in column i: outs[j*R + i]).
+template <int M, int R>
+__device__ __forceinline__ void three_phase_delivery(const uint32_t* q, int wp, uint32_t* outs, const Mach<R>& mc,
                                                      uint32_t empty) {
+    const int row = mc.row;
     int cnt = 0;
     for (int c = 0; c < wp; ++c)
-        cnt += q[c * 32 + lane] != empty ? 1 : 0;
+        cnt += q[c * R + row] != empty ? 1 : 0;
     int f = 0, l0 = cnt;
     if (cnt > 0) {
-        const uint32_t i_first = q[lane] / M, i_last = q[(cnt - 1) * 32 + lane] / M;
-        while (f < cnt && q[f * 32 + lane] / M == i_first)
+        const uint32_t i_first = q[row] / M, i_last = q[(cnt - 1) * R + row] / M;
+        while (f < cnt && q[f * R + row] / M == i_first)
             ++f;
         if (i_last != i_first)
-            while (l0 > f && q[(l0 - 1) * 32 + lane] / M == i_last)
+            while (l0 > f && q[(l0 - 1) * R + row] / M == i_last)
                 --l0;
         else
             l0 = f;
     }
     // middle labels: destination rows owned by this packed row alone, one per step
     const int nmid = l0 - f;
-    const int max_mid = __reduce_max_sync(0xFFFFFFFFu, (uint32_t)nmid);
+    const int max_mid = (int)mc.max_all((uint32_t)nmid);
     for (int k = 0; k < max_mid; ++k) {
         if (k < nmid) {
-            const uint32_t label = q[(f + k) * 32 + lane];
-            outs[(label % M) * 32 + label / M] = label;
+            const uint32_t label = q[(f + k) * R + row];
+            outs[(label % M) * R + label / M] = label;
         }
-        __syncwarp();
+        mc.sync();
     }
     // first group, then last group: at step j every row sends its label with slot j
     int pf = 0, pl = l0;
     for (int j = 0; j < M; ++j) {
         if (pf < f) {
-            const uint32_t label = q[pf * 32 + lane];
+            const uint32_t label = q[pf * R + row];
             if (label % M == (uint32_t)j) {
-                outs[(label % M) * 32 + label / M] = label;
+                outs[(label % M) * R + label / M] = label;
                 ++pf;
             }
         }
-        __syncwarp();
+        mc.sync();
     }
     for (int j = 0; j < M; ++j) {
         if (pl < cnt) {
-            const uint32_t label = q[pl * 32 + lane];
+            const uint32_t label = q[pl * R + row];
             if (label % M == (uint32_t)j) {
-                outs[(label % M) * 32 + label / M] = label;
+                outs[(label % M) * R + label / M] = label;
                 ++pl;
             }
         }
-        __syncwarp();
+        mc.sync();
     }
 }
 
-// finish (permute.hpp:536-541) on a packed 32 x WP view held in registers y[0..WP):
+// finish (permute.hpp:536-541) on a packed R x WP view held in registers y[0..WP):
 // integer_sort_general(packed, n+1, -, enforce=false), then the three-phase delivery.
 // Returns false on PostconditionFailed (strict): the caller falls back.
-template <int WP, int M>
+template <int WP, int M, int R>
 __device__ __forceinline__ bool finish_packed(uint32_t (&y)[WP], uint32_t* buf, uint32_t* q, uint32_t* outs,
-                                              int lane, uint32_t empty, uint32_t& retries) {
-    using V = VF<0xFFFFFFFFu, 0, 1, kWarp, 0, WP>;
+                                              const Mach<R>& mc, uint32_t empty, uint32_t& retries) {
+    using V = VF<0xFFFFFFFFu, 0, 1, R, 0, WP, R, R>;
     GenResult res{{0u, 0u}, 0u};
-    balance_divide_sort<1, V, false, 0x80000000u>(y, buf, lane, res);  // packed labels <= n < 2^31
-    res.finish();
+    balance_divide_sort<1, V, false, 0x80000000u>(y, buf, mc.row, res);  // packed labels <= n < 2^31
+    if constexpr (R == kWarp)
+        res.finish();
+    else
+        res.template finish_machine<R>(mc.row, mc.red);
     if (res.unsorted & 1u)
         return false;
     retries = res.retries[0];
-    __syncwarp();
+    mc.sync();
 #pragma unroll
     for (int c = 0; c < WP; ++c)
-        q[c * 32 + lane] = y[c];
-    __syncwarp();
-    three_phase_delivery<M>(q, WP, outs, lane, empty);
+        q[c * R + mc.row] = y[c];
+    mc.sync();
+    three_phase_delivery<M, R>(q, WP, outs, mc, empty);
     return true;
 }
 
-template <int M>
+template <int M, int R>
 __host__ __device__ constexpr int perm_stage_words() {
-    return (2 * M * 32 > relayout_buf_words(M) ? 2 * M * 32 : relayout_buf_words(M));
+    return (2 * M * R > relayout_buf_words(M) * (R / 32) ? 2 * M * R : relayout_buf_words(M) * (R / 32));
 }
-template <int M>
-__host__ __device__ constexpr int perm_warp_words() {  // u32 words of smem per warp
-    return 2 * kRngWords + M * 32 + perm_stage_words<M>();
+template <int M, int R>
+__host__ __device__ constexpr int perm_machine_words() {  // u32 words of smem per machine
+    return 2 * kRngWords + M * R + perm_stage_words<M, R>() + (R > kWarp ? R + 32 : 0);
+}
+template <int R>
+__host__ __device__ constexpr int perm_machines_per_cta() { return R > kWarp ? 1 : kPermWarps; }
+
+// packed finish of width WP when the machine shape admits it (width_ok gates it on the host)
+template <int WP, int M, int R>
+__device__ __forceinline__ bool finish_width(uint32_t width, const uint32_t* pk, uint32_t* stage, uint32_t* B,
+                                             uint32_t* outs, const Mach<R>& mc, uint32_t empty, uint32_t& retries,
+                                             bool& handled) {
+    if constexpr (WP >= 2 && 2 * WP <= M && general_shape_ok_c(R, WP, false)) {
+        if (width == (uint32_t)WP) {
+            handled = true;
+            uint32_t y[WP];
+#pragma unroll
+            for (int c = 0; c < WP; ++c)
+                y[c] = pk[c * R + mc.row];
+            return finish_packed<WP, M, R>(y, stage, B, outs, mc, empty, retries);
+        }
+    }
+    return false;
 }
 
-template <int M>
-__global__ void __launch_bounds__(kPermWarps * 32) k_permute(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
-                                                 uint64_t count, const uint64_t* __restrict__ seeds,
-                                                 const uint64_t* __restrict__ states, PermArgs a,
-                                                 dmm_permute_report* __restrict__ reps, uint64_t* __restrict__ hist,
-                                                 uint32_t* __restrict__ shifts_out, uint8_t* __restrict__ status) {
+template <int M, int R>
+__global__ void __launch_bounds__(perm_machines_per_cta<R>() * R) k_permute(
+    const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count, const uint64_t* __restrict__ seeds,
+    const uint64_t* __restrict__ states, PermArgs a, dmm_permute_report* __restrict__ reps, uint64_t* __restrict__ hist,
+    uint32_t* __restrict__ shifts_out, uint8_t* __restrict__ status) {
     extern __shared__ uint64_t smem64[];
-    constexpr int W = kWarp;
+    constexpr int W = R;
     constexpr uint32_t n = W * M;
     constexpr uint32_t empty = n;  // empty_label permute.hpp:88
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    uint32_t* wbase = reinterpret_cast<uint32_t*>(smem64) + warp * perm_warp_words<M>();
-    WarpRng rng{wbase, wbase + kRngWords, 0};
-    uint32_t* outs = wbase + 2 * kRngWords;     // output region, row i in bank i: outs[j*32 + i]
-    uint32_t* stage = outs + M * 32;            // relayout buffer / own-bank rows A,B,H
-    uint32_t* pk = stage + M * 32;                 // packed rows (own bank), capacity m: aliases B,
-                                                   // which is dead from packing until the finish
-    uint32_t* H = stage;                           // per-colour counts, then bucket starts
-    uint32_t* B = stage + M * 32;                  // colour-sorted (compacted) row
-    const uint64_t k = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    constexpr bool kMulti = R > kWarp;
+    const int row = kMulti ? (int)threadIdx.x : (int)(threadIdx.x & 31);
+    const int mach = kMulti ? 0 : (int)(threadIdx.x >> 5);
+    uint32_t* wbase = reinterpret_cast<uint32_t*>(smem64) + mach * perm_machine_words<M, R>();
+    MachRng<R> rng{wbase, wbase + kRngWords, 0};
+    uint32_t* outs = wbase + 2 * kRngWords;     // output region, row i in column i: outs[j*R + i]
+    uint32_t* stage = outs + M * R;             // relayout buffer / own-bank rows A,B,H
+    uint32_t* pk = stage + M * R;               // packed rows (own bank), capacity m: aliases B,
+                                                // which is dead from packing until the finish
+    uint32_t* H = stage;                        // per-colour counts, then bucket starts
+    uint32_t* B = stage + M * R;                // colour-sorted (compacted) row
+    uint32_t* hsh = stage + perm_stage_words<M, R>();  // R > 32: per-row hashes / exchange
+    const Mach<R> mc{hsh, hsh + R, row};
+    const uint64_t k = (uint64_t)blockIdx.x * perm_machines_per_cta<R>() + mach;
     if (k >= count)
         return;
 
     uint32_t x[M];
-    load_row<M>(in + (k * kWarp + lane) * M, x);
+    load_row<M>(in + (k * W + row) * M, x);
     uint32_t badkey = 0;
 #pragma unroll
     for (int c = 0; c < M; ++c) {
         badkey |= x[c] >= n ? 1u : 0u;
-        outs[c * 32 + lane] = 0xFFFFFFFFu;  // sentinel: undelivered
+        outs[c * R + row] = 0xFFFFFFFFu;  // sentinel: undelivered
     }
-    badkey = __reduce_or_sync(0xFFFFFFFFu, badkey);
+    badkey = mc.or_all(badkey);
     if (states)
-        rng.load(states + k * (kRngWords + 1), lane);
+        rng.load(states + k * (kRngWords + 1), mc);
     else
-        rng.seed(seeds[k], lane);
+        rng.seed(seeds[k], mc);
 
     uint64_t random_words = 0;
     uint32_t drawn = 0;
     // ---- preprocess_shuffle permute.hpp:109-142 ---------------------------------------
     {
-        rng.advance_to(drawn + W - 1, lane);
-        const uint32_t s = 1u + (uint32_t)(rng.word(drawn + lane) % M);  // rng_below(M), M a power of two
+        rng.advance_to(drawn + W - 1, mc);
+        const uint32_t s = 1u + (uint32_t)(rng.word(drawn + row) % M);  // rng_below(M), M a power of two
         drawn += W;
         random_words += W;
         if (shifts_out)
-            shifts_out[k * W + lane] = s;
+            shifts_out[k * W + row] = s;
         const uint32_t sh = s % M;
-        __syncwarp();
+        mc.sync();
 #pragma unroll
         for (int c = 0; c < M; ++c)
-            H[((c + sh) % M) * 32 + lane] = x[c];  // own bank: row r rotates in bank r
-        __syncwarp();
+            H[((c + sh) % M) * R + row] = x[c];  // own bank: row r rotates in its own column
+        mc.sync();
 #pragma unroll
         for (int c = 0; c < M; ++c)
-            x[c] = H[c * 32 + lane];
-        using Blk = VF<0xFFFFFFFFu, 0, 1, M, 0, M>;  // every aligned m x m block of rows
-        transpose_square<Blk>(x, stage, lane);
+            x[c] = H[c * R + row];
+        using Blk = VF<0xFFFFFFFFu, 0, 1, M, 0, M, R, R>;  // every aligned m x m block of rows
+        transpose_square<Blk>(x, stage, row);
     }
 
     // ---- iterations permute.hpp:570-577 ---------------------------------------------------
@@ -289,73 +381,84 @@ __global__ void __launch_bounds__(kPermWarps * 32) k_permute(const uint32_t* __r
     uint32_t iterations = 0;
     while (leftover > a.threshold && iterations < a.iter_cap) {
         // draw_and_broadcast_hash permute.hpp:147-166: m draws, key = the first
-        rng.advance_to(drawn, lane);
+        rng.advance_to(drawn, mc);
         const uint64_t key = rng.word(drawn);
         drawn += M;
         random_words += M;
         // rescan_and_bucket permute.hpp:174-216: stable own-bank counting sort by colour.
-        // Every access below is to the lane's own bank (H, B columns = lane): conflict-free
-        // for any data, no warp synchronisation needed.
+        // Every access below is to the row's own column (H, B columns = row): conflict-free
+        // for any data.
+        mc.sync();
 #pragma unroll
         for (int b = 0; b < M; ++b)
-            H[b * 32 + lane] = 0;
-        // h(i) for the 32 source rows i: lane l evaluates h(l) once, keys fetch theirs by
-        // shuffle (one SHFL instead of a 64-bit splitmix64 per key)
-        const uint32_t h_lane = hash_eval(key, M, (uint32_t)lane);
+            H[b * R + row] = 0;
+        // h(i) for the source rows i: row l evaluates h(l) once, keys fetch theirs by
+        // shuffle (R = 32) or from the machine's hash table (one lookup instead of a 64-bit
+        // splitmix64 per key)
+        const uint32_t h_row = hash_eval(key, M, (uint32_t)row);
+        if constexpr (kMulti) {
+            hsh[row] = h_row;
+            __syncthreads();
+        }
         uint32_t col[M];
 #pragma unroll
         for (int c = 0; c < M; ++c) {
             const bool live = x[c] != empty;
             const uint32_t i = live ? x[c] / M : 0u, j = x[c] % M;
-            const uint32_t hi = __shfl_sync(0xFFFFFFFFu, h_lane, (int)(i & 31u));
+            uint32_t hi;
+            if constexpr (kMulti)
+                hi = hsh[i % R];
+            else
+                hi = __shfl_sync(0xFFFFFFFFu, h_row, (int)(i & 31u));
             col[c] = live ? (j + M - hi) % M : 0u;
             if (live)
-                H[col[c] * 32 + lane] += 1;
+                H[col[c] * R + row] += 1;
         }
         uint32_t run = 0;
-        uint32_t lane_left = 0;
+        uint32_t row_left = 0;
 #pragma unroll
         for (int b = 0; b < M; ++b) {
-            const uint32_t cnt = H[b * 32 + lane];
-            lane_left += cnt > a.alpha ? cnt - a.alpha : 0;
-            H[b * 32 + lane] = run;  // bucket start
+            const uint32_t cnt = H[b * R + row];
+            row_left += cnt > a.alpha ? cnt - a.alpha : 0;
+            H[b * R + row] = run;  // bucket start
             run += cnt;
         }
 #pragma unroll
         for (int c = 0; c < M; ++c)
             if ((uint32_t)c >= run)
-                B[c * 32 + lane] = empty;
+                B[c * R + row] = empty;
         // scatter into the colour-sorted order
 #pragma unroll
         for (int c = 0; c < M; ++c) {
             if (x[c] != empty) {
-                const uint32_t pos = H[col[c] * 32 + lane];
-                H[col[c] * 32 + lane] = pos + 1;
-                B[pos * 32 + lane] = x[c];
+                const uint32_t pos = H[col[c] * R + row];
+                H[col[c] * R + row] = pos + 1;
+                B[pos * R + row] = x[c];
             }
         }
         // communication_phase permute.hpp:225-274.  Step (pass p, colour k): every row sends
-        // its p-th label of colour k to out[i][j]; the output region keeps row i in bank i and
-        // the colouring makes the destinations of one step distinct rows, so every step is one
-        // conflict-free warp-wide store.  H holds the bucket ends now: start = end - count.
+        // its p-th label of colour k to out[i][j]; the output region keeps row i in column i
+        // and the colouring makes the destinations of one step distinct rows, so on a 32-row
+        // machine every step is one conflict-free warp-wide store (taller machines map rows
+        // to 32 banks, where distinct rows can share one).  H holds the bucket ends now.
         // A sent label's cell becomes empty in place (the compacted row keeps its holes):
         // exactly the first min(count, alpha) cells of every colour bucket.
         for (int kc = 0; kc < M; ++kc) {
-            const uint32_t end = H[kc * 32 + lane];
-            const uint32_t start = kc == 0 ? 0u : H[(kc - 1) * 32 + lane];
+            const uint32_t end = H[kc * R + row];
+            const uint32_t start = kc == 0 ? 0u : H[(kc - 1) * R + row];
             const uint32_t take = min(end - start, a.alpha);
             for (uint32_t p = 0; p < take; ++p) {
-                const uint32_t label = B[(start + p) * 32 + lane];
-                outs[(label % M) * 32 + label / M] = label;
-                B[(start + p) * 32 + lane] = empty;
+                const uint32_t label = B[(start + p) * R + row];
+                outs[(label % M) * R + label / M] = label;
+                B[(start + p) * R + row] = empty;
             }
         }
 #pragma unroll
         for (int c = 0; c < M; ++c)
-            x[c] = B[c * 32 + lane];
+            x[c] = B[c * R + row];
         // synchronize permute.hpp:278-285
-        leftover = __reduce_add_sync(0xFFFFFFFFu, lane_left);
-        if (lane == 0 && hist && iterations < DMM_PERMUTE_MAX_HIST)
+        leftover = mc.add_all(row_left);
+        if (row == 0 && hist && iterations < DMM_PERMUTE_MAX_HIST)
             hist[k * DMM_PERMUTE_MAX_HIST + iterations] = leftover;
         ++iterations;
     }
@@ -372,40 +475,40 @@ __global__ void __launch_bounds__(kPermWarps * 32) k_permute(const uint32_t* __r
         while (2 * width <= M && !((a.width_ok >> (31 - __clz(width))) & 1u))
             width <<= 1;
         if (2 * width <= M) {
-            // compaction into the packed rows (own bank)
+            // compaction into the packed rows (own column)
             uint32_t load = 0;
-            __syncwarp();
+            mc.sync();
 #pragma unroll
             for (int c = 0; c < M; ++c)
                 if (x[c] != empty)
-                    pk[(load++) * 32 + lane] = x[c];
+                    pk[(load++) * R + row] = x[c];
             for (uint32_t c = load; c < width; ++c)
-                pk[c * 32 + lane] = empty;
+                pk[c * R + row] = empty;
             uint32_t cell_load = load, cell_cursor = load;
             bool recv = false;
             random_words += a.t;
             for (uint32_t round = 0; round < a.t; ++round) {
-                rng.advance_to(drawn, lane);
-                const uint32_t shift = 1u + (uint32_t)(rng.word(drawn) % W);  // rng_below(W), W = 32
+                rng.advance_to(drawn, mc);
+                const uint32_t shift = 1u + (uint32_t)(rng.word(drawn) % W);  // rng_below(W), W a power of two
                 ++drawn;
-                const int partner = (lane + shift) & 31, src = (lane - shift) & 31;
-                const uint32_t p_load = __shfl_sync(0xFFFFFFFFu, cell_load, partner);
-                const bool p_recv = __shfl_sync(0xFFFFFFFFu, recv, partner);
+                const int partner = (row + (int)shift) % W, src = (row - (int)shift + W) % W;
+                const uint32_t p_load = mc.shfl(cell_load, partner);
+                const bool p_recv = mc.shfl(recv ? 1u : 0u, partner) != 0;
                 const bool sender = load > theta && !p_recv && p_load <= theta;
                 const uint32_t give = sender ? min(a.bundle, load) : 0u;
-                const uint32_t p_cursor = __shfl_sync(0xFFFFFFFFu, cell_cursor, partner);
-                const uint32_t maxgive = __reduce_max_sync(0xFFFFFFFFu, give);
+                const uint32_t p_cursor = mc.shfl(cell_cursor, partner);
+                const uint32_t maxgive = mc.max_all(give);
                 for (uint32_t kk = 0; kk < maxgive; ++kk) {
                     uint32_t moved = 0;
                     if (kk < give)
-                        moved = pk[(load - 1 - kk) * 32 + lane];
-                    __syncwarp();
+                        moved = pk[(load - 1 - kk) * R + row];
+                    mc.sync();
                     if (kk < give && p_cursor + kk < M)
-                        pk[(p_cursor + kk) * 32 + partner] = moved;  // distinct partner banks
-                    __syncwarp();
+                        pk[(p_cursor + kk) * R + partner] = moved;  // distinct partner columns
+                    mc.sync();
                 }
-                const bool got = __shfl_sync(0xFFFFFFFFu, sender, src);
-                const uint32_t give_in = __shfl_sync(0xFFFFFFFFu, give, src);
+                const bool got = mc.shfl(sender ? 1u : 0u, src) != 0;
+                const uint32_t give_in = mc.shfl(give, src);
                 if (sender) {
                     cell_load = load - give;  // the own-load write lands last (permute.hpp:415-419)
                     recv = false;
@@ -417,24 +520,20 @@ __global__ void __launch_bounds__(kPermWarps * 32) k_permute(const uint32_t* __r
                     cell_cursor = cell_cursor + give_in;
                 load = load - give + (got ? give_in : 0u);
             }
-            const bool overflow = __any_sync(0xFFFFFFFFu, load > width);
+            const bool overflow = mc.any(load > width);
             if (!overflow) {
-                __syncwarp();
+                mc.sync();
                 for (uint32_t c = load; c < width; ++c)
-                    pk[c * 32 + lane] = empty;
-                __syncwarp();
+                    pk[c * R + row] = empty;
+                mc.sync();
                 used_packing = true;
                 packed_width = width;
-                bool ok = false;
-                if constexpr (M == 32) {
-                    if (width == 16) {
-                        uint32_t y[16];
-#pragma unroll
-                        for (int c = 0; c < 16; ++c)
-                            y[c] = pk[c * 32 + lane];
-                        ok = finish_packed<16, M>(y, stage, B, outs, lane, empty, cleanup_retries);
-                    }
-                }
+                bool ok = false, handled = false;
+                ok = finish_width<2, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled) || ok;
+                ok = finish_width<4, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled) || ok;
+                ok = finish_width<8, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled) || ok;
+                ok = finish_width<16, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled) || ok;
+                ok = finish_width<32, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled) || ok;
                 delivered = ok;
             }
         }
@@ -445,53 +544,53 @@ __global__ void __launch_bounds__(kPermWarps * 32) k_permute(const uint32_t* __r
         uint32_t y[M];
         {
             uint32_t o = 0;
-            __syncwarp();
+            mc.sync();
 #pragma unroll
             for (int c = 0; c < M; ++c)
                 if (x[c] != empty)
-                    B[(o++) * 32 + lane] = x[c];
+                    B[(o++) * R + row] = x[c];
             for (uint32_t c = o; c < M; ++c)
-                B[c * 32 + lane] = empty;
-            __syncwarp();
+                B[c * R + row] = empty;
+            mc.sync();
 #pragma unroll
             for (int c = 0; c < M; ++c)
-                y[c] = B[c * 32 + lane];
+                y[c] = B[c * R + row];
         }
         uint32_t y_keep[M];
 #pragma unroll
         for (int c = 0; c < M; ++c)
             y_keep[c] = y[c];
         uint32_t r2 = 0;
-        if (!finish_packed<M, M>(y, stage, B, outs, lane, empty, r2) && M < kWarp) {
+        if (!finish_packed<M, M, R>(y, stage, B, outs, mc, empty, r2) && M < W) {
             // last resort: comparison tall sort on the compacted multiset (permute.hpp:618-625).
             // The reference sorts the working window left by the failed attempt; any
             // arrangement of the same multiset sorts to the same matrix.
-            using V = VF<0xFFFFFFFFu, 0, 1, kWarp, 0, M>;
-            if constexpr (M < kWarp)
-                sort_tall<1, V>(y_keep, stage, lane);
-            __syncwarp();
+            using V = VF<0xFFFFFFFFu, 0, 1, R, 0, M, R, R>;
+            if constexpr (M < W)
+                sort_tall<1, V>(y_keep, stage, row);
+            mc.sync();
 #pragma unroll
             for (int c = 0; c < M; ++c)
-                B[c * 32 + lane] = y_keep[c];
-            __syncwarp();
-            three_phase_delivery<M>(B, M, outs, lane, empty);
+                B[c * R + row] = y_keep[c];
+            mc.sync();
+            three_phase_delivery<M, R>(B, M, outs, mc, empty);
         } else {
             cleanup_retries = r2;
         }
     }
-    __syncwarp();
-    // output region (row i in bank i) -> global row-major; verify the bijection
+    mc.sync();
+    // output region (row i in column i) -> global row-major; verify the bijection
     uint32_t v[M];
     uint32_t wrong = badkey;
 #pragma unroll
     for (int j = 0; j < M; ++j) {
-        const uint32_t o = outs[j * 32 + lane];
-        wrong |= o != (uint32_t)lane * M + j ? 1u : 0u;
+        const uint32_t o = outs[j * R + row];
+        wrong |= o != (uint32_t)row * M + j ? 1u : 0u;
         v[j] = o == 0xFFFFFFFFu ? 0u : o;  // undelivered cells keep the machine's zero
     }
-    wrong = __reduce_or_sync(0xFFFFFFFFu, wrong);
-    store_row<M>(out + (k * kWarp + lane) * M, v);
-    if (lane == 0) {
+    wrong = mc.or_all(wrong);
+    store_row<M>(out + (k * W + row) * M, v);
+    if (row == 0) {
         if (reps) {
             dmm_permute_report r;
             r.iterations = iterations;
@@ -521,13 +620,13 @@ uint64_t permute_threshold(uint32_t w, uint32_t m) {  // permute.hpp:97-101
     return std::max<uint64_t>(uint64_t(t), w);
 }
 
-template <int M>
+template <int M, int R = dmmdev::kWarp>
 dmm_status launch_permute(const uint32_t* in, uint32_t* out, uint64_t count, const uint64_t* seeds,
-                          const uint64_t* states, const dmmdev::PermArgs& a, dmm_permute_report* reps, uint64_t* hist, uint32_t* shifts,
-                          uint8_t* status, cudaStream_t s) {
-    constexpr int kWarps = dmmdev::kPermWarps;
-    auto kern = dmmdev::k_permute<M>;
-    const size_t smem = size_t(kWarps) * dmmdev::perm_warp_words<M>() * sizeof(uint32_t);
+                          const uint64_t* states, const dmmdev::PermArgs& a, dmm_permute_report* reps, uint64_t* hist,
+                          uint32_t* shifts, uint8_t* status, cudaStream_t s) {
+    constexpr int kMach = dmmdev::perm_machines_per_cta<R>();
+    auto kern = dmmdev::k_permute<M, R>;
+    const size_t smem = size_t(kMach) * dmmdev::perm_machine_words<M, R>() * sizeof(uint32_t);
     static bool configured = false;
     if (!configured) {
         if (smem > 48 * 1024 &&
@@ -537,8 +636,8 @@ dmm_status launch_permute(const uint32_t* in, uint32_t* out, uint64_t count, con
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         configured = true;
     }
-    const uint64_t blocks = (count + kWarps - 1) / kWarps;
-    kern<<<unsigned(blocks), kWarps * 32, smem, s>>>(in, out, count, seeds, states, a, reps, hist, shifts, status);
+    const uint64_t blocks = (count + kMach - 1) / kMach;
+    kern<<<unsigned(blocks), kMach * R, smem, s>>>(in, out, count, seeds, states, a, reps, hist, shifts, status);
     return check_launch("k_permute");
 }
 
@@ -574,10 +673,6 @@ static dmm_status permute_impl(const uint32_t* in, uint32_t* out, uint32_t w, ui
         set_error("in/out must be 16-byte aligned");
         return DMM_INVALID_ARGUMENT;
     }
-    if (w != 32) {
-        set_error("kernels are built for w = 32 (one warp per machine)");
-        return DMM_UNSUPPORTED_SHAPE;
-    }
     dmmdev::PermArgs a;
     a.alpha = alpha;
     a.iter_cap = iter_cap;
@@ -596,12 +691,27 @@ static dmm_status permute_impl(const uint32_t* in, uint32_t* out, uint32_t w, ui
             a.width_ok |= 1u << b;
     }
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
-    switch (m) {
-        case 2: return launch_permute<2>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
-        case 4: return launch_permute<4>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
-        case 16: return launch_permute<16>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
-        case 32: return launch_permute<32>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
-        default: break;
+    if (w == 32) {
+        switch (m) {
+            case 2: return launch_permute<2>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
+            case 4: return launch_permute<4>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
+            case 16: return launch_permute<16>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
+            case 32: return launch_permute<32>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
+            default: break;
+        }
+    } else if (w == 64) {  // machines of two warps (one per CTA)
+        switch (m) {
+            case 8: return launch_permute<8, 64>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
+            case 16:
+                return launch_permute<16, 64>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
+            default: break;
+        }
+    } else if (w == 128) {  // n = 8192: the reference's own permute shape at the BASELINE's n
+        switch (m) {
+            case 64:
+                return launch_permute<64, 128>(in, out, count, seeds, states, a, reports, history, shifts, status, s);
+            default: break;
+        }
     }
     set_error("no permute kernel compiled for this shape");
     return DMM_UNSUPPORTED_SHAPE;

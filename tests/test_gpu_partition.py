@@ -21,7 +21,8 @@ def _oracle_batch(port, kind, w, m, seeds):
     return np.stack([port.gen_instance(kind, w, m, s) for s in seeds]).astype(np.uint32)
 
 
-@pytest.mark.parametrize("kind,w,m", [(1, 32, 8), (1, 32, 16), (1, 32, 32), (2, 32, 32), (2, 32, 16), (1, 32, 64)])
+@pytest.mark.parametrize("kind,w,m", [(1, 32, 8), (1, 32, 16), (1, 32, 32), (2, 32, 32), (2, 32, 16), (1, 32, 64),
+                                      (2, 128, 64), (1, 64, 128)])
 def test_gen_instances_bit_exact(port, kind, w, m):
     seeds = list(range(100, 164))
     dev = dmm.as_uint32(dmm.gen_instances(kind, w, m, 100, 64))

@@ -36,7 +36,7 @@ def test_permute_vs_oracle(port, m):
 def test_permute_golden(golden):
     meta, arr = golden
     for case in meta["permute"]:
-        if case["w"] != 32:
+        if not dmm.supported("permute", case["w"], case["m"]):
             continue
         out, reps = dmm.permute(arr[case["key"] + "_in"][None], [case["seed"]])
         assert (dmm.as_uint32(out)[0] == arr[case["key"] + "_out"]).all(), case["key"]
@@ -74,3 +74,22 @@ def test_permute_rejects_non_bijection(port):
     g[3, 3] = g[4, 4]
     with pytest.raises(dmm.InvalidInstance):
         dmm.permute(g[None], [5])
+
+
+@pytest.mark.parametrize("w,m,n_inst", [(64, 8, 12), (64, 16, 12), (128, 64, 6)])
+def test_permute_tall_vs_oracle(port, w, m, n_inst):
+    # machines taller than a warp (one per CTA); 128 x 64 is n = 8192, the BASELINE's n,
+    # at a shape the reference accepts
+    seeds = list(range(1, 1 + n_inst))
+    grids = np.stack([port.gen_instance(2, w, m, s) for s in seeds]).astype(np.uint32)
+    out, reps = dmm.permute(grids, seeds)
+    out = dmm.as_uint32(out)
+    for k, s in enumerate(seeds):
+        st, oout, orep = port.permute(grids[k], s)
+        assert st == 0
+        assert (out[k] == oout).all(), (w, m, s)
+        got = reps.report(k)
+        for f in FIELDS:
+            assert got[f] == orep[f], (w, m, s, f, got[f], orep[f])
+    exp = np.arange(w * m, dtype=np.uint32).reshape(1, w, m)
+    assert (out == exp).all()
