@@ -395,21 +395,31 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R) k_permute(
         // h(i) for the source rows i: row l evaluates h(l) once, keys fetch theirs by
         // shuffle (R = 32) or from the machine's hash table (one lookup instead of a 64-bit
         // splitmix64 per key)
-        const uint32_t h_row = hash_eval(key, M, (uint32_t)row);
-        if constexpr (kMulti) {
-            hsh[row] = h_row;
-            __syncthreads();
-        }
+        // R > 32: lane l of every warp holds h(l + 32 t) for t < R / 32 in registers and a key
+        // fetches h(i) with R / 32 shuffles (a shared table lookup by data-dependent row would
+        // conflict on banks)
+        constexpr int kHT = R / kWarp;
+        uint32_t h_reg[kHT];
+#pragma unroll
+        for (int t = 0; t < kHT; ++t)
+            h_reg[t] = hash_eval(key, M, (uint32_t)((row & 31) + kWarp * t));
+        const uint32_t h_row = h_reg[0];
         uint32_t col[M];
 #pragma unroll
         for (int c = 0; c < M; ++c) {
             const bool live = x[c] != empty;
             const uint32_t i = live ? x[c] / M : 0u, j = x[c] % M;
             uint32_t hi;
-            if constexpr (kMulti)
-                hi = hsh[i % R];
-            else
+            if constexpr (kMulti) {
+                hi = 0;
+#pragma unroll
+                for (int t = 0; t < kHT; ++t) {
+                    const uint32_t v = __shfl_sync(0xFFFFFFFFu, h_reg[t], (int)(i & 31u));
+                    hi = (i >> 5) == (uint32_t)t ? v : hi;
+                }
+            } else {
                 hi = __shfl_sync(0xFFFFFFFFu, h_row, (int)(i & 31u));
+            }
             col[c] = live ? (j + M - hi) % M : 0u;
             if (live)
                 H[col[c] * R + row] += 1;
