@@ -304,7 +304,8 @@ struct ToRowMajor {
 //                   loads its own slots (own-slot loads are conflict-free for any kappa);
 //      gather  (1): every lane stores into its own slots (conflict-free), then lane b
 //                   loads register d from its SOURCE slot;
-//  * lane-major (vector modes 2/3): slot (b, d) at word b * Q + (d - C0), Q = pitch, so a
+//  * lane-major (vector modes 2/3): slot (b, d) at word b * Q + S * (b / 8) + (d - C0), Q =
+//    pitch, S = skew per group of 8 rows (Q, S multiples of 4: 16-byte aligned rows), so a
 //    lane's own slots are contiguous and move as 128-bit STS.128 / LDS.128 (a quarter of
 //    the shared-memory instructions on the own side; the MIO queue is what stalls the
 //    relayout-heavy kernels):
@@ -315,21 +316,24 @@ struct ToRowMajor {
 //
 // find_layout picks, at compile time, the first layout (vector modes first) for which
 // every warp-wide access touches distinct banks -- the reference's CAC (core.hpp:445-467)
-// checked exhaustively over all lanes and registers.  Returns mode * 64 + k (k = kappa
-// for modes 0/1, Q - MV for modes 2/3) or -1.
+// checked exhaustively over all lanes and registers.  Returns mode * 4096 + k (k = kappa
+// for modes 0/1; (S / 4) * 64 + Q - MV for modes 2/3) or -1.
 __host__ __device__ constexpr int relayout_buf_words(int mv) {
     return (mv * (mv >= 32 ? 33 : 64)) > 32 * (mv + 4) ? (mv * (mv >= 32 ? 33 : 64)) : 32 * (mv + 4);
 }
 
+// lane-major slot address (vector modes)
+__host__ __device__ constexpr int v4_addr(int b, int d0, int Q, int S) { return b * Q + S * (b / 8) + d0; }
+
 template <class V, class Map>
-__host__ __device__ constexpr bool v4_own_ok(int Q) {  // own-slot 128-bit accesses, per quarter-warp
+__host__ __device__ constexpr bool v4_own_ok(int Q, int S) {  // own-slot 128-bit accesses, per quarter-warp
     for (int j = 0; j < V::MV / 4; ++j) {
         for (int q = 0; q < V::ROWS / 8; ++q) {
             uint32_t seen = 0;
             for (int a = 8 * q; a < 8 * q + 8; ++a) {
                 if (!V::active(a))
                     continue;
-                const int g = ((a * Q + 4 * j) / 4) & 7;
+                const int g = (v4_addr(a, 4 * j, Q, S) / 4) & 7;
                 if ((seen >> g) & 1u)
                     return false;
                 seen |= 1u << g;
@@ -340,7 +344,7 @@ __host__ __device__ constexpr bool v4_own_ok(int Q) {  // own-slot 128-bit acces
 }
 
 template <class V, class Map>
-__host__ __device__ constexpr bool v4_cross_ok(int Q, bool gather) {  // scalar cross accesses
+__host__ __device__ constexpr bool v4_cross_ok(int Q, int S, bool gather) {  // scalar cross accesses
     for (int c = V::C0; c < V::C0 + V::MV; ++c) {
         for (int w = 0; w < V::ROWS / 32; ++w) {  // one warp-wide instruction per warp
             uint32_t seen = 0;
@@ -349,7 +353,7 @@ __host__ __device__ constexpr bool v4_cross_ok(int Q, bool gather) {  // scalar 
                     continue;
                 const int b = gather ? Map::src_lane(lane, c) : Map::dst_lane(lane, c);
                 const int d = gather ? Map::src_col(lane, c) : Map::dst_col(lane, c);
-                const int bank = (b * Q + (d - V::C0)) & 31;
+                const int bank = v4_addr(b, d - V::C0, Q, S) & 31;
                 if ((seen >> bank) & 1u)
                     return false;
                 seen |= 1u << bank;
@@ -377,9 +381,11 @@ __host__ __device__ constexpr int find_layout() {
     }
     if (V::MV % 4 == 0 && V::C0 % 4 == 0 && quarters_whole) {
         for (int mode = 2; mode < 4; ++mode) {
-            for (int Q = V::MV; Q * V::ROWS <= relayout_words<V>(); Q += 4) {
-                if (v4_own_ok<V, Map>(Q) && v4_cross_ok<V, Map>(Q, mode == 2))
-                    return mode * 64 + (Q - V::MV);
+            for (int S = 0; S < 32; S += 4) {
+                for (int Q = V::MV; v4_addr(V::ROWS - 1, V::MV, Q, S) <= relayout_words<V>(); Q += 4) {
+                    if (v4_own_ok<V, Map>(Q, S) && v4_cross_ok<V, Map>(Q, S, mode == 2))
+                        return mode * 4096 + (S / 4) * 64 + (Q - V::MV);
+                }
             }
         }
     }
@@ -406,7 +412,7 @@ __host__ __device__ constexpr int find_layout() {
                 }
             }
             if (ok)
-                return mode * 64 + k;
+                return mode * 4096 + k;
         }
     }
     return -1;
@@ -434,12 +440,12 @@ __device__ __forceinline__ void relayout(uint32_t (&x)[M], uint32_t* buf, int la
     constexpr int L = find_layout<V, Map>();
     static_assert(L >= 0, "no conflict-free layout for this relayout");
     static_assert(map_is_consistent<V, Map>(), "relayout map is not a bijection with a matching inverse");
-    constexpr int mode = L / 64;
+    constexpr int mode = L / 4096;
     const bool act = V::active(lane);
     if constexpr (mode >= 2) {
-        constexpr int Q = V::MV + (L & 63);
-        static_assert(Q * V::ROWS <= relayout_words<V>(), "relayout buffer too small for this pitch");
-        uint32_t* own = buf + lane * Q;
+        constexpr int Q = V::MV + (L & 63), S = 4 * ((L / 64) & 63);
+        static_assert(v4_addr(V::ROWS - 1, V::MV, Q, S) <= relayout_words<V>(), "relayout buffer too small");
+        uint32_t* own = buf + v4_addr(lane, 0, Q, S);
         machine_sync<V>();
         if (act) {
             if constexpr (mode == 2) {
@@ -451,7 +457,7 @@ __device__ __forceinline__ void relayout(uint32_t (&x)[M], uint32_t* buf, int la
 #pragma unroll
                 for (int c = V::C0; c < V::C0 + V::MV; ++c) {
                     const int b = Map::dst_lane(lane, c), d = Map::dst_col(lane, c);
-                    buf[b * Q + (d - V::C0)] = x[c];
+                    buf[v4_addr(b, d - V::C0, Q, S)] = x[c];
                 }
             }
         }
@@ -461,7 +467,7 @@ __device__ __forceinline__ void relayout(uint32_t (&x)[M], uint32_t* buf, int la
 #pragma unroll
                 for (int d = V::C0; d < V::C0 + V::MV; ++d) {
                     const int a = Map::src_lane(lane, d), c = Map::src_col(lane, d);
-                    x[d] = buf[a * Q + (c - V::C0)];
+                    x[d] = buf[v4_addr(a, c - V::C0, Q, S)];
                 }
             } else {
 #pragma unroll
@@ -475,7 +481,7 @@ __device__ __forceinline__ void relayout(uint32_t (&x)[M], uint32_t* buf, int la
             }
         }
     } else {
-        constexpr int P = V::ROWS + (L & 63);
+        constexpr int P = V::ROWS + (L & 63);  // scalar modes: kappa in the low bits
         constexpr bool gather = mode == 1;
         static_assert(V::MV * P <= relayout_words<V>(), "relayout buffer too small for this skew");
         machine_sync<V>();
