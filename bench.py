@@ -145,6 +145,21 @@ def cpu_baseline(cfg_name: str, seconds: float = 15.0):
                       f"{good}/{sample} correct"}
 
 
+def smem_line(traffic, ms):
+    """Shared-memory side of the roofline: the committed ncu capture's wavefronts per launch
+    (x 128 B) over this run's launch time, against 128 B/clk/SM x 148 SMs at the max SM clock;
+    plus its bank-conflict count (excessive wavefronts)."""
+    if not traffic or "smem_wavefronts" not in traffic:
+        return None
+    peaks, _ = _peaks()
+    peak = 128 * 148 * peaks.get("sm_max_mhz", 1965.0) / 1e3  # GB/s
+    achieved = traffic["smem_wavefronts"] * 128 / (ms / 1e3) / 1e9
+    return {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "wavefronts_per_launch": traffic["smem_wavefronts"],
+            "excessive_wavefronts_per_launch": traffic["smem_excessive_wavefronts"],
+            "source": traffic.get("source")}
+
+
 def measured_traffic(cfg_name: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the config's dominant kernel,
     from the committed ncu --set full capture (profiles/traffic.json, written by
@@ -338,6 +353,7 @@ def main():
                          "traffic_source": (traffic or {}).get("source"),
                          "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
                          else "fallback 6650 GB/s"},
+            "smem": smem_line(traffic, ms),
             "e2e": {"value": total_keys / (e2e_ms / 1e3), "unit": "keys/s",
                     "h2d_bytes_per_step": keys_per_gpu * 4, "d2h_bytes_per_step": keys_per_gpu * 4},
             "gpu_launches": launches_per_step * args.steps,

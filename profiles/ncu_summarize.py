@@ -100,8 +100,18 @@ def traffic(args):
         m = raw_metrics(rep)
         rd = to_bytes(*m["dram__bytes_read.sum"])
         wr = to_bytes(*m["dram__bytes_write.sum"])
+        dur_us = float(m["gpu__time_duration.sum"][0].replace(",", ""))
+        wf = float(m["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"][0].replace(",", ""))
+        exc = float(m["derived__memory_l1_wavefronts_shared_excessive"][0].replace(",", ""))
+        clk = float(m["sm__cycles_elapsed.avg.per_second"][0].replace(",", ""))  # GHz
+        # shared memory: one wavefront moves up to 128 B; peak 128 B/clk/SM x 148 SMs
+        smem_peak_gbs = 128 * 148 * clk
         out[cfg] = {"kernel": m["Kernel Name"][0][:120], "bytes_per_launch": rd + wr, "read_bytes": rd,
-                    "write_bytes": wr, "ncu_duration_us": float(m["gpu__time_duration.sum"][0].replace(",", "")),
+                    "write_bytes": wr, "ncu_duration_us": dur_us,
+                    "smem_wavefronts": wf, "smem_excessive_wavefronts": exc,
+                    "smem_wavefront_bytes_per_launch": wf * 128, "smem_peak_gbs_at_clock": smem_peak_gbs,
+                    "smem_frac_of_peak_under_ncu": (wf / (dur_us * 1e-6)) / (148 * clk * 1e9),
+                    "issue_active_pct": float(m["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]),
                     "source": os.path.join(src_dir or os.path.dirname(rep), os.path.basename(rep))}
         print(cfg, out[cfg])
     with open(path, "w") as f:
