@@ -89,7 +89,7 @@ def traffic(args):
         i = args.index("--source-dir")
         src_dir = args[i + 1]
         args = args[:i] + args[i + 2:]
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "traffic.json")
+    path = os.environ.get("TRAFFIC_JSON") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "traffic.json")
     try:
         with open(path) as f:
             out = json.load(f)

@@ -1,19 +1,24 @@
 #!/bin/bash
-# One round's measurement pass (run under gpurun on ONE B200, from the repo root):
-# bench lines for every config (with the reference CPU baseline), the default bench and the
-# reference arm, then an ncu launch list + one full-set capture per config.
+# ncu evidence for one round (run under gpurun on ONE B200, from the repo root): per config, the
+# plain command first, then an ncu launch list and one full-set capture of its dominant kernel,
+# summarised on the box (the .ncu-rep files stay there: gpurun_out/ returns at most 64 MiB).
+#   bash profiles/round_capture.sh <tag> [configs...]
 set -u
 TAG=${1:-r01}
+shift || true
+LIST=${*:-"cfg1:k_general_sort cfg2:k_general_sort cfg2b:k_general_sort cfg3:k_tile_sort cfg4:k_permute cfg4s:k_permute cfg5:k_ms_scatter"}
 mkdir -p gpurun_out/$TAG
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/$TAG/gpu.txt
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/$TAG/pytest_gpu.log 2>&1; echo "pytest rc=$?"
-for c in cfg1 cfg2 cfg2b cfg3 cfg4; do
-    timeout 400 python bench.py --config $c --steps 20 --warmup 5 > gpurun_out/$TAG/bench_$c.json 2> gpurun_out/$TAG/bench_$c.err
-    echo "bench $c rc=$?"
-done
-timeout 400 python bench.py > gpurun_out/$TAG/bench_default.json 2> gpurun_out/$TAG/bench_default.err; echo "default rc=$?"
-timeout 400 python bench.py --impl reference > gpurun_out/$TAG/bench_reference.json 2>&1; echo "reference rc=$?"
-for a in "cfg1 k_general_sort" "cfg2 k_general_sort" "cfg2b k_general_sort" "cfg3 k_tile_sort" "cfg4 k_permute"; do
-    set -- $a
-    timeout 600 bash profiles/ncu_capture.sh $1 $TAG $2 && echo "ncu $1 ok"
+cp profiles/traffic.json gpurun_out/$TAG/traffic.json 2>/dev/null
+for a in $LIST; do
+    c=${a%%:*}; k=${a##*:}
+    if timeout 900 bash profiles/ncu_capture.sh $c $TAG $k; then
+        rep=gpurun_out/prof_${c}_${TAG}.ncu-rep
+        python profiles/ncu_summarize.py $rep 16 > gpurun_out/$TAG/summary_${c}.txt 2>&1
+        ncu -i $rep --page details --csv > gpurun_out/$TAG/details_${c}.csv 2>/dev/null
+        TRAFFIC_JSON=gpurun_out/$TAG/traffic.json python profiles/ncu_summarize.py --traffic $c=$rep \
+            --source-dir profiles/$TAG > /dev/null 2>&1
+        mv gpurun_out/launches_${c}_${TAG}.csv gpurun_out/$TAG/
+        rm -f $rep
+        echo "ncu $c ok"
+    fi
 done
