@@ -74,3 +74,14 @@ def test_layout_and_sort_shape_contracts(lib):
 def test_missing_library_fails_loudly(tmp_path):
     with pytest.raises(ImportError):
         _lib.load(str(tmp_path / "nope.so"))
+
+
+def test_probe_snapshot_count_matches_reference_hooks(lib, ref):
+    # dmm_general_probe_snaps = the number of PartitionProbe hook calls of the outer recursion
+    # (after_balance + after_divide per level, partition.hpp:376-390), host-side, no GPU needed
+    import numpy as np
+    for (w, m) in [(32, 16), (16, 8), (64, 16), (256, 16), (64, 8), (128, 32), (32, 32), (8, 8)]:
+        g = ref.gen_instance(1, w, m, 1)
+        st, _, rep = ref.integer_sort_general(g, w, enforce_pre=False, probe_snaps=64)
+        assert st == 0
+        assert lib.dmm_general_probe_snaps(w, m, 0) == rep["snapshots"].shape[0], (w, m)

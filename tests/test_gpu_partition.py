@@ -208,3 +208,21 @@ def test_probe_batch_matches_plain_run(port, w, m):
     assert (np.sort(s[:, -1].reshape(11, -1), axis=1) == np.sort(grids.reshape(11, -1), axis=1)).all()
     _, st2 = dmm.partition_general(port.gen_instance(1, 32, 32, 1), probe=True)
     assert st2.snapshots.shape == (0, 32, 32)
+
+
+def test_empty_and_single_batches(port):
+    # count 0: no launch, no error; count 1: a lone packed half / lone machine in its warp or CTA
+    empty = np.zeros((0, 32, 16), dtype=np.uint32)
+    out, st = dmm.partition_general(empty)
+    assert out.shape == (0, 32, 16) and st.cleanup_retries.numel() == 0
+    out, _ = dmm.integer_sort_general(np.zeros((0, 64, 16), dtype=np.uint32), 1024)
+    assert out.shape == (0, 64, 16)
+    assert dmm.sort_tall(np.zeros((0, 128, 32), dtype=np.uint32)).shape == (0, 128, 32)
+    for (w, m) in [(32, 16), (4, 8), (64, 16)]:
+        g = port.gen_instance(1, w, m, 9).astype(np.uint32)
+        out, st = dmm.partition_general(g[None], flags=dmm.FLAG_NO_ENFORCE_PRE)
+        s, exp, rep = port.partition_general(g, dmm.FLAG_NO_ENFORCE_PRE)
+        assert (dmm.as_uint32(out)[0] == exp).all() and int(st.cleanup_retries[0]) == rep["cleanup_retries"]
+    keys = dmm.gen_keys(0, 0)
+    out, starts = dmm.multisplit(keys, 8, 29)
+    assert out.numel() == 0
