@@ -39,6 +39,10 @@ constexpr int kRngWords = 312;
 #define DMM_PERM_WARPS 4
 #endif
 constexpr int kPermWarps = DMM_PERM_WARPS;
+// CTAs per SM asked of ptxas for 128-row machines (register cap 65536 / (128 * minb))
+#ifndef DMM_PERM_TALL_MINB
+#define DMM_PERM_TALL_MINB 3
+#endif
 
 // Collective primitives of one machine of R rows: one warp (R = 32: shuffles and warp
 // votes) or one CTA of R / 32 warps (R > 32: a machine barrier and an exchange array `xch`
@@ -284,13 +288,19 @@ __device__ __forceinline__ bool finish_packed(uint32_t (&y)[WP], uint32_t* buf, 
     return true;
 }
 
+// stage = [H: per-colour counts / bucket bounds as bytes (<= m <= 64), ceil(M/4)*R words | B: the
+// colour-sorted rows, M*R words]; the relayout buffer overlays it (B's contents are always in
+// registers before a sort uses the buffer)
+template <int M, int R>
+__host__ __device__ constexpr int perm_h_words() { return ((M + 3) / 4) * R; }  // 4 colours per word
 template <int M, int R>
 __host__ __device__ constexpr int perm_stage_words() {
-    return (2 * M * R > relayout_buf_words(M) * (R / 32) ? 2 * M * R : relayout_buf_words(M) * (R / 32));
+    return (perm_h_words<M, R>() + M * R > relayout_buf_words(M) * (R / 32) ? perm_h_words<M, R>() + M * R
+                                                                             : relayout_buf_words(M) * (R / 32));
 }
 template <int M, int R>
 __host__ __device__ constexpr int perm_machine_words() {  // u32 words of smem per machine
-    return 2 * kRngWords + M * R + perm_stage_words<M, R>() + (R > kWarp ? R + 32 : 0);
+    return 2 * kRngWords + M * R + perm_stage_words<M, R>();
 }
 template <int R>
 __host__ __device__ constexpr int perm_machines_per_cta() { return R > kWarp ? 1 : kPermWarps; }
@@ -314,7 +324,7 @@ __device__ __forceinline__ bool finish_width(uint32_t width, const uint32_t* pk,
 }
 
 template <int M, int R>
-__global__ void __launch_bounds__(perm_machines_per_cta<R>() * R) k_permute(
+__global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DMM_PERM_TALL_MINB : 1)) k_permute(
     const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count, const uint64_t* __restrict__ seeds,
     const uint64_t* __restrict__ states, PermArgs a, dmm_permute_report* __restrict__ reps, uint64_t* __restrict__ hist,
     uint32_t* __restrict__ shifts_out, uint8_t* __restrict__ status) {
@@ -329,12 +339,17 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R) k_permute(
     MachRng<R> rng{wbase, wbase + kRngWords, 0};
     uint32_t* outs = wbase + 2 * kRngWords;     // output region, row i in column i: outs[j*R + i]
     uint32_t* stage = outs + M * R;             // relayout buffer / own-bank rows A,B,H
-    uint32_t* pk = stage + M * R;               // packed rows (own bank), capacity m: aliases B,
-                                                // which is dead from packing until the finish
-    uint32_t* H = stage;                        // per-colour counts, then bucket starts
-    uint32_t* B = stage + M * R;                // colour-sorted (compacted) row
-    uint32_t* hsh = stage + perm_stage_words<M, R>();  // R > 32: per-row hashes / exchange
-    const Mach<R> mc{hsh, hsh + R, row};
+    uint32_t* B = stage + perm_h_words<M, R>();  // colour-sorted (compacted) row
+    uint32_t* pk = B;                            // packed rows (own column), capacity m: aliases B,
+                                                 // which is dead from packing until the finish
+    uint8_t* H = reinterpret_cast<uint8_t*>(stage);  // per-colour counts, then bucket bounds
+    // colour b of this row: byte b % 4 of word (b / 4) * R + row -- the row's own bank, for
+    // any (data-dependent) colour
+    auto hx = [&](uint32_t b) -> uint32_t { return (((b >> 2) * (uint32_t)R + (uint32_t)row) << 2) | (b & 3u); };
+    // R > 32: the machine's exchange / reduction scratch overlays the start of the colour
+    // counts H: every use (input check, leftover sum, packing rounds, finish reductions,
+    // delivery) falls where H is dead (and CTA barriers separate them from its uses)
+    const Mach<R> mc{stage, stage + R, row};
     const uint64_t k = (uint64_t)blockIdx.x * perm_machines_per_cta<R>() + mach;
     if (k >= count)
         return;
@@ -367,11 +382,11 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R) k_permute(
         mc.sync();
 #pragma unroll
         for (int c = 0; c < M; ++c)
-            H[((c + sh) % M) * R + row] = x[c];  // own bank: row r rotates in its own column
+            B[((c + sh) % M) * R + row] = x[c];  // own bank: row r rotates in its own column
         mc.sync();
 #pragma unroll
         for (int c = 0; c < M; ++c)
-            x[c] = H[c * R + row];
+            x[c] = B[c * R + row];
         using Blk = VF<0xFFFFFFFFu, 0, 1, M, 0, M, R, R>;  // every aligned m x m block of rows
         transpose_square<Blk>(x, stage, row);
     }
@@ -391,7 +406,7 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R) k_permute(
         mc.sync();
 #pragma unroll
         for (int b = 0; b < M; ++b)
-            H[b * R + row] = 0;
+            H[hx(b)] = 0;
         // h(i) for the source rows i: row l evaluates h(l) once, keys fetch theirs by
         // shuffle (R = 32) or from the machine's hash table (one lookup instead of a 64-bit
         // splitmix64 per key)
@@ -404,11 +419,11 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R) k_permute(
         for (int t = 0; t < kHT; ++t)
             h_reg[t] = hash_eval(key, M, (uint32_t)((row & 31) + kWarp * t));
         const uint32_t h_row = h_reg[0];
-        uint32_t col[M];
-#pragma unroll
-        for (int c = 0; c < M; ++c) {
-            const bool live = x[c] != empty;
-            const uint32_t i = live ? x[c] / M : 0u, j = x[c] % M;
+        // colour of a label (recomputed in both passes: keeping M colours live would cost M
+        // registers)
+        auto colour_of = [&](uint32_t lab) -> uint32_t {
+            const bool live = lab != empty;
+            const uint32_t i = live ? lab / M : 0u, j = lab % M;
             uint32_t hi;
             if constexpr (kMulti) {
                 hi = 0;
@@ -420,17 +435,21 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R) k_permute(
             } else {
                 hi = __shfl_sync(0xFFFFFFFFu, h_row, (int)(i & 31u));
             }
-            col[c] = live ? (j + M - hi) % M : 0u;
-            if (live)
-                H[col[c] * R + row] += 1;
+            return (j + M - hi) % M;
+        };
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+            const uint32_t cl = colour_of(x[c]);
+            if (x[c] != empty)
+                H[hx(cl)] += 1;
         }
         uint32_t run = 0;
         uint32_t row_left = 0;
 #pragma unroll
         for (int b = 0; b < M; ++b) {
-            const uint32_t cnt = H[b * R + row];
+            const uint32_t cnt = H[hx(b)];
             row_left += cnt > a.alpha ? cnt - a.alpha : 0;
-            H[b * R + row] = run;  // bucket start
+            H[hx(b)] = (uint8_t)run;  // bucket start
             run += cnt;
         }
 #pragma unroll
@@ -440,9 +459,10 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R) k_permute(
         // scatter into the colour-sorted order
 #pragma unroll
         for (int c = 0; c < M; ++c) {
+            const uint32_t cl = colour_of(x[c]);
             if (x[c] != empty) {
-                const uint32_t pos = H[col[c] * R + row];
-                H[col[c] * R + row] = pos + 1;
+                const uint32_t pos = H[hx(cl)];
+                H[hx(cl)] = (uint8_t)(pos + 1);
                 B[pos * R + row] = x[c];
             }
         }
@@ -454,8 +474,8 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R) k_permute(
         // A sent label's cell becomes empty in place (the compacted row keeps its holes):
         // exactly the first min(count, alpha) cells of every colour bucket.
         for (int kc = 0; kc < M; ++kc) {
-            const uint32_t end = H[kc * R + row];
-            const uint32_t start = kc == 0 ? 0u : H[(kc - 1) * R + row];
+            const uint32_t end = H[hx(kc)];
+            const uint32_t start = kc == 0 ? 0u : H[hx(kc - 1)];
             const uint32_t take = min(end - start, a.alpha);
             for (uint32_t p = 0; p < take; ++p) {
                 const uint32_t label = B[(start + p) * R + row];
@@ -566,22 +586,17 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R) k_permute(
             for (int c = 0; c < M; ++c)
                 y[c] = B[c * R + row];
         }
-        uint32_t y_keep[M];
-#pragma unroll
-        for (int c = 0; c < M; ++c)
-            y_keep[c] = y[c];
         uint32_t r2 = 0;
         if (!finish_packed<M, M, R>(y, stage, B, outs, mc, empty, r2) && M < W) {
-            // last resort: comparison tall sort on the compacted multiset (permute.hpp:618-625).
-            // The reference sorts the working window left by the failed attempt; any
-            // arrangement of the same multiset sorts to the same matrix.
+            // last resort: comparison tall sort of the working window left by the failed
+            // attempt (permute.hpp:618-625) -- y, the same multiset in the attempt's arrangement
             using V = VF<0xFFFFFFFFu, 0, 1, R, 0, M, R, R>;
             if constexpr (M < W)
-                sort_tall<1, V>(y_keep, stage, row);
+                sort_tall<1, V>(y, stage, row);
             mc.sync();
 #pragma unroll
             for (int c = 0; c < M; ++c)
-                B[c * R + row] = y_keep[c];
+                B[c * R + row] = y[c];
             mc.sync();
             three_phase_delivery<M, R>(B, M, outs, mc, empty);
         } else {
