@@ -157,6 +157,8 @@ def smem_line(traffic, ms):
     return {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "wavefronts_per_launch": traffic["smem_wavefronts"],
             "excessive_wavefronts_per_launch": traffic["smem_excessive_wavefronts"],
+            # what actually bounds these kernels: the SM's instruction issue (ncu, same launch)
+            "issue_active_pct_of_peak": traffic.get("issue_active_pct"),
             "source": traffic.get("source")}
 
 
