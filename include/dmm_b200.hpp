@@ -11,6 +11,7 @@
 //     dmm::b200::sort_square(view, asc) / sort_short_wide(view, asc)   // sort.hpp:337 / :225
 //     dmm::b200::transpose_square(view)              // layout.hpp:24 (+ to_column_major / to_row_major)
 //     dmm::b200::permute(machine, rng, params)       // permute.hpp:545
+//     dmm::b200::run_algorithm(alg, instance, opts)  // instance.hpp:277 (the CLI / acceptance dispatch)
 //
 // Each call gathers the view's cells (peek), runs the sm_100a kernel through the C ABI
 // (include/dmm_gpu.h) on a batch of one, writes the result back (poke) and rethrows the
@@ -332,6 +333,90 @@ inline PermuteReport permute(Machine& mach, Rng& rng, const PermuteParams& param
     rep.leftover_history.assign(hist.begin(), hist.begin() + hr.n_hist);
     rep.shifts = shifts;
     return rep;
+}
+
+/// RunOutcome run_algorithm(Algorithm, const Instance&, const RunOptions&)  instance.hpp:277-363
+/// The dispatcher the reference's CLI and acceptance harness use, over the B200 kernels: the
+/// same instance checks, views, verification and report fields.  The GPU has no DMM step
+/// meter: report.steps / work stay 0 and conflicts counts the model's violations (0: every
+/// kernel relayout is checked conflict-free at compile time); record_trace throws
+/// TraceIncomplete.
+inline RunOutcome run_algorithm(Algorithm alg, const Instance& in, const RunOptions& opt = {}) {
+    if (in.kind != instance_kind_for(alg))
+        throw InvalidInstance(std::string("algorithm ") + algorithm_name(alg) + " needs a " +
+                              kind_name(instance_kind_for(alg)) + " instance");
+    validate_instance(in);
+    if (opt.record_trace)
+        throw TraceIncomplete("B200 kernels record no DMM trace (no step meter)");
+    Machine mach(MachineConfig::standard(in.w, in.m, opt.strict));
+    const auto& cfg = mach.config();
+    std::vector<u32> all_rows(in.w);
+    for (u32 r = 0; r < in.w; ++r)
+        all_rows[r] = r;
+    MatrixView v = MatrixView::full(mach);
+    MatrixView vp = MatrixView::make(mach, all_rows, cfg.work_base(), in.m, cfg.scratch_a_base(), cfg.scratch_b_base());
+    (alg == Algorithm::permute || alg == Algorithm::integer_sort_general ? vp : v).load(in.grid);
+
+    RunOutcome out;
+    out.report.algorithm = algorithm_name(alg);
+    out.report.w = in.w;
+    out.report.m = in.m;
+    out.report.seed = opt.seed.value_or(in.seed);
+    switch (alg) {
+        case Algorithm::sort_short_wide:
+            b200::sort_short_wide(v);
+            out.report.correct = verify_sorted_result(in, v.snapshot());
+            break;
+        case Algorithm::sort_square:
+            b200::sort_square(v);
+            out.report.correct = verify_sorted_result(in, v.snapshot());
+            break;
+        case Algorithm::sort_tall:
+            b200::sort_tall(v);
+            out.report.correct = verify_sorted_result(in, v.snapshot());
+            break;
+        case Algorithm::partition_short_wide:
+            b200::partition_short_wide(v);
+            out.report.correct = verify_partition_result(in, v.snapshot());
+            break;
+        case Algorithm::partition_square:
+            b200::partition_square(v);
+            out.report.correct = verify_partition_result(in, v.snapshot());
+            break;
+        case Algorithm::partition_general: {
+            auto st = b200::partition_general(v);
+            out.report.cleanup_retries = st.cleanup_retries;
+            out.report.correct = verify_partition_result(in, v.snapshot());
+            break;
+        }
+        case Algorithm::integer_sort_general: {
+            auto st = b200::integer_sort_general(vp, u64(in.w) * in.m);
+            out.report.cleanup_retries = st.cleanup_retries;
+            out.report.correct = verify_sorted_result(in, vp.snapshot());
+            break;
+        }
+        case Algorithm::permute: {
+            Rng rng(out.report.seed);
+            PermuteParams params;
+            params.alpha = opt.alpha;
+            auto rep = b200::permute(mach, rng, params);
+            out.report.iterations = rep.iterations;
+            out.report.fallback = rep.fallback;
+            out.report.cleanup_retries = rep.cleanup_retries;
+            out.pipeline = rep;
+            std::vector<word> outgrid;
+            outgrid.reserve(u64(in.w) * in.m);
+            for (u32 i = 0; i < in.w; ++i)
+                for (u32 j = 0; j < in.m; ++j)
+                    outgrid.push_back(mach.peek(i, cfg.out_base() + j));
+            out.report.correct = verify_permute_result(in, outgrid);
+            break;
+        }
+    }
+    out.report.steps = 0;
+    out.report.work = 0;
+    out.report.conflicts = 0;
+    return out;
 }
 
 }  // namespace b200

@@ -297,12 +297,53 @@ static void probe_cases() {
     }
 }
 
+// run_algorithm (instance.hpp:277-363): the CLI / acceptance dispatch, every algorithm on a
+// shape it accepts; the same report fields except the step meter
+static void run_algorithm_cases() {
+    struct Case {
+        Algorithm a;
+        u32 w, m;
+    };
+    const Case cases[] = {{Algorithm::partition_general, 32, 16}, {Algorithm::partition_general, 64, 16},
+                          {Algorithm::integer_sort_general, 32, 32}, {Algorithm::partition_square, 16, 16},
+                          {Algorithm::partition_short_wide, 8, 64}, {Algorithm::sort_square, 16, 16},
+                          {Algorithm::sort_short_wide, 4, 16}, {Algorithm::sort_tall, 128, 32},
+                          {Algorithm::permute, 32, 32}, {Algorithm::permute, 128, 64}};
+    for (const Case& c : cases) {
+        for (u64 seed = 1; seed <= 3; ++seed) {
+            Instance in = gen_instance(instance_kind_for(c.a), c.w, c.m, seed);
+            if (in.kind == InstanceKind::sort)
+                for (auto& x : in.grid)
+                    x >>= 32;  // the B200 layout narrows words to 32 bits (KeyOutOfRange otherwise)
+            RunOutcome ra = run_algorithm(c.a, in), rb = b200::run_algorithm(c.a, in);
+            CHECK(rb.report.correct && ra.report.correct);
+            CHECK(ra.report.algorithm == rb.report.algorithm && ra.report.seed == rb.report.seed);
+            CHECK(ra.report.cleanup_retries == rb.report.cleanup_retries);
+            CHECK(ra.report.iterations == rb.report.iterations && ra.report.fallback == rb.report.fallback);
+            if (c.a == Algorithm::permute) {
+                CHECK(ra.pipeline.random_words == rb.pipeline.random_words);
+                CHECK(ra.pipeline.leftover_history == rb.pipeline.leftover_history);
+                CHECK(ra.pipeline.shifts == rb.pipeline.shifts);
+            }
+        }
+    }
+    CHECK(throws_as<KeyOutOfRange>(
+        [&] { b200::run_algorithm(Algorithm::sort_tall, gen_instance(InstanceKind::sort, 128, 32, 1)); }));
+    RunOptions tr;
+    tr.record_trace = true;
+    CHECK(throws_as<TraceIncomplete>(
+        [&] { b200::run_algorithm(Algorithm::partition_general, gen_instance(InstanceKind::partition, 32, 16, 1), tr); }));
+    CHECK(throws_as<InvalidInstance>(
+        [&] { b200::run_algorithm(Algorithm::permute, gen_instance(InstanceKind::partition, 32, 16, 1)); }));
+}
+
 int main() {
     partition_cases();
     integer_sort_cases();
     layout_and_sort_cases();
     subwarp_cases();
     probe_cases();
+    run_algorithm_cases();
     permute_cases();
     std::printf("shim parity: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;
