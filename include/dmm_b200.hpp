@@ -21,8 +21,8 @@
 //
 // Not reproduced (GPU kernels have no DMM step meter): Machine::steps()/work() do not
 // advance; PartitionProbe hooks are replayed from the kernel's snapshots (the caller's
-// machine holds the reference's window at each call); ShortWideHook and traces are
-// unsupported (Error); permute() reproduces
+// machine holds the reference's window at each call), ShortWideHook calls likewise; traces
+// are unsupported (TraceIncomplete); permute() reproduces
 // the output region, the report and the Rng position, not the scratch/counter cells.
 // Words must fit in 32 bits (KeyOutOfRange otherwise).  Requires <dmm/dmm.hpp>.
 #pragma once
@@ -217,9 +217,30 @@ inline void sort_tall(const MatrixView& v) {
     detail::simple(v, [&](uint32_t* p) { return dmm_sort_tall(p, p, v.W(), v.M(), 1, nullptr); }, "sort_tall");
 }
 namespace detail {
-inline void no_hook(const ShortWideHook& hook) {
-    if (hook)
-        throw Error("ShortWideHook observation points are not supported by the B200 kernels");
+// ShortWideHook replay (sort.hpp:189-218): the kernel's literal skeleton captured the window
+// at the three stages; the caller's machine holds each when its hook call happens.
+inline void short_wide_hooked(const MatrixView& v, bool partition, bool ascending, const ShortWideHook& hook,
+                              const char* where) {
+    std::vector<uint32_t> g = gather(v);
+    DeviceBuffer d(sizeof(uint32_t) * g.size()), ss(16), dsnap(sizeof(uint32_t) * 3 * g.size());
+    to_device(d, g);
+    check(dmm_short_wide_probe(d.as<uint32_t>(), d.as<uint32_t>(), v.W(), v.M(), 1, partition ? 1 : 0,
+                               ascending ? 1 : 0, ss.as<uint8_t>(), dsnap.as<uint32_t>(), nullptr),
+          where);
+    uint8_t status = 0;
+    cuda_check(cudaMemcpy(&status, ss.ptr, 1, cudaMemcpyDeviceToHost), "D2H");
+    if (status != DMM_OK)  // check_partition_instance fails before any stage
+        raise(static_cast<dmm_status>(status), where);
+    std::vector<uint32_t> snaps(3 * g.size());
+    to_host(snaps, dsnap);
+    const ShortWideStage stages[3] = {ShortWideStage::after_first_convert, ShortWideStage::after_first_pass,
+                                      ShortWideStage::done};
+    for (int i = 0; i < 3; ++i) {
+        scatter(v, std::vector<uint32_t>(snaps.begin() + i * g.size(), snaps.begin() + (i + 1) * g.size()));
+        hook(stages[i]);
+    }
+    to_host(g, d);
+    scatter(v, g);
 }
 // a partition entry point: per-instance status -> the reference's exception
 template <class Fn>
@@ -245,7 +266,10 @@ inline void partition_square(const MatrixView& v) {
 }
 /// void partition_short_wide(const MatrixView&, const ShortWideHook& = {})  partition.hpp:178-185
 inline void partition_short_wide(const MatrixView& v, const ShortWideHook& hook = {}) {
-    detail::no_hook(hook);
+    if (u64(v.W()) * v.W() > v.M())
+        throw ShapeViolation("partition_short_wide needs w^2 <= m");
+    if (hook)
+        return detail::short_wide_hooked(v, true, true, hook, "partition_short_wide");
     detail::partition_entry(
         v, [&](uint32_t* p, uint8_t* st) { return dmm_partition_short_wide(p, p, v.W(), v.M(), 1, st, nullptr); },
         "partition_short_wide");
@@ -257,7 +281,11 @@ inline void sort_square(const MatrixView& v, bool ascending = true) {
 }
 /// void sort_short_wide(const MatrixView&, bool ascending = true, const ShortWideHook& = {})  sort.hpp:225-230
 inline void sort_short_wide(const MatrixView& v, bool ascending = true, const ShortWideHook& hook = {}) {
-    detail::no_hook(hook);
+    if (hook) {
+        if (u64(v.W()) * v.W() > v.M())
+            throw ShapeViolation("short-wide sort needs w^2 <= m");
+        return detail::short_wide_hooked(v, false, ascending, hook, "sort_short_wide");
+    }
     detail::simple(v,
                    [&](uint32_t* p) { return dmm_sort_short_wide(p, p, v.W(), v.M(), 1, ascending ? 1 : 0, nullptr); },
                    "sort_short_wide");

@@ -100,6 +100,12 @@ dmm_status dmm_integer_sort_general_probe(const uint32_t* in, uint32_t* out, uin
                                           uint64_t domain, uint32_t flags, dmm_general_stats* stats, uint8_t* status,
                                           uint32_t* snapshots, uint32_t max_snaps, void* stream);
 
+/* ShortWideHook capture (sort.hpp:189-218): partition_short_wide (partition != 0) or
+ * sort_short_wide(ascending) run as the literal short-wide skeleton, writing the w x m window at
+ * after_first_convert, after_first_pass and done to snapshots[k * 3 * w * m ...]. */
+dmm_status dmm_short_wide_probe(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                int partition, int ascending, uint8_t* status, uint32_t* snapshots, void* stream);
+
 /* void partition_square(const MatrixView&)                       partition.hpp:189-197 */
 dmm_status dmm_partition_square(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
                                 uint8_t* status, void* stream);

@@ -67,6 +67,31 @@ __host__ __device__ constexpr PParams pparams_c(int W, int M, bool ext) {
     return p;
 }
 
+// PartitionProbe (partition.hpp:298-301) capture: the full working window after every
+// balance (after_balance) and every convert-and-divide (after_divide) of the OUTER
+// recursion, in the order the reference calls its hooks.  Each lane stores its row of
+// the window; with PK = 2 each 16-bit half goes to its own instance's snapshot area.
+struct ProbeSink {
+    uint32_t* dst[2];  // per half: this instance's snapshot area (max x WM x M words) or null
+    uint32_t n, max;
+    int row, wm;
+    template <int PK, int M>
+    __device__ __forceinline__ void capture(const uint32_t (&x)[M]) {
+        if (n < max) {
+#pragma unroll
+            for (int h = 0; h < PK; ++h) {
+                if (dst[h] == nullptr)
+                    continue;
+                uint32_t* q = dst[h] + ((size_t)n * wm + row) * M;
+#pragma unroll
+                for (int c = 0; c < M; ++c)
+                    q[c] = PK == 2 ? ((x[c] >> (16 * h)) & 0xFFFFu) : x[c];
+            }
+        }
+        ++n;
+    }
+};
+
 // ---------------------------------------------------------------------------
 // Column sorts and skeletons  sort.hpp:162-311
 // ---------------------------------------------------------------------------
@@ -82,20 +107,33 @@ __device__ __forceinline__ void sort_columns_blocked(uint32_t (&x)[M], uint32_t*
 }
 
 // short_wide_skeleton sort.hpp:200-218 (Lemma 1); asc may differ per lane (per view)
+// ps: ShortWideHook capture (sort.hpp:189-218): after_first_convert, after_first_pass, done
 template <int PK, class V, int M>
-__device__ __forceinline__ void short_wide(uint32_t (&x)[M], uint32_t* buf, int lane, bool asc) {
+__device__ __forceinline__ void short_wide(uint32_t (&x)[M], uint32_t* buf, int lane, bool asc,
+                                           ProbeSink* ps = nullptr) {
     static_assert(V::WV * V::WV <= V::MV, "short-wide needs w^2 <= m (ShapeViolation)");
     if constexpr (V::WV == 1) {
         row_sort<PK, V>(x, lane, asc);
+        if (ps) {  // conversions of a one-row view are no-ops: every stage sees the sorted row
+            ps->template capture<PK>(x);
+            ps->template capture<PK>(x);
+            ps->template capture<PK>(x);
+        }
     } else {
 #pragma unroll 1
         for (int pass = 0; pass < 2; ++pass) {
             row_sort<PK, V>(x, lane, alt_dir<V>(lane, asc));
             to_column_major<V>(x, buf, lane);
+            if (ps && pass == 0)
+                ps->template capture<PK>(x);  // ShortWideStage::after_first_convert
             row_sort<PK, V>(x, lane, asc);
             to_row_major<V>(x, buf, lane);
+            if (ps && pass == 0)
+                ps->template capture<PK>(x);  // ShortWideStage::after_first_pass
         }
         row_sort<PK, V>(x, lane, asc);
+        if (ps)
+            ps->template capture<PK>(x);  // ShortWideStage::done
     }
 }
 
@@ -143,9 +181,10 @@ __device__ __forceinline__ void shearsort_rect(uint32_t (&x)[M], uint32_t* buf, 
 
 // sort_wide_any sort.hpp:321-330 (comparison sorter, W <= M, W | M)
 template <int PK, class V, int M>
-__device__ __forceinline__ void sort_wide_any(uint32_t (&x)[M], uint32_t* buf, int lane, bool asc) {
+__device__ __forceinline__ void sort_wide_any(uint32_t (&x)[M], uint32_t* buf, int lane, bool asc,
+                                              ProbeSink* ps = nullptr) {
     if constexpr (V::WV * V::WV <= V::MV)
-        short_wide<PK, V>(x, buf, lane, asc);
+        short_wide<PK, V>(x, buf, lane, asc, ps);
     else if constexpr (square_fits_c(V::WV, V::MV))
         square_skeleton<PK, V>(x, buf, lane, asc);
     else
@@ -351,31 +390,6 @@ __device__ __forceinline__ void balance_rounds(uint32_t (&x)[M], uint32_t* buf, 
 
 // balance + convert_and_divide (partition.hpp:275-286) until subproblems have <= m
 // rows, then the leaves (balance_divide_sort steps (1) and (2), :373-396)
-// PartitionProbe (partition.hpp:298-301) capture: the full working window after every
-// balance (after_balance) and every convert-and-divide (after_divide) of the OUTER
-// recursion, in the order the reference calls its hooks.  Each lane stores its row of
-// the window; with PK = 2 each 16-bit half goes to its own instance's snapshot area.
-struct ProbeSink {
-    uint32_t* dst[2];  // per half: this instance's snapshot area (max x WM x M words) or null
-    uint32_t n, max;
-    int row, wm;
-    template <int PK, int M>
-    __device__ __forceinline__ void capture(const uint32_t (&x)[M]) {
-        if (n < max) {
-#pragma unroll
-            for (int h = 0; h < PK; ++h) {
-                if (dst[h] == nullptr)
-                    continue;
-                uint32_t* q = dst[h] + ((size_t)n * wm + row) * M;
-#pragma unroll
-                for (int c = 0; c < M; ++c)
-                    q[c] = PK == 2 ? ((x[c] >> (16 * h)) & 0xFFFFu) : x[c];
-            }
-        }
-        ++n;
-    }
-};
-
 template <int PK, class V, bool EXT, int M>
 __device__ __forceinline__ void levels(uint32_t (&x)[M], uint32_t* buf, int lane, ProbeSink* ps = nullptr) {
     if constexpr (V::WV > V::MV) {

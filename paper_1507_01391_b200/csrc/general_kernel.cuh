@@ -157,16 +157,16 @@ __global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_
 
     using V = VF<0xFFFFFFFFu, 0, 1, WM, 0, M, (kMulti ? WM : 32), (kMulti ? WM : 32)>;
     GenResult res{{0u, 0u}, 0u};
-    if constexpr (MODE == kModeSortAny)
-        sort_wide_any<PK, V>(x, buf, lane, ascending != 0);
-    else {
-        // PartitionProbe snapshots (one code path: the hook points test a uniform pointer):
-        // instance k's area is probe[k * probe_max * WM * M ...]
-        ProbeSink ps{{nullptr, nullptr}, 0u, probe_max, row, WM};
+    // probe snapshots (PartitionProbe / ShortWideHook points; one code path: the capture
+    // points test a uniform pointer): instance k's area is probe[k * probe_max * WM * M ...]
+    ProbeSink ps{{nullptr, nullptr}, 0u, probe_max, row, WM};
 #pragma unroll
-        for (int h = 0; h < PK; ++h)
-            if (probe != nullptr && inst_of(h) < count)
-                ps.dst[h] = probe + inst_of(h) * probe_max * WM * M;
+    for (int h = 0; h < PK; ++h)
+        if (probe != nullptr && inst_of(h) < count)
+            ps.dst[h] = probe + inst_of(h) * probe_max * WM * M;
+    if constexpr (MODE == kModeSortAny) {
+        sort_wide_any<PK, V>(x, buf, lane, ascending != 0, probe != nullptr ? &ps : nullptr);
+    } else {
         // partition labels are < w <= 32: the top key bit of every half is free for the fused
         // cleanup (cleanup_pass_pair); integer keys may use every bit
         // (multi-warp machines always run the fused cleanup: their integer sorts need a
@@ -181,7 +181,9 @@ __global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_
         res.template finish<WM>();
 
     uint32_t invalid = 0;
-    if constexpr (MODE == kModePartition) {
+    // partition entry points run as MODE kModePartition, or as the literal comparison skeleton
+    // (kModeSortAny with domain = w < 2^32: partition_short_wide with its hook points)
+    if (MODE == kModePartition || (MODE == kModeSortAny && domain < (1ull << 32))) {
         // check_partition_instance (partition.hpp:112-124): labels in [0, w), m copies
         // each  <=>  (labels < w) and the sorted result has row i = i everywhere.
         // OR of (key ^ row) over the row: one LOP3 per register, both halves at once
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_
         if (row == 0) {
             const bool unsorted = (res.unsorted >> h) & 1u;
             uint8_t s = DMM_OK;
-            if (MODE == kModePartition && ((invalid >> h) & 1u))
+            if ((invalid >> h) & 1u)
                 s = DMM_INVALID_INSTANCE;
             else if ((bad >> h) & 1u)
                 s = DMM_KEY_OUT_OF_RANGE;

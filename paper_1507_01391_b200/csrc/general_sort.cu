@@ -182,6 +182,23 @@ dmm_status dmm_partition_short_wide(const uint32_t* in, uint32_t* out, uint32_t 
                     static_cast<cudaStream_t>(stream));
 }
 
+// ShortWideHook capture (sort.hpp:189-218) for partition_short_wide / sort_short_wide: the
+// literal short-wide skeleton (its row sorts have unique outcomes, so every stage equals the
+// reference's, radix rows or merge rows alike), with the window written to
+// snapshots[k * 3 * w * m ...] at after_first_convert, after_first_pass and done.
+dmm_status dmm_short_wide_probe(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                                int partition, int ascending, uint8_t* status, uint32_t* snapshots, void* stream) {
+    reset_launches();
+    if (uint64_t(w) * w > m)
+        return DMM_SHAPE_VIOLATION;
+    if (dmm_status e = check_ptrs(in, out, count); e != DMM_OK || count == 0)
+        return e;
+    if (!snapshots)
+        return DMM_INVALID_ARGUMENT;
+    return dispatch(dmmdev::kModeSortAny, in, out, w, m, count, partition ? uint64_t(w) : (1ull << 32), false, 1,
+                    partition ? 1 : ascending, nullptr, status, static_cast<cudaStream_t>(stream), snapshots, 3);
+}
+
 // sort_square sort.hpp:337-346: w = m perfect square -> square_skeleton (Theorem 2),
 // run literally by the comparison-sort kernel (sort_wide_any dispatches on the shape)
 dmm_status dmm_sort_square(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,

@@ -337,6 +337,39 @@ static void run_algorithm_cases() {
         [&] { b200::run_algorithm(Algorithm::permute, gen_instance(InstanceKind::partition, 32, 16, 1)); }));
 }
 
+// ShortWideHook (sort.hpp:189-218): the same three calls with the same machine contents
+static void short_wide_hook_cases() {
+    for (auto [w, m] : {std::pair<u32, u32>{8, 64}, {4, 16}, {2, 8}}) {
+        for (int part = 0; part < 2; ++part) {
+            for (bool asc : {true, false}) {
+                if (part && !asc)
+                    continue;
+                Instance in = part ? gen_instance(InstanceKind::partition, w, m, 3)
+                                   : gen_instance(InstanceKind::sort, w, m, 3);
+                if (!part)
+                    for (auto& x : in.grid)
+                        x >>= 40;
+                Machine a = make_machine(w, m), b = make_machine(w, m);
+                MatrixView va = MatrixView::full(a), vb = MatrixView::full(b);
+                va.load(in.grid);
+                vb.load(in.grid);
+                std::vector<std::pair<int, std::vector<word>>> ea, eb;
+                ShortWideHook ha = [&](ShortWideStage st) { ea.push_back({int(st), va.snapshot()}); };
+                ShortWideHook hb = [&](ShortWideStage st) { eb.push_back({int(st), vb.snapshot()}); };
+                if (part) {
+                    partition_short_wide(va, ha);
+                    b200::partition_short_wide(vb, hb);
+                } else {
+                    sort_short_wide(va, asc, ha);
+                    b200::sort_short_wide(vb, asc, hb);
+                }
+                CHECK(ea.size() == 3 && ea == eb);
+                CHECK(va.snapshot() == vb.snapshot());
+            }
+        }
+    }
+}
+
 int main() {
     partition_cases();
     integer_sort_cases();
@@ -344,6 +377,7 @@ int main() {
     subwarp_cases();
     probe_cases();
     run_algorithm_cases();
+    short_wide_hook_cases();
     permute_cases();
     std::printf("shim parity: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;
