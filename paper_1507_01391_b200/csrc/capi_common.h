@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -23,6 +24,26 @@ inline dmm_status check_launch(const char* what) {
         return DMM_CUDA_ERROR;
     }
     count_launch();
+    return DMM_OK;
+}
+
+// Per-kernel launch attributes (dynamic shared memory above 48 KB, full carveout), set once
+// per device and kernel: `done` is the kernel's own static bitmask of configured devices
+// (atomic: concurrent host threads may race to configure; setting twice is harmless).
+template <class Kernel>
+inline dmm_status configure_kernel(Kernel kern, size_t smem, std::atomic<uint64_t>& done) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess)
+        return check_launch("cudaGetDevice");
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit)
+        return DMM_OK;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+        return check_launch("cudaFuncSetAttribute");
+    // prefer the full 228 KB shared-memory carveout: occupancy is bounded by smem + registers
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    done.fetch_or(bit, std::memory_order_release);
     return DMM_OK;
 }
 

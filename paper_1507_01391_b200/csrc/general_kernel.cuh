@@ -263,15 +263,9 @@ dmm_status launch_general(const GeneralArgs& a) {
     constexpr int kWarpsPerBlock = dmmdev::warps_per_block<M, PK, WM>();
     constexpr bool kMulti = WM > dmmdev::kWarp;
     const size_t smem = size_t(kMulti ? 1 : kWarpsPerBlock) * dmmdev::staging_words<M, WM>() * sizeof(uint32_t);
-    static bool configured = false;  // per instantiation
-    if (!configured) {
-        if (smem > 48 * 1024 &&
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
-            return check_launch("cudaFuncSetAttribute");
-        // prefer the full 228 KB shared-memory carveout: occupancy is bounded by smem + registers
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        configured = true;
-    }
+    static std::atomic<uint64_t> configured{0};  // devices configured, per instantiation
+    if (dmm_status e = configure_kernel(kern, smem, configured); e != DMM_OK)
+        return e;
     constexpr int kPerWarp = kMulti ? 1 : dmmdev::kWarp / WM;  // machines per warp
     const uint64_t units = (a.count + PK * kPerWarp - 1) / (PK * kPerWarp);  // warp-tasks / machines
     const uint64_t blocks = kMulti ? units : (units + kWarpsPerBlock - 1) / kWarpsPerBlock;

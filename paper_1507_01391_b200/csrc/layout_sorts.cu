@@ -64,15 +64,9 @@ dmm_status launch_layout(const uint32_t* in, uint32_t* out, uint64_t count, int 
     constexpr int kWarps = kMulti ? R / dmmdev::kWarp : 8;
     auto kern = dmmdev::k_layout<M, OP, R>;
     const size_t smem = size_t(kWarps) * dmmdev::relayout_buf_words(M) * sizeof(uint32_t);
-    static bool configured = false;
-    if (!configured) {
-        if (smem > 48 * 1024 &&
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
-            return check_launch("cudaFuncSetAttribute");
-        // prefer the full 228 KB shared-memory carveout: occupancy is bounded by smem + registers
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        configured = true;
-    }
+    static std::atomic<uint64_t> configured{0};  // devices configured, per instantiation
+    if (dmm_status e = configure_kernel(kern, smem, configured); e != DMM_OK)
+        return e;
     if (count == 0)
         return DMM_OK;
     const uint64_t blocks = kMulti ? count : (count + kWarps - 1) / kWarps;

@@ -652,15 +652,9 @@ dmm_status launch_permute(const uint32_t* in, uint32_t* out, uint64_t count, con
     constexpr int kMach = dmmdev::perm_machines_per_cta<R>();
     auto kern = dmmdev::k_permute<M, R>;
     const size_t smem = size_t(kMach) * dmmdev::perm_machine_words<M, R>() * sizeof(uint32_t);
-    static bool configured = false;
-    if (!configured) {
-        if (smem > 48 * 1024 &&
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
-            return check_launch("cudaFuncSetAttribute");
-        // prefer the full 228 KB shared-memory carveout: occupancy is bounded by smem + registers
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        configured = true;
-    }
+    static std::atomic<uint64_t> configured{0};  // devices configured, per instantiation
+    if (dmm_status e = configure_kernel(kern, smem, configured); e != DMM_OK)
+        return e;
     const uint64_t blocks = (count + kMach - 1) / kMach;
     kern<<<unsigned(blocks), kMach * R, smem, s>>>(in, out, count, seeds, states, a, reps, hist, shifts, status);
     return check_launch("k_permute");
