@@ -8,10 +8,10 @@
 //      row and sub-position j, log2(nbuckets) ballots give every bucket's lane mask and
 //      popc counts it;
 //   2. k_ms_scan_*: exclusive scan of the per-tile counts, bucket-major (two levels);
-//   3. k_ms_scatter: the warp re-reads its tile; a key's destination is
-//      offset[bucket][tile] + keys of its bucket in earlier rows + keys of its bucket held
-//      by lower lanes in this row + its own earlier keys of the same bucket, i.e. stable by
-//      source index.  A warp store writes at most nbuckets contiguous runs.
+//   3. k_ms_scatter: the warp re-reads its tile in rows of 32 consecutive keys (one per lane);
+//      a key's destination is offset[bucket][tile] + keys of its bucket in earlier rows + keys
+//      of its bucket in lower lanes of this row (a warp prefix scan of byte-packed counters),
+//      i.e. stable by source index, and a warp store writes at most nbuckets contiguous runs.
 // The cross-GPU exchange (bucket j -> rank owning j) is an NCCL all-to-all in
 // paper_1507_01391_b200/distributed.py.
 #include "capi_common.h"
@@ -210,51 +210,49 @@ __global__ void __launch_bounds__(256) k_ms_scatter(const uint32_t* __restrict__
     // lane b < NB holds the running output position of bucket b
     uint64_t pos = lane < NB ? offsets[(uint64_t)lane * ntiles + tile] : 0;
     const uint64_t base = tile * kMsTile;
-#pragma unroll 2
-    for (int r = 0; r < kMsRows; ++r) {
-        uint32_t k[4], valid, label[4];
-        load_row4(keys, n, base + (uint64_t)r * 128 + 4 * lane, k, valid);
-        Packed<NB> own;  // this lane's keys per bucket
-        own.clear();
+    // rows of 32 consecutive keys, one per lane (coalesced 128-byte loads, 4 rows in flight):
+    // the keys of one bucket in one row go to consecutive output words, so every warp store
+    // writes at most NB contiguous runs
+#pragma unroll 1
+    for (int r = 0; r < kMsRows * 4; r += 4) {
+        uint32_t k[4];
+        bool valid[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            label[j] = (k[j] >> shift) & (NB - 1);
-            if ((valid >> j) & 1u)
-                own.add(label[j]);
+            const uint64_t i = base + (uint64_t)(r + j) * 32 + lane;
+            valid[j] = i < n;
+            k[j] = valid[j] ? __ldg(keys + i) : 0u;
         }
-        // exclusive warp prefix of the packed counts: keys of each bucket in lower lanes
-        Packed<NB> lower;
 #pragma unroll
-        for (int h = 0; h < H; ++h) {
-            uint32_t x = own.p[h];
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t b = (k[j] >> shift) & (NB - 1);
+            Packed<NB> own;
+            own.clear();
+            if (valid[j])
+                own.add(b);
+            // exclusive warp prefix: keys of each bucket held by lower lanes in this row
+            uint32_t lower = 0, tot_mine = 0;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-                if (lane >= o)
-                    x += y;
+            for (int h = 0; h < H; ++h) {
+                uint32_t x = own.p[h];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+                    if (lane >= o)
+                        x += y;
+                }
+                const uint32_t excl = x - own.p[h];
+                if ((b >> 2) == (uint32_t)h)
+                    lower = (excl >> (8 * (b & 3))) & 0xFFu;
+                const uint32_t t = __shfl_sync(0xFFFFFFFFu, x, 31);  // row totals (inclusive, lane 31)
+                if ((lane >> 2) == h)
+                    tot_mine = (t >> (8 * (lane & 3))) & 0xFFu;
             }
-            lower.p[h] = x - own.p[h];
-        }
-        // row totals (inclusive prefix of lane 31) -> bucket b's lane advances pos after the row
-        uint32_t row_total = 0;
-#pragma unroll
-        for (int h = 0; h < H; ++h) {
-            const uint32_t t = __shfl_sync(0xFFFFFFFFu, lower.p[h] + own.p[h], 31);
-            if ((lane >> 2) == h)
-                row_total = (t >> (8 * (lane & 3))) & 0xFFu;
-        }
-        Packed<NB> seen;  // own earlier keys per bucket
-        seen.clear();
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t b = label[j];
             const uint64_t p0 = __shfl_sync(0xFFFFFFFFu, pos, (int)b);
-            if ((valid >> j) & 1u) {
-                out[p0 + lower.get(b) + seen.get(b)] = k[j];
-                seen.add(b);
-            }
+            if (valid[j])
+                out[p0 + lower] = k[j];
+            pos += tot_mine;
         }
-        pos += row_total;
     }
 }
 
