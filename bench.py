@@ -60,30 +60,64 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region, in-process through NVML
+    (every 10 ms; forking nvidia-smi from a process with a large CUDA address space stalls
+    the launching thread), falling back to nvidia-smi when NVML is unavailable."""
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, set of reason names)
         self._stop = threading.Event()
         self._t = None
 
+    def _run_nvml(self, nv):
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        while True:
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, mx, {k for k, b in bits.items() if r & b}))
+            except Exception:
+                pass
+            if self._stop.wait(0.01):
+                break
+
+    def _run_smi(self):
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+            "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                f = [x.strip() for x in out.split(",")]
+                if len(f) >= 6:
+                    self.samples.append((float(f[0]), float(f[1]),
+                                         {n for n, v in zip(self.NAMES, f[2:6]) if v.lower().startswith("active")}))
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
     def __enter__(self):
-        def run():
-            q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
-                "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
-                "clocks_event_reasons.sw_power_cap"
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
-        self._t = threading.Thread(target=run, daemon=True)
+        if os.environ.get("DMM_BENCH_NO_CLOCKS"):  # diagnostics only: no sampling thread
+            self.source = None
+            return self
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            target = lambda: self._run_nvml(nv)  # noqa: E731
+            self.source = "nvml"
+        except Exception:
+            target = self._run_smi
+            self.source = "nvidia-smi"
+        self._t = threading.Thread(target=target, daemon=True)
         self._t.start()
         return self
 
@@ -95,13 +129,10 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted(set().union(*(s[2] for s in self.samples))), "samples": len(self.samples),
+                "source": getattr(self, "source", None)}
 
 
 def cpu_baseline(cfg_name: str, seconds: float = 15.0):
@@ -202,6 +233,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--count", type=int, default=0, help="instances per GPU (default: the config's)")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="pipeline chunks of the end-to-end leg")
+    ap.add_argument("--no-graph", action="store_true", help="time the eager launch loop instead of graph replay")
     ap.add_argument("--e2e-streams", type=int, default=3, help="CUDA streams of the end-to-end leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -256,6 +288,26 @@ def main():
     torch.cuda.synchronize()
     launches_per_step = int(dmm.lib().dmm_last_launch_count())
 
+    # The step is one kernel launch; it is captured once into a CUDA graph and the timed loop
+    # replays it K times, so host-side stalls cannot starve the GPU between steps (measured:
+    # the eager loop's step time varied up to 2x run to run on a shared host).  cfg5's step
+    # has a host sync (bucket counts) and stays eager.
+    graph = None
+    if alg != "global_partition" and not args.no_graph:
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cap):
+            step(g, out)  # settle allocations on the capture stream
+        torch.cuda.current_stream().wait_stream(cap)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            _, st_graph = step(g, out)
+        torch.cuda.synchronize()
+        for _ in range(2):
+            graph.replay()
+        torch.cuda.synchronize()
+
     def barrier():
         if world > 1:
             dist.barrier()
@@ -267,9 +319,14 @@ def main():
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            _, st = step(g, out)
+            if graph is not None:
+                graph.replay()
+            else:
+                _, st = step(g, out)
         e1.record(stream)
         torch.cuda.synchronize()
+    if graph is not None:
+        st = st_graph
     ms = e0.elapsed_time(e1) / args.steps
     barrier()
     t = torch.tensor([ms], device="cuda")
@@ -348,6 +405,7 @@ def main():
             "vs_baseline": None, "dtype": "u32", "data": "synthetic (reference gen_instance, on device)",
             "config": {"workload": desc, "algorithm": alg, "w": w, "m": m, "instances_per_gpu": count,
                        "keys_per_gpu": keys_per_gpu, "l2": "inputs 2x L2 (no flush needed)",
+                       "timed_loop": "CUDA graph replay of the one-launch step" if graph is not None else "eager launches",
                        "parallelism": f"instances sharded over {world} GPU(s)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"],
