@@ -274,12 +274,51 @@ __device__ __forceinline__ void block_merge_levels(uint32_t (&x)[M], uint32_t* b
     }
 }
 
+// ascending stages js..0 over the 32 registers (pairs (p, p ^ 2^j)), js < 5 chosen at
+// runtime; each case is one straight-line sequence, so register renaming only has to be
+// undone once per sequence (a per-stage switch cost 16 moves per stage)
+template <int PK>
+__device__ __forceinline__ void stages_down(uint32_t (&x)[32], int js) {
+    switch (js) {
+        case 0: reg_stages<PK, 0, 32, 0, -1>(x); break;
+        case 1: reg_stages<PK, 0, 32, 1, -1>(x); break;
+        case 2: reg_stages<PK, 0, 32, 2, -1>(x); break;
+        case 3: reg_stages<PK, 0, 32, 3, -1>(x); break;
+        default: reg_stages<PK, 0, 32, 4, -1>(x); break;
+    }
+}
+
+// The 32 x 32 block sort with levels 6..10 as passes of one runtime loop over shared
+// stage bodies (the tile sort's structure): flip the rows whose direction bit (local row bit
+// level - 5) is set, transpose / row-bit stages / transpose / register stages, all ascending.
+// About half the SASS of the unrolled network; used on multi-warp machines, whose kernels
+// (the 128-row permutation's finish) otherwise stall on instruction fetch.
+template <int PK, class V>
+__device__ __forceinline__ void sort_block_compact(uint32_t (&x)[32], uint32_t* buf, int lane) {
+    block_merge_levels<PK, V, 1, 5>(x, buf, lane);  // register-local levels
+    uint32_t fcur = 0;
+#pragma unroll 1
+    for (int level = 6; level <= 10; ++level) {
+        const uint32_t f = (level < 10 && ((V::local(lane) >> (level - 5)) & 1)) ? 0xFFFFFFFFu : 0u;
+        flip<0, 32>(x, f ^ fcur);
+        fcur = f;
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+            transpose_blocks<V>(x, buf, lane);
+            stages_down<PK>(x, half == 0 ? level - 6 : 4);
+        }
+    }
+    flip<0, 32>(x, fcur);
+}
+
 // sort each view's WV x MV block ascending in row-major order (WV, MV powers of two, WV | MV)
 template <int PK, class V, int M>
 __device__ __forceinline__ void sort_block(uint32_t (&x)[M], uint32_t* buf, int lane) {
     static_assert(V::MV % V::WV == 0, "block sort needs WV | MV");
     if constexpr (V::WV == 1) {
         row_sort<PK, V>(x, lane, true);
+    } else if constexpr (V::ROWS > kWarp && V::WV == 32 && V::MV == 32 && V::C0 == 0 && M == 32) {
+        sort_block_compact<PK, V>(x, buf, lane);
     } else {
         block_merge_levels<PK, V, 1>(x, buf, lane);
     }

@@ -47,20 +47,6 @@ __device__ __forceinline__ void cross_warp_stage(uint32_t (&x)[32], uint32_t* sl
     __syncthreads();
 }
 
-// ascending stages js..0 over the 32 registers (pairs (p, p ^ 2^j)), js < 5 chosen at
-// runtime; each case is one straight-line sequence, so register renaming only has to be
-// undone once per sequence (a per-stage switch cost 16 moves per stage)
-template <int PK>
-__device__ __forceinline__ void stages_down(uint32_t (&x)[32], int js) {
-    switch (js) {
-        case 0: reg_stages<PK, 0, 32, 0, -1>(x); break;
-        case 1: reg_stages<PK, 0, 32, 1, -1>(x); break;
-        case 2: reg_stages<PK, 0, 32, 2, -1>(x); break;
-        case 3: reg_stages<PK, 0, 32, 3, -1>(x); break;
-        default: reg_stages<PK, 0, 32, 4, -1>(x); break;
-    }
-}
-
 template <int PK, int MODE>
 __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* __restrict__ in,
                                                                uint32_t* __restrict__ out, uint64_t count,
