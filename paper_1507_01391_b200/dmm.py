@@ -170,11 +170,15 @@ def _raise_first(status: torch.Tensor, where: str) -> None:
 class GeneralStats:
     """GeneralStats partition.hpp:292-295, per instance."""
     cleanup_retries: torch.Tensor  # int32 [count]
-    sorted: torch.Tensor           # bool  [count]
+    sorted_raw: torch.Tensor       # int32 [count] (0 / 1 as written by the kernel)
     status: torch.Tensor           # uint8 [count] (dmm_status)
     # PartitionProbe capture (probe=True): [count, snaps, w, m] windows after every
     # after_balance / after_divide hook of the outer recursion, in hook order
     snapshots: torch.Tensor | None = None
+
+    @property
+    def sorted(self) -> torch.Tensor:  # bool [count]; computed on access (no extra kernel per call)
+        return self.sorted_raw != 0
 
 
 # --------------------------------------------------------------------------------------
@@ -227,7 +231,7 @@ def _general(fn_name: str, grid, domain: int | None, flags: int, out, stream, ch
             st = L.dmm_integer_sort_general(t.data_ptr(), res.data_ptr(), w, m, count, domain, flags,
                                             stats.data_ptr(), status.data_ptr(), _stream(stream))
     _check(st, fn_name)
-    gs = GeneralStats(stats[:, 0], stats[:, 1] != 0, status, snaps[0] if (single and snaps is not None) else snaps)
+    gs = GeneralStats(stats[:, 0], stats[:, 1], status, snaps[0] if (single and snaps is not None) else snaps)
     if check:
         _raise_first(status, fn_name)
     return (res[0] if single else res), gs
