@@ -295,7 +295,7 @@ __device__ __forceinline__ void stages_down(uint32_t (&x)[32], int js) {
 // (the 128-row permutation's finish) otherwise stall on instruction fetch.
 template <int PK, class V>
 __device__ __forceinline__ void sort_block_compact(uint32_t (&x)[32], uint32_t* buf, int lane) {
-    block_merge_levels<PK, V, 1, 5>(x, buf, lane);  // register-local levels
+    row_sort<PK, V>(x, lane, (V::local(lane) & 1) == 0);  // register-local levels 1..5 (odd-even merge sort)
     uint32_t fcur = 0;
 #pragma unroll 1
     for (int level = 6; level <= 10; ++level) {
@@ -320,7 +320,11 @@ __device__ __forceinline__ void sort_block(uint32_t (&x)[M], uint32_t* buf, int 
     } else if constexpr (V::ROWS > kWarp && V::WV == 32 && V::MV == 32 && V::C0 == 0 && M == 32) {
         sort_block_compact<PK, V>(x, buf, lane);
     } else {
-        block_merge_levels<PK, V, 1>(x, buf, lane);
+        // levels 1..log2(MV) stay inside each row; their outcome is the row sorted in the
+        // direction of its local-row bit 0, which Batcher's odd-even merge sort reaches with
+        // fewer comparators than the bitonic stages (32 keys: 191 vs 240)
+        row_sort<PK, V>(x, lane, (V::local(lane) & 1) == 0);
+        block_merge_levels<PK, V, ilog2_ceil_c(V::MV) + 1>(x, buf, lane);
     }
 }
 

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
 
     using V = VF<0xFFFFFFFFu, 0, 1, kWarp, 0, 32>;
     // levels 1..5: register-local, static
-    block_merge_levels<PK, V, 1, 5>(x, buf, lane);
+    row_sort<PK, V>(x, lane, (lane & 1) == 0);  // levels 1..5 (odd-even merge sort per row)
     // levels 6..12 as passes of one loop (see the header); the flip that ends a pass and
     // the one that starts the next are merged into one
     auto dir_mask = [&](int level) -> uint32_t {
