@@ -341,9 +341,18 @@ def main():
         exp = torch.arange(w * m, device="cuda", dtype=torch.int32).view(1, w, m)
         ok = bool((out == exp).all())
     elif alg == "global_partition":
+        # this rank received exactly the keys whose label it owns (8 labels over `world` ranks),
+        # and the total over ranks is every key (counts all-reduced)
         res, _ = step(g, out)
         lab = (res.to(torch.int64) & 0xFFFFFFFF) >> 29
-        ok = bool((lab[1:] >= lab[:-1]).all()) and res.numel() == keys_per_gpu
+        lo, hi = rank * 8 // world, (rank + 1) * 8 // world
+        ok = bool(((lab >= lo) & (lab < hi)).all())
+        if world == 1:
+            ok = ok and bool((lab[1:] >= lab[:-1]).all())
+        n_recv = torch.tensor([res.numel()], device="cuda", dtype=torch.int64)
+        if world > 1:
+            dist.all_reduce(n_recv)
+        ok = ok and int(n_recv.item()) == keys_per_gpu * world
     else:
         ok = bool((out.view(count, -1)[:, 1:].to(torch.int64) & 0xFFFFFFFF >=
                    out.view(count, -1)[:, :-1].to(torch.int64) & 0xFFFFFFFF).all())
