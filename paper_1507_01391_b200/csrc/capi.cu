@@ -38,6 +38,7 @@ int dmm_supported(const char* algorithm, uint32_t w, uint32_t m) {
             case 8: return m == 8 || m == 16 || m == 32 || m == 64;
             case 4: return m == 4 || m == 8 || m == 16;
             case 2: return m == 2 || m == 4 || m == 8;
+            case 3: return m == 9;
             default: return false;
         }
     };

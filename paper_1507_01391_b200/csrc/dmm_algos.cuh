@@ -335,7 +335,11 @@ __device__ __forceinline__ void sort_block(uint32_t (&x)[M], uint32_t* buf, int 
 // for the reference's comparison-sort entry points (dmm_sort_wide_any, sort_tall).
 template <int PK, class V, int M>
 __device__ __forceinline__ void partition_leaf(uint32_t (&x)[M], uint32_t* buf, int lane) {
-    sort_block<PK, V>(x, buf, lane);
+    constexpr bool pow2 = (V::WV & (V::WV - 1)) == 0 && (V::MV & (V::MV - 1)) == 0;
+    if constexpr (pow2)
+        sort_block<PK, V>(x, buf, lane);
+    else  // shapes that are not powers of two: the reference's own leaf dispatch, literally
+        sort_wide_any<PK, V>(x, buf, lane, true);
 }
 
 // sort_columns_network sort.hpp:115-156: every column sorted ascending across the

@@ -43,11 +43,20 @@ __device__ __forceinline__ void static_for(F&& f) {
     }
 }
 
-// Reductions over aligned groups of WM lanes (one machine each; WM = 32: the warp).
+// Reductions over aligned groups of WM lanes (one machine each; WM = 32: the warp).  WM that
+// is not a power of two (e.g. 3-row machines, 10 per warp) reduces over the group's lane mask.
+__device__ __forceinline__ uint32_t group_lane_mask(int wm) {
+    const int lane = threadIdx.x & 31;
+    const int g0 = (lane / wm) * wm;
+    const int n = g0 + wm > 32 ? 32 - g0 : wm;
+    return (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u)) << g0;
+}
 template <int WM>
 __device__ __forceinline__ uint32_t seg_or(uint32_t v) {
     if constexpr (WM >= kWarp) {
         return __reduce_or_sync(0xFFFFFFFFu, v);
+    } else if constexpr ((WM & (WM - 1)) != 0) {
+        return __reduce_or_sync(group_lane_mask(WM), v);
     } else {
 #pragma unroll
         for (int off = 1; off < WM; off <<= 1)
@@ -59,6 +68,8 @@ template <int WM>
 __device__ __forceinline__ uint32_t seg_max(uint32_t v) {
     if constexpr (WM >= kWarp) {
         return __reduce_max_sync(0xFFFFFFFFu, v);
+    } else if constexpr ((WM & (WM - 1)) != 0) {
+        return __reduce_max_sync(group_lane_mask(WM), v);
     } else {
 #pragma unroll
         for (int off = 1; off < WM; off <<= 1)
@@ -146,40 +157,48 @@ struct Key<2> {  // two 16-bit keys per register (instance A low half, B high ha
 // compile-time constant (no local memory).  N = 8/16/32/64: 19/63/191/543
 // comparators, each one VIMNMX pair (min + max).
 // ---------------------------------------------------------------------------
-template <int PK, int LO, int HI, int R, int M>
+// LIM: registers [LIM, HI] are virtual +inf padding (sizes that are not powers of two):
+// a comparator touching one never swaps, so it is dropped and the padding never moves.
+template <int PK, int LO, int HI, int R, int LIM, int M>
 __device__ __forceinline__ void oe_merge(uint32_t (&x)[M]) {
     constexpr int step = R * 2;
     if constexpr (step < HI - LO) {
-        oe_merge<PK, LO, HI, step>(x);
-        oe_merge<PK, LO + R, HI, step>(x);
+        oe_merge<PK, LO, HI, step, LIM>(x);
+        oe_merge<PK, LO + R, HI, step, LIM>(x);
         static_for<LO + R, HI - R, step>([&](auto i) {
-            Key<PK>::template cx<(decltype(i)::value - LO) / step>(x[decltype(i)::value], x[decltype(i)::value + R]);
+            constexpr int a = decltype(i)::value;
+            if constexpr (a + R < LIM)
+                Key<PK>::template cx<(a - LO) / step>(x[a], x[a + R]);
         });
-    } else {
+    } else if constexpr (LO + R < LIM) {
         Key<PK>::template cx<LO>(x[LO], x[LO + R]);
     }
 }
 
-template <int PK, int LO, int HI, int M>
+template <int PK, int LO, int HI, int LIM, int M>
 __device__ __forceinline__ void oe_sort(uint32_t (&x)[M]) {
-    if constexpr (HI - LO >= 1) {
+    if constexpr (HI - LO >= 1 && LO + 1 < LIM) {
         constexpr int mid = LO + (HI - LO) / 2;
-        oe_sort<PK, LO, mid>(x);
-        oe_sort<PK, mid + 1, HI>(x);
-        oe_merge<PK, LO, HI, 1>(x);
+        oe_sort<PK, LO, mid, LIM>(x);
+        oe_sort<PK, mid + 1, HI, LIM>(x);
+        oe_merge<PK, LO, HI, 1, LIM>(x);
     }
 }
 
-// ascending sort of x[OFF .. OFF+N)
+// ascending sort of x[OFF .. OFF+N): Batcher's odd-even merge sort on the next power of two,
+// comparators that touch the (virtual) padding dropped
+__host__ __device__ constexpr int next_pow2_c(int n) {
+    int p = 1;
+    while (p < n)
+        p <<= 1;
+    return p;
+}
 template <int PK, int OFF, int N, int M>
 __device__ __forceinline__ void sort_net(uint32_t (&x)[M]) {
     static_assert(OFF + N <= M, "window outside the register row");
-    static_assert((N & (N - 1)) == 0, "network size must be a power of two");
-    oe_sort<PK, OFF, OFF + N - 1>(x);
+    oe_sort<PK, OFF, OFF + next_pow2_c(N) - 1, OFF + N>(x);
 }
 
-// x ^= f for f in {0, ~0}, computed as x * (f | 1) + f (= x, or -x - 1 = ~x) on the
-// FMA pipe: the ALU pipe is the sorting networks' bottleneck
 template <int OFF, int N, int M>
 __device__ __forceinline__ void flip(uint32_t (&x)[M], uint32_t f) {
     const uint32_t s = f | 1u;

@@ -66,13 +66,15 @@ __global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_
     k_general_sort(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count, uint64_t domain,
                    int strict, int ascending, dmm_general_stats* __restrict__ stats, uint8_t* __restrict__ status,
                    uint32_t* __restrict__ probe, uint32_t probe_max) {
-    static_assert(WM >= 1 && (kWarp % WM == 0 || WM % kWarp == 0), "machines must tile the warp or the CTA");
+    static_assert(WM >= 1 && (WM < kWarp || WM % kWarp == 0), "machines tile the warp or the CTA");
     constexpr bool kMulti = WM > kWarp;
-    constexpr int G = kMulti ? 1 : kWarp / WM;
+    constexpr int G = kMulti ? 1 : kWarp / WM;  // machines per warp (lanes >= G * WM idle)
+    constexpr uint32_t kMask = (kMulti || G * WM == kWarp) ? 0xFFFFFFFFu : ((1u << (G * WM)) - 1u);
     extern __shared__ uint32_t smem[];
     const int lane = kMulti ? (int)threadIdx.x : (int)(threadIdx.x & 31);  // the machine row index space
     const int warp = kMulti ? 0 : (int)(threadIdx.x >> 5);
     const int grp = kMulti ? 0 : lane / WM, row = kMulti ? lane : lane % WM;
+    const bool live_lane = ((kMask >> (lane & 31)) & 1u) != 0;
     uint32_t* buf = smem + warp * staging_words<M, WM>();
     const uint64_t first = kMulti ? (uint64_t)blockIdx.x * PK
                                   : ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * (PK * G);  // half 0, group 0
@@ -89,7 +91,7 @@ __global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_
     constexpr bool kAnyLayout = MODE != kModeSortAny && WM <= M && M % 4 == 0;
     auto load = [&](int h, uint32_t (&v)[M]) {
         const uint64_t k = inst_of(h);
-        if (k >= count) {
+        if (k >= count || !live_lane) {
 #pragma unroll
             for (int c = 0; c < M; ++c)
                 v[c] = 0;
@@ -155,14 +157,14 @@ __global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_
     };
     bad = machine_or(bad);
 
-    using V = VF<0xFFFFFFFFu, 0, 1, WM, 0, M, (kMulti ? WM : 32), (kMulti ? WM : 32)>;
+    using V = VF<kMask, 0, 1, WM, 0, M, (kMulti ? WM : 32), (kMulti ? WM : 32)>;
     GenResult res{{0u, 0u}, 0u};
     // probe snapshots (PartitionProbe / ShortWideHook points; one code path: the capture
     // points test a uniform pointer): instance k's area is probe[k * probe_max * WM * M ...]
     ProbeSink ps{{nullptr, nullptr}, 0u, probe_max, row, WM};
 #pragma unroll
     for (int h = 0; h < PK; ++h)
-        if (probe != nullptr && inst_of(h) < count)
+        if (probe != nullptr && inst_of(h) < count && live_lane)
             ps.dst[h] = probe + inst_of(h) * probe_max * WM * M;
     if constexpr (MODE == kModeSortAny) {
         sort_wide_any<PK, V>(x, buf, lane, ascending != 0, probe != nullptr ? &ps : nullptr);
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_
 #pragma unroll
     for (int h = 0; h < PK; ++h) {
         const uint64_t k = inst_of(h);
-        if (k >= count)
+        if (k >= count || !live_lane)
             continue;
         if constexpr (M % 4 == 0) {
             // unpack one 16-byte vector at a time (register budget)
@@ -295,5 +297,6 @@ dmm_status launch_general_w16(uint32_t m, int mode, bool pk2, bool ext, const Ge
 dmm_status launch_general_w8(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_w4(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_w2(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);
+dmm_status launch_general_w3(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);
 
 }  // namespace dmmhost

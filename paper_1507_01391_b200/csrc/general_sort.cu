@@ -36,9 +36,10 @@ dmm_status dispatch(int mode, const uint32_t* in, uint32_t* out, uint32_t w, uin
         case 8: return launch_general_w8(m, mode, pk2, ext, a);
         case 4: return launch_general_w4(m, mode, pk2, ext, a);
         case 2: return launch_general_w2(m, mode, pk2, ext, a);
+        case 3: return launch_general_w3(m, mode, pk2, ext, a);
         default: break;
     }
-    set_error("no kernel compiled for this shape (w in {2, 4, 8, 16, 32, 64, 128, 256})");
+    set_error("no kernel compiled for this shape (w in {2, 3, 4, 8, 16, 32, 64, 128, 256})");
     return DMM_UNSUPPORTED_SHAPE;
 }
 

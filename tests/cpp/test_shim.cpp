@@ -194,7 +194,7 @@ static void permute_cases() {
 // sub-warp machines (w < 32): the square / short-wide entry points exist only there
 static void subwarp_cases() {
     // partition_square / partition_short_wide (partition.hpp:178-197); 64 x 64 is a two-warp machine
-    for (auto [w, m] : {std::pair<u32, u32>{16, 16}, {4, 4}, {64, 64}, {8, 64}, {4, 16}, {2, 4}}) {
+    for (auto [w, m] : {std::pair<u32, u32>{16, 16}, {4, 4}, {64, 64}, {8, 64}, {4, 16}, {2, 4}, {3, 9}}) {
         for (u64 seed = 1; seed <= 3; ++seed) {
             Instance in = gen_instance(InstanceKind::partition, w, m, seed);
             Machine a = make_machine(w, m), b = make_machine(w, m);
@@ -306,7 +306,8 @@ static void run_algorithm_cases() {
     };
     const Case cases[] = {{Algorithm::partition_general, 32, 16}, {Algorithm::partition_general, 64, 16},
                           {Algorithm::integer_sort_general, 32, 32}, {Algorithm::partition_square, 16, 16},
-                          {Algorithm::partition_short_wide, 8, 64}, {Algorithm::sort_square, 16, 16},
+                          {Algorithm::partition_short_wide, 8, 64}, {Algorithm::partition_short_wide, 3, 9},
+                          {Algorithm::sort_square, 16, 16},
                           {Algorithm::sort_short_wide, 4, 16}, {Algorithm::sort_tall, 128, 32},
                           {Algorithm::permute, 32, 32}, {Algorithm::permute, 128, 64}};
     for (const Case& c : cases) {
@@ -339,7 +340,7 @@ static void run_algorithm_cases() {
 
 // ShortWideHook (sort.hpp:189-218): the same three calls with the same machine contents
 static void short_wide_hook_cases() {
-    for (auto [w, m] : {std::pair<u32, u32>{8, 64}, {4, 16}, {2, 8}}) {
+    for (auto [w, m] : {std::pair<u32, u32>{8, 64}, {4, 16}, {2, 8}, {3, 9}}) {
         for (int part = 0; part < 2; ++part) {
             for (bool asc : {true, false}) {
                 if (part && !asc)

@@ -107,3 +107,34 @@ def test_subwarp_errors(port):
         dmm.partition_short_wide(_batch(port, 1, 8, 32, [1]))
     with pytest.raises(dmm.ShapeViolation):  # m not a perfect square (sort.hpp:340-342)
         dmm.sort_square(np.zeros((1, 8, 8), dtype=np.uint32))
+
+
+def test_odd_machine_3x9(port, golden):
+    # 3-row machines (10 per warp, 2 idle lanes) at the reference's own odd test shape 3 x 9:
+    # the leaf runs the reference's short-wide dispatch with padded Batcher row networks
+    seeds = list(range(1, 24))  # two warps' worth and a ragged third
+    grids = _batch(port, 1, 3, 9, seeds)
+    out, st = dmm.partition_general(grids)
+    out = dmm.as_uint32(out)
+    for k in range(len(seeds)):
+        s, exp, rep = port.partition_general(grids[k])
+        assert s == 0 and (out[k] == exp).all() and int(st.cleanup_retries[k]) == rep["cleanup_retries"]
+    rng = np.random.default_rng(39)
+    keys = rng.integers(0, 1 << 20, size=(13, 3, 9), dtype=np.uint64).astype(np.uint32)
+    out, _ = dmm.integer_sort_general(keys, 1 << 20)
+    for k in range(13):
+        s, exp, _ = port.integer_sort_general(keys[k], 1 << 20)
+        assert s == 0 and (dmm.as_uint32(out)[k] == exp).all()
+    out = dmm.as_uint32(dmm.partition_short_wide(grids))
+    for k in range(len(seeds)):
+        s, exp = port.simple("partition_short_wide", grids[k])
+        assert s == 0 and (out[k] == exp).all()
+    for asc in (True, False):
+        out = dmm.as_uint32(dmm.sort_short_wide(keys, ascending=asc))
+        for k in range(13):
+            s, exp = port.simple("sort_short_wide", keys[k], int(asc))
+            assert s == 0 and (out[k] == exp).all()
+    meta, arr = golden
+    case = [c for c in meta["partition"] if (c["w"], c["m"]) == (3, 9)][0]
+    out, st = dmm.partition_general(arr[case["key"] + "_in"])
+    assert (dmm.as_uint32(out) == arr[case["key"] + "_out"]).all()
