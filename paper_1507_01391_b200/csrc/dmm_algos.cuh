@@ -16,6 +16,10 @@
 
 #include "dmm_device.cuh"
 
+#ifndef DMM_COMPACT_WARP_BLOCKS
+#define DMM_COMPACT_WARP_BLOCKS 1  // one-warp 32 x 32 block sorts use the looped form too (+3 % cfg1)
+#endif
+
 namespace dmmdev {
 
 // ---------------------------------------------------------------------------
@@ -317,7 +321,7 @@ __device__ __forceinline__ void sort_block(uint32_t (&x)[M], uint32_t* buf, int 
     static_assert(V::MV % V::WV == 0, "block sort needs WV | MV");
     if constexpr (V::WV == 1) {
         row_sort<PK, V>(x, lane, true);
-    } else if constexpr (V::ROWS > kWarp && V::WV == 32 && V::MV == 32 && V::C0 == 0 && M == 32) {
+    } else if constexpr ((V::ROWS > kWarp || DMM_COMPACT_WARP_BLOCKS) && V::WV == 32 && V::MV == 32 && V::C0 == 0 && M == 32) {
         sort_block_compact<PK, V>(x, buf, lane);
     } else {
         // levels 1..log2(MV) stay inside each row; their outcome is the row sorted in the
