@@ -278,41 +278,57 @@ __device__ __forceinline__ void block_merge_levels(uint32_t (&x)[M], uint32_t* b
     }
 }
 
-// ascending stages js..0 over the 32 registers (pairs (p, p ^ 2^j)), js < 5 chosen at
-// runtime; each case is one straight-line sequence, so register renaming only has to be
-// undone once per sequence (a per-stage switch cost 16 moves per stage)
-template <int PK>
-__device__ __forceinline__ void stages_down(uint32_t (&x)[32], int js) {
+// ascending stages js..0 over registers [C0, C0 + N) (pairs (p, p ^ 2^j)), js < log2(N)
+// chosen at runtime; each case is one straight-line sequence, so register renaming only has
+// to be undone once per sequence (a per-stage switch cost N / 2 moves per stage)
+template <int PK, int C0 = 0, int N = 32, int M>
+__device__ __forceinline__ void stages_down(uint32_t (&x)[M], int js) {
+    static_assert(N == 8 || N == 16 || N == 32 || N == 64, "stage sequences for 8..64 registers");
     switch (js) {
-        case 0: reg_stages<PK, 0, 32, 0, -1>(x); break;
-        case 1: reg_stages<PK, 0, 32, 1, -1>(x); break;
-        case 2: reg_stages<PK, 0, 32, 2, -1>(x); break;
-        case 3: reg_stages<PK, 0, 32, 3, -1>(x); break;
-        default: reg_stages<PK, 0, 32, 4, -1>(x); break;
+        case 0: reg_stages<PK, C0, N, 0, -1>(x); break;
+        case 1: reg_stages<PK, C0, N, 1, -1>(x); break;
+        case 2: reg_stages<PK, C0, N, 2, -1>(x); break;
+        default:
+            if constexpr (N >= 16) {
+                if (js == 3) {
+                    reg_stages<PK, C0, N, 3, -1>(x);
+                    break;
+                }
+            }
+            if constexpr (N >= 32) {
+                if (js == 4) {
+                    reg_stages<PK, C0, N, 4, -1>(x);
+                    break;
+                }
+            }
+            if constexpr (N >= 64)
+                reg_stages<PK, C0, N, 5, -1>(x);
+            break;
     }
 }
 
-// The 32 x 32 block sort with levels 6..10 as passes of one runtime loop over shared
-// stage bodies (the tile sort's structure): flip the rows whose direction bit (local row bit
-// level - 5) is set, transpose / row-bit stages / transpose / register stages, all ascending.
-// About half the SASS of the unrolled network; used on multi-warp machines, whose kernels
-// (the 128-row permutation's finish) otherwise stall on instruction fetch.
-template <int PK, class V>
-__device__ __forceinline__ void sort_block_compact(uint32_t (&x)[32], uint32_t* buf, int lane) {
-    row_sort<PK, V>(x, lane, (V::local(lane) & 1) == 0);  // register-local levels 1..5 (odd-even merge sort)
+// The square (WV = MV = 2^L) block sort with levels L+1 .. 2L as passes of one runtime loop over
+// shared stage bodies (the tile sort's structure): flip the rows whose direction bit (local row
+// bit level - L) is set, transpose / row-bit stages / transpose / register stages, all
+// ascending.  About half the SASS of the unrolled network; kernels full of leaf sorts (the
+// permutation's finish) otherwise stall on instruction fetch (ncu: no_inst 20 %).
+template <int PK, class V, int M>
+__device__ __forceinline__ void sort_block_compact(uint32_t (&x)[M], uint32_t* buf, int lane) {
+    constexpr int L = ilog2_ceil_c(V::MV);
+    row_sort<PK, V>(x, lane, (V::local(lane) & 1) == 0);  // register-local levels 1..L (odd-even merge sort)
     uint32_t fcur = 0;
 #pragma unroll 1
-    for (int level = 6; level <= 10; ++level) {
-        const uint32_t f = (level < 10 && ((V::local(lane) >> (level - 5)) & 1)) ? 0xFFFFFFFFu : 0u;
-        flip<0, 32>(x, f ^ fcur);
+    for (int level = L + 1; level <= 2 * L; ++level) {
+        const uint32_t f = (level < 2 * L && ((V::local(lane) >> (level - L)) & 1)) ? 0xFFFFFFFFu : 0u;
+        flip<V::C0, V::MV>(x, f ^ fcur);
         fcur = f;
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
             transpose_blocks<V>(x, buf, lane);
-            stages_down<PK>(x, half == 0 ? level - 6 : 4);
+            stages_down<PK, V::C0, V::MV>(x, half == 0 ? level - L - 1 : L - 1);
         }
     }
-    flip<0, 32>(x, fcur);
+    flip<V::C0, V::MV>(x, fcur);
 }
 
 // sort each view's WV x MV block ascending in row-major order (WV, MV powers of two, WV | MV)
@@ -321,7 +337,8 @@ __device__ __forceinline__ void sort_block(uint32_t (&x)[M], uint32_t* buf, int 
     static_assert(V::MV % V::WV == 0, "block sort needs WV | MV");
     if constexpr (V::WV == 1) {
         row_sort<PK, V>(x, lane, true);
-    } else if constexpr ((V::ROWS > kWarp || DMM_COMPACT_WARP_BLOCKS) && V::WV == 32 && V::MV == 32 && V::C0 == 0 && M == 32) {
+    } else if constexpr ((V::ROWS > kWarp || DMM_COMPACT_WARP_BLOCKS) && V::WV == 32 && V::MV == 32) {
+        // (16 x 16 blocks measured slower looped: cfg2b 152 -> 140 G keys/s)
         sort_block_compact<PK, V>(x, buf, lane);
     } else {
         // levels 1..log2(MV) stay inside each row; their outcome is the row sorted in the

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
             transpose_blocks<V>(x, buf, lane);
-            stages_down<PK>(x, half == 0 ? row_stages : 4);
+            stages_down<PK, 0, 32>(x, half == 0 ? row_stages : 4);
         }
     }
     flip<0, 32>(x, fcur);
