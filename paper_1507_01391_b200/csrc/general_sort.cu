@@ -1,18 +1,21 @@
 // general_sort.cu -- C ABI of kernels 1-3: w-way partition (n >= w^2), general
-// partition (Lemma 4) and integer sort over a batch of 32 x m machines.
+// partition (Lemma 4), integer sort and the comparison skeletons over a batch of w x m
+// machines (w = 32: one warp each; w in {2, 3, 4, 8, 16}: several per warp; w in {64, 128,
+// 256}: one per CTA).
 //
 // C ABI: dmm_partition_general (partition.hpp:453), dmm_integer_sort_general
 // (partition.hpp:436), dmm_sort_wide_any (sort.hpp:321), dmm_partition_square
-// (partition.hpp:189), dmm_partition_short_wide (partition.hpp:178).  The kernel
-// template is general_kernel.cuh; one translation unit per row width m.
+// (partition.hpp:189), dmm_partition_short_wide (partition.hpp:178), dmm_sort_square
+// (sort.hpp:337), dmm_sort_short_wide (sort.hpp:225), the probe entry points.  The kernel
+// template is general_kernel.cuh; one translation unit per machine width / row width.
 #include "general_kernel.cuh"
 
 namespace {
 
 using namespace dmmhost;
 
-// Dispatch over the compiled shapes (W = 32).  PK = 2 whenever every legal key
-// fits in 16 bits (domain <= 2^16).
+// Dispatch over the compiled (w, m) shapes.  PK = 2 whenever every legal key fits in 16
+// bits (domain <= 2^16).
 dmm_status dispatch(int mode, const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
                     uint64_t domain, bool ext, int strict, int ascending, dmm_general_stats* stats, uint8_t* status,
                     cudaStream_t s, uint32_t* probe = nullptr, uint32_t probe_max = 0) {
