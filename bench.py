@@ -72,8 +72,18 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _handle(self, nv):
+        # the NVML device of this process's CUDA device (CUDA_VISIBLE_DEVICES may renumber it)
+        try:
+            import torch
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.index)
+
     def _run_nvml(self, nv):
-        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        h = self._handle(nv)
         bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
                 "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
                 "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
