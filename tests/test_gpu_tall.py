@@ -108,3 +108,33 @@ def test_sort_tall_multiwarp(port, w, m):
     for k in range(3):
         st, exp = port.simple("sort_tall", g[k])
         assert st == 0 and (out[k] == exp).all(), (w, m, k)
+
+
+@pytest.mark.parametrize("w,m,count", [(64, 16, 4096), (128, 32, 2048), (256, 16, 1024)])
+def test_tall_partition_at_scale(port, w, m, count):
+    # many CTAs at once (barrier-heavy multi-warp machines): every instance ends row i = i with
+    # GeneralStats equal to the oracle's on a sample of instances
+    g = dmm.gen_instances(dmm.KIND_PARTITION, w, m, 77, count)
+    out, st = dmm.partition_general(g, flags=dmm.FLAG_NO_ENFORCE_PRE)
+    rows = torch.arange(w, device="cuda", dtype=torch.int32).view(1, w, 1)
+    assert bool((out == rows).all()) and int((st.status != 0).sum()) == 0
+    host = dmm.as_uint32(g)
+    retries = st.cleanup_retries.cpu().numpy()
+    for k in range(0, count, count // 8):
+        s, _, rep = port.partition_general(host[k], FLAG_NO_ENFORCE_PRE)
+        assert s == 0 and retries[k] == rep["cleanup_retries"]
+
+
+def test_tall_permute_at_scale(port):
+    count = 512
+    g = dmm.gen_instances(dmm.KIND_PERMUTE, 128, 64, 500, count)
+    seeds = np.arange(500, 500 + count, dtype=np.uint64)
+    out, reps = dmm.permute(g, seeds)
+    exp = torch.arange(128 * 64, device="cuda", dtype=torch.int32).view(1, 128, 64)
+    assert bool((out == exp).all())
+    host = dmm.as_uint32(g)
+    for k in range(0, count, 64):
+        s, _, rep = port.permute(host[k], int(seeds[k]))
+        got = reps.report(k)
+        assert s == 0 and all(got[f] == rep[f] for f in ("iterations", "random_words", "packed_width",
+                                                           "cleanup_retries", "leftover_history", "shifts"))
