@@ -89,6 +89,8 @@ extern "C" dmm_status dmm_gen_instances(int kind, uint32_t w, uint32_t m, uint64
         return DMM_OK;
     const unsigned threads = 128;
     const uint64_t blocks = (count + threads - 1) / threads;
+    if (blocks > 0x7FFFFFFFull)
+        return DMM_INVALID_ARGUMENT;  // grid x limit
     dmmdev::k_gen_instances<<<unsigned(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(kind, w, m, seed0,
                                                                                                count, out);
     return dmmhost::check_launch("k_gen_instances");

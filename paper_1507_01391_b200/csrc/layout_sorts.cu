@@ -70,6 +70,8 @@ dmm_status launch_layout(const uint32_t* in, uint32_t* out, uint64_t count, int 
     if (count == 0)
         return DMM_OK;
     const uint64_t blocks = kMulti ? count : (count + kWarps - 1) / kWarps;
+    if (blocks > 0x7FFFFFFFull)
+        return DMM_INVALID_ARGUMENT;  // grid x limit
     kern<<<unsigned(blocks), kWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(in, out, count, order, domain,
                                                                                      status);
     return check_launch("k_layout");

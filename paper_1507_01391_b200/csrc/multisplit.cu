@@ -274,6 +274,8 @@ dmm_status run_multisplit(const uint32_t* keys, uint64_t n, uint32_t shift, uint
     uint64_t* block_sums = offsets + ((total + 31) & ~uint64_t(31));
     const unsigned warps_per_block = 8;
     const uint64_t grid = (ntiles + warps_per_block - 1) / warps_per_block;
+    if (grid > 0x7FFFFFFFull || nblocks > 0x7FFFFFFFull)
+        return DMM_INVALID_ARGUMENT;  // grid x limit
     dmmdev::k_ms_count<LB><<<unsigned(grid), warps_per_block * 32, 0, s>>>(keys, n, shift, tile_counts, ntiles);
     if (dmm_status e = check_launch("k_ms_count"); e != DMM_OK)
         return e;

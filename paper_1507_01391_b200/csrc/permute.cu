@@ -656,6 +656,8 @@ dmm_status launch_permute(const uint32_t* in, uint32_t* out, uint64_t count, con
     if (dmm_status e = configure_kernel(kern, smem, configured); e != DMM_OK)
         return e;
     const uint64_t blocks = (count + kMach - 1) / kMach;
+    if (blocks > 0x7FFFFFFFull)
+        return DMM_INVALID_ARGUMENT;  // grid x limit
     kern<<<unsigned(blocks), kMach * R, smem, s>>>(in, out, count, seeds, states, a, reps, hist, shifts, status);
     return check_launch("k_permute");
 }
