@@ -179,10 +179,20 @@ def cpu_baseline(cfg_name: str, seconds: float = 15.0):
         if secs * 4 >= seconds or sample >= (1 << 16) or sample * w * m >= (1 << 26):
             break
         sample *= 2
+    # the growth runs warmed the host; multi-threaded host timings vary run to run, so take
+    # the median of three timed runs of the final sample
+    times = [secs]
+    for _ in range(2):
+        _, t, g2 = ref.cpu_baseline(alg_id, inst, seeds=np.arange(sample, dtype=np.uint64),
+                                    domain=1 << 32, nthreads=nthreads)
+        times.append(t)
+        good = min(good, g2)
+    secs = sorted(times)[1]
     keys = sample * w * m
     return {"value": keys / secs, "unit": "keys/s", "cores": nthreads, "kind": "reference",
             "sample": f"{note}{sample} instances of {w}x{m} through run_algorithm({alg}) "
-                      f"(strict, auditor on, host_threads=1) on {nthreads} threads, {secs:.2f} s, "
+                      f"(strict, auditor on, host_threads=1) on {nthreads} threads, median of 3 "
+                      f"runs {secs:.2f} s (range {min(times):.2f}-{max(times):.2f} s), "
                       f"{good}/{sample} correct"}
 
 
