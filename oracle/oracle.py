@@ -216,6 +216,10 @@ class Ref:
         L.dmmr_layout.argtypes = [C.c_int, C.c_uint32, C.c_uint32, u64p]
         L.dmmr_general_sort_shape_ok.argtypes = [C.c_uint64, C.c_uint64]
         L.dmmr_permute_threshold.argtypes = [C.c_uint32, C.c_uint32]
+        L.dmmr_instance_to_text.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, u64p, C.c_char_p,
+                                            C.c_uint64]
+        L.dmmr_instance_to_text.restype = C.c_uint64
+        L.dmmr_instance_from_text.argtypes = [C.c_char_p, u64p, u64p, C.c_uint64]
         L.dmmr_permute_threshold.restype = C.c_uint64
         L.dmmr_cpu_baseline.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, u32p, u64p, C.c_uint64,
                                         C.c_uint32, C.POINTER(C.c_double), u64p]
@@ -224,6 +228,21 @@ class Ref:
         g = np.zeros(w * m, dtype=np.uint64)
         self.lib.dmmr_gen_instance(kind, w, m, seed, _ptr(g))
         return g.reshape(w, m)
+
+    def instance_to_text(self, kind: int, w: int, m: int, seed: int, grid) -> str:
+        g = np.ascontiguousarray(grid, dtype=np.uint64).reshape(-1)
+        n = self.lib.dmmr_instance_to_text(kind, w, m, seed, _ptr(g), None, 0)
+        buf = C.create_string_buffer(n)
+        self.lib.dmmr_instance_to_text(kind, w, m, seed, _ptr(g), buf, n)
+        return buf.raw[:n].decode()
+
+    def instance_from_text(self, text: str, cap: int = 1 << 16):
+        """-> (status, (kind, w, m, seed), grid[:w*m])"""
+        hdr = np.zeros(4, dtype=np.uint64)
+        g = np.zeros(cap, dtype=np.uint64)
+        s = self.lib.dmmr_instance_from_text(text.encode(), _ptr(hdr), _ptr(g), cap)
+        k, w, m, sd = (int(x) for x in hdr)
+        return s, (k, w, m, sd), g[: w * m] if s == 0 else None
 
     def run_algorithm(self, alg: int, grid, seed: int, strict: bool = True):
         g = _u64(grid)

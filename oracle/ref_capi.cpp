@@ -14,6 +14,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstring>
+#include <sstream>
 #include <thread>
 
 #include "../include/dmm_status.h"
@@ -349,6 +350,38 @@ int dmmr_cpu_baseline(int alg, uint32_t w, uint32_t m, uint64_t count, const uin
     if (n_correct)
         *n_correct = good.load();
     return err.load();
+}
+
+// instance_to_text (instance.hpp:103-115): writes up to cap bytes, returns the full length.
+uint64_t dmmr_instance_to_text(int kind, uint32_t w, uint32_t m, uint64_t seed, const uint64_t* grid, char* buf,
+                               uint64_t cap) {
+    Instance in;
+    in.kind = static_cast<InstanceKind>(kind);
+    in.w = w;
+    in.m = m;
+    in.seed = seed;
+    in.grid.assign(grid, grid + uint64_t(w) * m);
+    const std::string s = instance_to_text(in);
+    if (buf && cap)
+        std::memcpy(buf, s.data(), std::min<uint64_t>(cap, s.size()));
+    return s.size();
+}
+
+// instance_from_text (instance.hpp:117-128): header into hdr[kind, w, m, seed], grid into
+// grid[0..cap); returns a dmm_status.
+int dmmr_instance_from_text(const char* text, uint64_t* hdr, uint64_t* grid, uint64_t cap) {
+    try {
+        std::istringstream is(text);
+        Instance in = instance_from_text(is);
+        hdr[0] = static_cast<uint64_t>(in.kind);
+        hdr[1] = in.w;
+        hdr[2] = in.m;
+        hdr[3] = in.seed;
+        std::memcpy(grid, in.grid.data(), sizeof(uint64_t) * std::min<uint64_t>(cap, in.grid.size()));
+        return 0;
+    } catch (...) {
+        return status_of_current_exception();
+    }
 }
 
 }  // extern "C"

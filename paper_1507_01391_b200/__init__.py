@@ -11,3 +11,7 @@ from .dmm import (  # noqa: F401
     as_uint32, gen_instances, gen_keys, multisplit, integer_sort_general, lib, partition_general, partition_short_wide,
     partition_square, permute, permute_into, sort_rows, sort_short_wide, sort_square, sort_tall, sort_wide_any, supported,
     to_column_major, to_row_major, transpose_square, version)
+from . import instance  # noqa: F401,E402  (instance.hpp mirror: text format, run_algorithm)
+from .instance import (  # noqa: F401,E402
+    Instance, RunOutcome, RunReport, TraceIncomplete, csv_header, csv_line, gen_instance, instance_from_text,
+    instance_to_text, load_instance, run_algorithm, run_algorithms, save_instance, validate_instance)

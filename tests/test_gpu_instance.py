@@ -1,0 +1,85 @@
+"""run_algorithm over the B200 kernels (paper_1507_01391_b200/instance.py) against the
+reference's own run_algorithm (instance.hpp:283-363, oracle/_ref) on the same instances:
+every report field except the step meter, the permute pipeline report, and the final grid.
+Also the reference harness's run_algorithm cases (tests/test_harness.cpp:54-83)."""
+import numpy as np
+import pytest
+
+import paper_1507_01391_b200 as dmm
+from oracle.oracle import ALGORITHMS as REF_ALG
+from paper_1507_01391_b200 import instance as I
+
+pytestmark = pytest.mark.gpu
+
+KIND_ID = {"sort": 0, "partition": 1, "permute": 2}
+
+CASES = [
+    ("partition_general", 32, 32), ("partition_general", 32, 16), ("partition_general", 64, 8),
+    ("partition_square", 16, 16), ("partition_short_wide", 8, 64), ("integer_sort_general", 32, 16),
+    ("integer_sort_general", 32, 128), ("sort_square", 16, 16), ("sort_tall", 64, 16),
+    ("sort_short_wide", 4, 16), ("permute", 32, 32), ("permute", 64, 8), ("permute", 128, 64),
+]
+
+
+def _gen(ref, alg, w, m, seed):
+    kind = I.instance_kind_for(alg)
+    if kind == "sort":
+        # 32-bit keys (the B200 layout); the reference's sort kind draws 64-bit words
+        return I.gen_instance("sort", w, m, seed)
+    return I.Instance(kind, w, m, seed, ref.gen_instance(KIND_ID[kind], w, m, seed))
+
+
+@pytest.mark.parametrize("alg,w,m", CASES)
+def test_run_algorithm_matches_reference(ref, alg, w, m):
+    if not dmm.supported(alg, w, m):
+        pytest.skip(f"{alg} {w}x{m} not compiled")
+    insts = [_gen(ref, alg, w, m, seed) for seed in (1, 2, 3)]
+    outs = I.run_algorithms(alg, insts)
+    for inst, out in zip(insts, outs):
+        s, ref_grid, rr = ref.run_algorithm(REF_ALG[alg], inst.grid.reshape(w, m), inst.seed)
+        assert s == 0
+        rep = out.report
+        assert rep.correct and rr["correct"]
+        assert (rep.algorithm, rep.w, rep.m, rep.seed) == (alg, w, m, inst.seed)
+        assert (rep.iterations, rep.fallback, rep.cleanup_retries) == \
+            (rr["iterations"], rr["fallback"], rr["cleanup_retries"])
+        assert rep.conflicts == rr["conflicts"] == 0
+        assert (out.result == ref_grid).all()
+        if alg == "permute":
+            assert out.pipeline == rr["pipeline"]
+    # one instance through the single-instance entry gives the same report
+    one = I.run_algorithm(alg, insts[0])
+    assert one.report == outs[0].report
+
+
+def test_gen_instance_matches_reference(ref):
+    for kind, w, m in [("partition", 32, 32), ("partition", 4, 16), ("permute", 128, 64), ("permute", 16, 8)]:
+        inst = I.gen_instance(kind, w, m, 7)
+        assert (inst.grid == ref.gen_instance(KIND_ID[kind], w, m, 7).reshape(-1)).all()
+
+
+def test_harness_cases(ref):
+    # test_harness.cpp:55-61: an already sorted sort_square instance
+    inst = I.gen_instance("sort", 16, 16, 5)
+    inst.grid = np.sort(inst.grid)
+    out = I.run_algorithm("sort_square", inst)
+    assert out.report.correct and out.report.conflicts == 0
+    # :66-71 partition_general at a small general shape
+    out = I.run_algorithm("partition_general", _gen(ref, "partition_general", 64, 8, 21))
+    assert out.report.correct and out.report.conflicts == 0
+    # :72-77 permute reports iterations and the exact layout
+    out = I.run_algorithm("permute", _gen(ref, "permute", 64, 8, 13))
+    assert out.report.correct and out.report.iterations >= 1
+    # :78-83 reproducibility
+    inst = _gen(ref, "permute", 64, 8, 17)
+    assert I.run_algorithm("permute", inst).report.summary() == I.run_algorithm("permute", inst).report.summary()
+    # an explicit algorithm seed replaces the instance seed (RunOptions.seed)
+    s, _, rr = ref.run_algorithm(REF_ALG["permute"], inst.grid.reshape(64, 8), 99)
+    out = I.run_algorithm("permute", inst, seed=99)
+    assert out.report.seed == 99 and out.pipeline == rr["pipeline"]
+
+
+def test_wide_words_rejected():
+    inst = I.Instance("sort", 4, 16, 0, np.full(64, 1 << 40, dtype=np.uint64))
+    with pytest.raises(dmm.KeyOutOfRange):
+        I.run_algorithm("sort_short_wide", inst)
