@@ -54,6 +54,8 @@ namespace b200 {
         case DMM_NOT_SQUARE: throw NotSquare(msg);
         case DMM_OUT_OF_BOUNDS: throw OutOfBounds(msg);
         case DMM_OVERLAPPING_VIEWS: throw OverlappingViews(msg);
+        case DMM_NOT_BIJECTIVE: throw NotBijective(msg);
+        case DMM_CONFLICT_VIOLATION: throw ConflictViolation(msg);
         default: throw Error(msg);
     }
 }
@@ -308,6 +310,71 @@ inline void to_row_major(const MatrixView& v) {
     detail::simple(v, [&](uint32_t* p) { return dmm_to_row_major(p, p, v.W(), v.M(), 1, nullptr); },
                    "to_row_major");
 }
+
+/// Schedule offline_schedule(W, M, perm)  layout.hpp:207-230 -- the host precompute of
+/// libdmm_b200.so; the same rounds as the reference, move for move.
+inline Schedule offline_schedule(u32 W, u32 M, const std::vector<std::pair<u32, u32>>& perm) {
+    if (perm.size() != u64(W) * M)
+        throw NotBijective("permutation table has wrong size");
+    std::vector<uint32_t> p(2 * perm.size()), mv(4 * perm.size() + 4);
+    for (std::size_t i = 0; i < perm.size(); ++i) {
+        p[2 * i] = perm[i].first;
+        p[2 * i + 1] = perm[i].second;
+    }
+    check(dmm_offline_schedule(W, M, p.data(), mv.data()), "offline_schedule");
+    Schedule s;
+    for (u32 r = 0; W && r < M; ++r) {
+        std::vector<Move> round(W);
+        for (u32 i = 0; i < W; ++i) {
+            const uint32_t* x = &mv[4 * (u64(r) * W + i)];
+            round[i] = {x[0], x[1], x[2], x[3]};
+        }
+        s.rounds.push_back(std::move(round));
+    }
+    return s;
+}
+
+/// void apply_schedule(const MatrixView&, const Schedule&, u32 dst_base)  layout.hpp:246-263:
+/// moves the view's working window into the window at dst_base on the B200 (one warp, DMM bank
+/// = shared-memory bank); cells no move writes keep their contents.  A round reusing a bank
+/// raises ConflictViolation, a move outside the shape OutOfBounds -- before any write.
+inline void apply_schedule(const MatrixView& v, const Schedule& s, u32 dst_base) {
+    const u32 W = v.W(), M = v.M();
+    std::vector<uint32_t> src = gather(v), dstw(u64(W) * M);
+    for (u32 r = 0; r < W; ++r)
+        for (u32 c = 0; c < M; ++c) {
+            const word x = v.machine().peek(v.bank(r), dst_base + c);
+            if (x >> 32)
+                throw KeyOutOfRange("B200 kernels take 32-bit words");
+            dstw[u64(r) * M + c] = static_cast<uint32_t>(x);
+        }
+    std::vector<uint32_t> mv, starts{0};
+    for (const auto& round : s.rounds) {
+        for (const Move& m : round)
+            mv.insert(mv.end(), {m.src_bank, m.src_off, m.dst_bank, m.dst_off});
+        starts.push_back(uint32_t(mv.size() / 4));
+    }
+    DeviceBuffer din(sizeof(uint32_t) * src.size()), dout(sizeof(uint32_t) * dstw.size()),
+        dmv(sizeof(uint32_t) * mv.size()), dst(sizeof(uint32_t) * starts.size()), dstatus(16);
+    to_device(din, src);
+    to_device(dout, dstw);
+    if (!mv.empty())
+        to_device(dmv, mv);
+    to_device(dst, starts);
+    check(dmm_apply_schedule(din.as<uint32_t>(), dout.as<uint32_t>(), W, M, 1, dmv.as<uint32_t>(),
+                                     dst.as<uint32_t>(), uint32_t(s.rounds.size()), uint32_t(mv.size() / 4),
+                                     dstatus.as<uint8_t>(), nullptr),
+                  "apply_schedule");
+    uint8_t status = 0;
+    cuda_check(cudaMemcpy(&status, dstatus.ptr, 1, cudaMemcpyDeviceToHost), "D2H");
+    if (status != DMM_OK)
+        raise(static_cast<dmm_status>(status), "apply_schedule");
+    to_host(dstw, dout);
+    for (u32 r = 0; r < W; ++r)
+        for (u32 c = 0; c < M; ++c)
+            v.machine().poke(v.bank(r), dst_base + c, dstw[u64(r) * M + c]);
+}
+inline void apply_schedule(const MatrixView& v, const Schedule& s) { b200::apply_schedule(v, s, v.s0_base()); }
 
 /// PermuteReport permute(Machine&, Rng&, const PermuteParams&)  permute.hpp:545-628
 inline PermuteReport permute(Machine& mach, Rng& rng, const PermuteParams& params = {}) {

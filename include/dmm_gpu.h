@@ -166,6 +166,27 @@ uint64_t dmm_multisplit_workspace_bytes(uint64_t n, uint32_t nbuckets);
 dmm_status dmm_multisplit(const uint32_t* keys, uint64_t n, uint32_t shift, uint32_t nbuckets, uint32_t* out,
                           uint64_t* bucket_starts, void* workspace, void* stream);
 
+/* ---- offline schedules for fixed permutations --------------------------------- */
+/* Schedule offline_schedule(W, M, perm)                          layout.hpp:207-230
+ * Host precompute (no device work), as in the reference.  perm[2*(r*m + c)] / [.. + 1] =
+ * destination bank / offset of cell (r, c).  moves: w*m moves of 4 words (src_bank, src_off,
+ * dst_bank, dst_off) -- exactly m rounds of w moves, round k = moves[k*w .. (k+1)*w), the
+ * reference's rounds move for move.  DMM_NOT_BIJECTIVE on a table that is not a bijection. */
+dmm_status dmm_offline_schedule(uint32_t w, uint32_t m, const uint32_t* perm, uint32_t* moves);
+
+/* void apply_schedule(const MatrixView&, const Schedule&, u32 dst_base)   layout.hpp:246-263
+ * Applies any schedule (device arrays: moves as above, 16-byte aligned; round r = moves
+ * [round_start[r], round_start[r+1]), n_moves = round_start[n_rounds]) to count instances
+ * [count][w][m] of in, writing out: out(dst) = in(src) per move, rounds in order.  Cells no
+ * move writes keep out's contents.  The schedule is validated on the device before any write:
+ * status[0] (device byte) = DMM_OUT_OF_BOUNDS / DMM_CONFLICT_VIOLATION (a round reusing a source
+ * or destination bank, Schedule::validate layout.hpp:80-95) or 0.  w <= 32, m <= 64,
+ * n_moves, n_rounds <= 8192. */
+uint64_t dmm_apply_schedule_smem_bytes(uint32_t m, uint32_t n_moves, uint32_t n_rounds);
+dmm_status dmm_apply_schedule(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
+                              const uint32_t* moves, const uint32_t* round_start, uint32_t n_rounds,
+                              uint32_t n_moves, uint8_t* status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,8 @@ typedef enum dmm_status {
     DMM_OUT_OF_BOUNDS = 9,          /* dmm::OutOfBounds           core.hpp:66 */
     DMM_OVERLAPPING_VIEWS = 10,     /* dmm::OverlappingViews      core.hpp:65 */
     DMM_ERROR = 11,                 /* dmm::Error (generic)       core.hpp:59 */
+    DMM_NOT_BIJECTIVE = 12,         /* dmm::NotBijective          core.hpp:71 */
+    DMM_CONFLICT_VIOLATION = 13,    /* dmm::ConflictViolation     core.hpp:63 */
     /* B200-side conditions with no reference counterpart */
     DMM_UNSUPPORTED_SHAPE = 64,     /* shape the reference accepts but no kernel is built for */
     DMM_INVALID_ARGUMENT = 65,      /* null pointer / zero count / bad flag */

@@ -220,6 +220,9 @@ class Ref:
                                             C.c_uint64]
         L.dmmr_instance_to_text.restype = C.c_uint64
         L.dmmr_instance_from_text.argtypes = [C.c_char_p, u64p, u64p, C.c_uint64]
+        L.dmmr_offline_schedule.argtypes = [C.c_uint32, C.c_uint32, u32p, u32p, u32p, u32p]
+        L.dmmr_schedule_to_text.argtypes = [u32p, u32p, C.c_uint32, C.c_char_p, C.c_uint64]
+        L.dmmr_schedule_to_text.restype = C.c_uint64
         L.dmmr_permute_threshold.restype = C.c_uint64
         L.dmmr_cpu_baseline.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, u32p, u64p, C.c_uint64,
                                         C.c_uint32, C.POINTER(C.c_double), u64p]
@@ -234,6 +237,30 @@ class Ref:
         n = self.lib.dmmr_instance_to_text(kind, w, m, seed, _ptr(g), None, 0)
         buf = C.create_string_buffer(n)
         self.lib.dmmr_instance_to_text(kind, w, m, seed, _ptr(g), buf, n)
+        return buf.raw[:n].decode()
+
+    def offline_schedule(self, w: int, m: int, perm):
+        """-> (status, rounds: list of lists of (src_bank, src_off, dst_bank, dst_off))"""
+        p = np.ascontiguousarray(perm, dtype=np.uint32).reshape(-1)
+        n = w * m
+        moves = np.zeros(max(4 * n, 4), dtype=np.uint32)
+        lens = np.zeros(max(n, 1), dtype=np.uint32)
+        nr = C.c_uint32()
+        s = self.lib.dmmr_offline_schedule(w, m, _ptr(p, u32p), _ptr(moves, u32p), _ptr(lens, u32p), C.byref(nr))
+        rounds, k = [], 0
+        for r in range(nr.value if s == 0 else 0):
+            rounds.append([tuple(int(x) for x in moves[4 * j: 4 * j + 4]) for j in range(k, k + int(lens[r]))])
+            k += int(lens[r])
+        return s, rounds
+
+    def schedule_to_text(self, rounds) -> str:
+        mv = np.array([x for r in rounds for x in r], dtype=np.uint32).reshape(-1)
+        if mv.size == 0:
+            mv = np.zeros(4, dtype=np.uint32)
+        lens = np.array([len(r) for r in rounds] or [0], dtype=np.uint32)
+        n = self.lib.dmmr_schedule_to_text(_ptr(mv, u32p), _ptr(lens, u32p), len(rounds), None, 0)
+        buf = C.create_string_buffer(max(n, 1))
+        self.lib.dmmr_schedule_to_text(_ptr(mv, u32p), _ptr(lens, u32p), len(rounds), buf, n)
         return buf.raw[:n].decode()
 
     def instance_from_text(self, text: str, cap: int = 1 << 16):

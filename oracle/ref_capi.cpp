@@ -384,4 +384,50 @@ int dmmr_instance_from_text(const char* text, uint64_t* hdr, uint64_t* grid, uin
     }
 }
 
+// offline_schedule (layout.hpp:207-230): perm as (dst_bank, dst_off) pairs; moves out as
+// (src_bank, src_off, dst_bank, dst_off) in round order, round_len[r] = moves in round r.
+int dmmr_offline_schedule(uint32_t w, uint32_t m, const uint32_t* perm, uint32_t* moves, uint32_t* round_len,
+                          uint32_t* n_rounds) {
+    try {
+        std::vector<std::pair<u32, u32>> p(uint64_t(w) * m);
+        for (uint64_t i = 0; i < p.size(); ++i)
+            p[i] = {perm[2 * i], perm[2 * i + 1]};
+        Schedule s = offline_schedule(w, m, p);
+        uint64_t k = 0;
+        *n_rounds = uint32_t(s.rounds.size());
+        for (std::size_t r = 0; r < s.rounds.size(); ++r) {
+            round_len[r] = uint32_t(s.rounds[r].size());
+            for (const Move& mv : s.rounds[r]) {
+                moves[4 * k] = mv.src_bank;
+                moves[4 * k + 1] = mv.src_off;
+                moves[4 * k + 2] = mv.dst_bank;
+                moves[4 * k + 3] = mv.dst_off;
+                ++k;
+            }
+        }
+        return 0;
+    } catch (const NotBijective&) {
+        return DMM_NOT_BIJECTIVE;
+    } catch (...) {
+        return status_of_current_exception();
+    }
+}
+
+// schedule_to_text (layout.hpp:268-278) of a schedule given as round lengths + moves.
+uint64_t dmmr_schedule_to_text(const uint32_t* moves, const uint32_t* round_len, uint32_t n_rounds, char* buf,
+                               uint64_t cap) {
+    Schedule s;
+    uint64_t k = 0;
+    for (uint32_t r = 0; r < n_rounds; ++r) {
+        std::vector<Move> round;
+        for (uint32_t i = 0; i < round_len[r]; ++i, ++k)
+            round.push_back({moves[4 * k], moves[4 * k + 1], moves[4 * k + 2], moves[4 * k + 3]});
+        s.rounds.push_back(std::move(round));
+    }
+    const std::string t = schedule_to_text(s);
+    if (buf && cap)
+        std::memcpy(buf, t.data(), std::min<uint64_t>(cap, t.size()));
+    return t.size();
+}
+
 }  // extern "C"

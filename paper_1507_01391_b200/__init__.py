@@ -6,7 +6,7 @@ DMM algorithms (/root/reference/proj/include/dmm).  The compute lives in libdmm_
 from .dmm import (  # noqa: F401
     FLAG_EXT_PARTIAL_GROUPS, FLAG_NO_ENFORCE_PRE, FLAG_NONSTRICT, KIND_PARTITION, KIND_PERMUTE, KIND_SORT_U32,
     ORDER_ALT, ORDER_ALT_DESC, ORDER_ASC, ORDER_DESC, CapacityExceeded, ConflictViolation, CudaError,
-    DivisibilityViolation, Error, GeneralStats, InvalidInstance, KeyOutOfRange, NotSquare, OutOfBounds,
+    DivisibilityViolation, Error, GeneralStats, InvalidInstance, KeyOutOfRange, NotBijective, NotSquare, OutOfBounds,
     OverlappingViews, PackingOverflow, PermuteReports, PostconditionFailed, ShapeViolation, UnsupportedShape,
     as_uint32, gen_instances, gen_keys, multisplit, integer_sort_general, lib, partition_general, partition_short_wide,
     partition_square, permute, permute_into, sort_rows, sort_short_wide, sort_square, sort_tall, sort_wide_any, supported,
@@ -15,3 +15,6 @@ from . import instance  # noqa: F401,E402  (instance.hpp mirror: text format, ru
 from .instance import (  # noqa: F401,E402
     Instance, RunOutcome, RunReport, TraceIncomplete, csv_header, csv_line, gen_instance, instance_from_text,
     instance_to_text, load_instance, run_algorithm, run_algorithms, save_instance, validate_instance)
+from . import schedule  # noqa: F401,E402  (layout.hpp offline schedules)
+from .schedule import (  # noqa: F401,E402
+    DeviceSchedule, Move, Schedule, apply_schedule, offline_schedule, schedule_from_text, schedule_to_text)

@@ -39,7 +39,7 @@ class Error(RuntimeError):
 
 
 class ConflictViolation(Error):
-    status = -1
+    status = 13
 
 
 class OverlappingViews(ConflictViolation):
@@ -82,6 +82,10 @@ class OutOfBounds(Error):
     status = 9
 
 
+class NotBijective(Error):
+    status = 12
+
+
 class UnsupportedShape(Error):
     """The reference accepts the shape but no B200 kernel is built for it (no fallback)."""
     status = 64
@@ -93,7 +97,8 @@ class CudaError(Error):
 
 _BY_STATUS = {c.status: c for c in (ShapeViolation, InvalidInstance, KeyOutOfRange, DivisibilityViolation,
                                      PostconditionFailed, PackingOverflow, CapacityExceeded, NotSquare,
-                                     OutOfBounds, OverlappingViews, UnsupportedShape, CudaError)}
+                                     OutOfBounds, OverlappingViews, NotBijective, ConflictViolation,
+                                     UnsupportedShape, CudaError)}
 _BY_STATUS[11] = Error
 _BY_STATUS[65] = ValueError
 

@@ -371,6 +371,44 @@ static void short_wide_hook_cases() {
     }
 }
 
+static void schedule_cases() {
+    // offline_schedule move for move, apply_schedule into the s0 window cell for cell
+    Rng rng(19);
+    for (auto [W, M] : {std::pair<u32, u32>{16, 8}, {32, 32}, {5, 7}, {4, 3}, {32, 64}}) {
+        for (int t = 0; t < 4; ++t) {
+            auto lin = random_permutation(rng, u64(W) * M);
+            std::vector<std::pair<u32, u32>> perm(lin.size());
+            for (std::size_t i = 0; i < lin.size(); ++i)
+                perm[i] = {u32(lin[i] / M), u32(lin[i] % M)};
+            Schedule a = offline_schedule(W, M, perm), b = b200::offline_schedule(W, M, perm);
+            CHECK(schedule_to_text(a) == schedule_to_text(b));
+            Machine ma = make_machine(W, M), mb = make_machine(W, M);
+            MatrixView va = MatrixView::full(ma), vb = MatrixView::full(mb);
+            std::vector<word> g(u64(W) * M);
+            for (auto& x : g)
+                x = rng() >> 33;
+            va.load(g);
+            vb.load(g);
+            apply_schedule(va, a);
+            b200::apply_schedule(vb, b);
+            bool same = true;
+            for (u32 r = 0; r < W; ++r)
+                for (u32 c = 0; c < M; ++c)
+                    same = same && ma.peek(r, va.s0(c)) == mb.peek(r, vb.s0(c));
+            CHECK(same);
+        }
+    }
+    {
+        std::vector<std::pair<u32, u32>> bad(8, {0, 0});
+        CHECK(throws_as<NotBijective>([&] { b200::offline_schedule(4, 2, bad); }));
+        Machine mb = make_machine(4, 2);
+        MatrixView vb = MatrixView::full(mb);
+        Schedule clash;
+        clash.rounds.push_back({{0, 0, 1, 0}, {0, 1, 2, 0}});
+        CHECK(throws_as<ConflictViolation>([&] { b200::apply_schedule(vb, clash); }));
+    }
+}
+
 int main() {
     partition_cases();
     integer_sort_cases();
@@ -380,6 +418,7 @@ int main() {
     run_algorithm_cases();
     short_wide_hook_cases();
     permute_cases();
+    schedule_cases();
     std::printf("shim parity: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;
 }
