@@ -255,6 +255,8 @@ def main():
     ap.add_argument("--e2e-chunks", type=int, default=8, help="pipeline chunks of the end-to-end leg")
     ap.add_argument("--no-graph", action="store_true", help="time the eager launch loop instead of graph replay")
     ap.add_argument("--e2e-streams", type=int, default=3, help="CUDA streams of the end-to-end leg")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="cfg5 exchange: fused scatter into peer buffers (p2p) or multisplit + NCCL all-to-all")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -298,15 +300,26 @@ def main():
         if alg == "permute":
             return dmm.permute_into(src, dst, seeds, perm_bufs)
         if alg == "global_partition":
-            from paper_1507_01391_b200.distributed import global_partition
-            res, _ = global_partition(src.view(-1))
+            if args.transport == "p2p":
+                res, _ = global_partition_p2p(src.view(-1), peers[0])
+            else:
+                res, _ = global_partition(src.view(-1))
             return res, None
         return dmm.integer_sort_general(src, 1 << 32, out=dst, check=False)
+
+    if alg == "global_partition":
+        from paper_1507_01391_b200 import distributed as dmm_dist
+        from paper_1507_01391_b200.distributed import PeerBuffers, global_partition, global_partition_p2p, p2p_capacity
+        # two receive buffers: the end-to-end leg double-buffers consecutive steps
+        peers = [PeerBuffers(p2p_capacity(keys_per_gpu, world)) for _ in range(2)] \
+            if args.transport == "p2p" else None
 
     for _ in range(args.warmup):
         step(g, out)
     torch.cuda.synchronize()
     launches_per_step = int(dmm.lib().dmm_last_launch_count())
+    if alg == "global_partition" and args.transport == "p2p":
+        launches_per_step = dmm_dist.last_launches
 
     # The step is one kernel launch; it is captured once into a CUDA graph and the timed loop
     # replays it K times, so host-side stalls cannot starve the GPU between steps (measured:
@@ -415,7 +428,6 @@ def main():
         # the global partition is bucket-major over the whole batch, so a step is not chunked;
         # consecutive steps are double-buffered instead (two streams, two host result buffers):
         # step i's D2H overlaps step i+1's H2D (PCIe is full duplex)
-        from paper_1507_01391_b200.distributed import global_partition
         e2e_streams = [torch.cuda.Stream(), torch.cuda.Stream()]
         d_in = [torch.empty_like(g) for _ in range(2)]
         h_outs = [h_out, torch.empty_like(h_in).pin_memory()]
@@ -424,7 +436,10 @@ def main():
             s = e2e_streams[i % 2]
             with torch.cuda.stream(s):
                 d_in[i % 2].copy_(h_in, non_blocking=True)
-                res, _ = global_partition(d_in[i % 2].view(-1))
+                if args.transport == "p2p":
+                    res, _ = global_partition_p2p(d_in[i % 2].view(-1), peers[i % 2])
+                else:
+                    res, _ = global_partition(d_in[i % 2].view(-1))
                 h_outs[i % 2].view(-1)[: res.numel()].copy_(res, non_blocking=True)
 
         for i in range(2):  # warm-up
@@ -470,7 +485,11 @@ def main():
             "config": {"workload": desc, "algorithm": alg, "w": w, "m": m, "instances_per_gpu": count,
                        "keys_per_gpu": keys_per_gpu, "l2": "inputs 2x L2 (no flush needed)",
                        "timed_loop": "CUDA graph replay of the one-launch step" if graph is not None else "eager launches",
-                       "parallelism": f"instances sharded over {world} GPU(s)"},
+                       "parallelism": (f"instances sharded over {world} GPU(s)" if alg != "global_partition" else
+                                       f"keys sharded over {world} GPU(s); exchange: " +
+                                       ("fused into the scatter (stores into the owners' receive buffers, "
+                                        "CUDA IPC / NVLink peer memory)" if args.transport == "p2p"
+                                        else "multisplit + NCCL all-to-all"))},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"],
                          "traffic": (traffic or {}).get("bytes_per_launch"),

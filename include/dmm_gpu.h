@@ -166,6 +166,19 @@ uint64_t dmm_multisplit_workspace_bytes(uint64_t n, uint32_t nbuckets);
 dmm_status dmm_multisplit(const uint32_t* keys, uint64_t n, uint32_t shift, uint32_t nbuckets, uint32_t* out,
                           uint64_t* bucket_starts, void* workspace, void* stream);
 
+/* The same partition with the exchange fused into the scatter (two calls, one workspace):
+ * dmm_multisplit_count writes bucket_starts (device, nbuckets entries: where bucket b would
+ * start in a local bucket-major output; the local counts follow) and keeps the per-tile
+ * offsets in the workspace; dmm_multisplit_scatter_to then writes bucket b's keys, stable by
+ * source index, to dst[b][dst_base[b] ..] -- dst (device array of nbuckets device pointers,
+ * e.g. peer GPUs' receive buffers mapped over NVLink) and dst_base (device) come from the
+ * caller's count exchange (paper_1507_01391_b200/distributed.py, global_partition_p2p). */
+dmm_status dmm_multisplit_count(const uint32_t* keys, uint64_t n, uint32_t shift, uint32_t nbuckets,
+                                uint64_t* bucket_starts, void* workspace, void* stream);
+dmm_status dmm_multisplit_scatter_to(const uint32_t* keys, uint64_t n, uint32_t shift, uint32_t nbuckets,
+                                     uint32_t* const* dst, const uint64_t* dst_base, void* workspace,
+                                     void* stream);
+
 /* ---- offline schedules for fixed permutations --------------------------------- */
 /* Schedule offline_schedule(W, M, perm)                          layout.hpp:207-230
  * Host precompute (no device work), as in the reference.  perm[2*(r*m + c)] / [.. + 1] =

@@ -197,10 +197,14 @@ __global__ void k_ms_scan_add(uint64_t* __restrict__ out, uint64_t total, const 
         out[i] += block_sums[blockIdx.x];
 }
 
-template <int LB>
+// REMOTE: bucket b goes to its own destination array dst[b] (a peer GPU's receive buffer over
+// NVLink, or any device pointer) starting at dst_base[b] -- the all-to-all fused into the
+// scatter: keys leave the SM straight for the owner's memory, no staging copy, no NCCL pass.
+template <int LB, bool REMOTE = false>
 __global__ void __launch_bounds__(256) k_ms_scatter(const uint32_t* __restrict__ keys, uint64_t n, uint32_t shift,
                                                     const uint64_t* __restrict__ offsets, uint64_t ntiles,
-                                                    uint32_t* __restrict__ out) {
+                                                    uint32_t* __restrict__ out, uint32_t* const* __restrict__ dst = nullptr,
+                                                    const uint64_t* __restrict__ dst_base = nullptr) {
     constexpr int NB = 1 << LB;
     constexpr int H = Packed<NB>::H;
     const int lane = threadIdx.x & 31;
@@ -209,6 +213,13 @@ __global__ void __launch_bounds__(256) k_ms_scatter(const uint32_t* __restrict__
         return;
     // lane b < NB holds the running output position of bucket b
     uint64_t pos = lane < NB ? offsets[(uint64_t)lane * ntiles + tile] : 0;
+    uint32_t* my_dst = out;  // lane b < NB: bucket b's destination array
+    if constexpr (REMOTE) {
+        if (lane < NB) {
+            pos = pos - offsets[(uint64_t)lane * ntiles] + dst_base[lane];  // rank within the bucket
+            my_dst = dst[lane];
+        }
+    }
     const uint64_t base = tile * kMsTile;
     // rows of 32 consecutive keys, one per lane (coalesced 128-byte loads, 4 rows in flight):
     // the keys of one bucket in one row go to consecutive output words, so every warp store
@@ -249,8 +260,15 @@ __global__ void __launch_bounds__(256) k_ms_scatter(const uint32_t* __restrict__
                     tot_mine = (t >> (8 * (lane & 3))) & 0xFFu;
             }
             const uint64_t p0 = __shfl_sync(0xFFFFFFFFu, pos, (int)b);
-            if (valid[j])
-                out[p0 + lower] = k[j];
+            if constexpr (REMOTE) {
+                uint32_t* d = reinterpret_cast<uint32_t*>(
+                    __shfl_sync(0xFFFFFFFFu, reinterpret_cast<unsigned long long>(my_dst), (int)b));
+                if (valid[j])
+                    d[p0 + lower] = k[j];
+            } else {
+                if (valid[j])
+                    out[p0 + lower] = k[j];
+            }
             pos += tot_mine;
         }
     }
@@ -261,9 +279,11 @@ __global__ void __launch_bounds__(256) k_ms_scatter(const uint32_t* __restrict__
 namespace {
 using namespace dmmhost;
 
+// phase: 1 = count + scans (+ starts), 2 = scatter only (workspace from phase 1), 3 = both
 template <int LB>
 dmm_status run_multisplit(const uint32_t* keys, uint64_t n, uint32_t shift, uint32_t* out, uint64_t* starts,
-                          void* workspace, cudaStream_t s) {
+                          void* workspace, cudaStream_t s, int phase = 3, uint32_t* const* dst = nullptr,
+                          const uint64_t* dst_base = nullptr) {
     constexpr int NB = 1 << LB;
     const uint64_t ntiles = (n + dmmdev::kMsTile - 1) / dmmdev::kMsTile;
     const uint64_t total = ntiles * NB;
@@ -276,6 +296,11 @@ dmm_status run_multisplit(const uint32_t* keys, uint64_t n, uint32_t shift, uint
     const uint64_t grid = (ntiles + warps_per_block - 1) / warps_per_block;
     if (grid > 0x7FFFFFFFull || nblocks > 0x7FFFFFFFull)
         return DMM_INVALID_ARGUMENT;  // grid x limit
+    if (phase == 2) {
+        dmmdev::k_ms_scatter<LB, true><<<unsigned(grid), warps_per_block * 32, 0, s>>>(keys, n, shift, offsets,
+                                                                                      ntiles, nullptr, dst, dst_base);
+        return check_launch("k_ms_scatter (remote)");
+    }
     dmmdev::k_ms_count<LB><<<unsigned(grid), warps_per_block * 32, 0, s>>>(keys, n, shift, tile_counts, ntiles);
     if (dmm_status e = check_launch("k_ms_count"); e != DMM_OK)
         return e;
@@ -289,9 +314,12 @@ dmm_status run_multisplit(const uint32_t* keys, uint64_t n, uint32_t shift, uint
     dmmdev::k_ms_scan_add<<<unsigned(nblocks), dmmdev::kScanBlock, 0, s>>>(offsets, total, block_sums);
     if (dmm_status e = check_launch("k_ms_scan_add"); e != DMM_OK)
         return e;
-    dmmdev::k_ms_scatter<LB><<<unsigned(grid), warps_per_block * 32, 0, s>>>(keys, n, shift, offsets, ntiles, out);
-    if (dmm_status e = check_launch("k_ms_scatter"); e != DMM_OK)
-        return e;
+    if (phase == 3) {
+        dmmdev::k_ms_scatter<LB><<<unsigned(grid), warps_per_block * 32, 0, s>>>(keys, n, shift, offsets, ntiles,
+                                                                                 out);
+        if (dmm_status e = check_launch("k_ms_scatter"); e != DMM_OK)
+            return e;
+    }
     if (starts) {
         // bucket b starts where its tile 0 writes: offsets[b * ntiles] (bucket-major scan)
         cudaMemcpy2DAsync(starts, sizeof(uint64_t), offsets, ntiles * sizeof(uint64_t), sizeof(uint64_t), NB,
@@ -311,6 +339,49 @@ uint64_t dmm_multisplit_workspace_bytes(uint64_t n, uint32_t nbuckets) {
     const uint64_t total = ntiles * nbuckets;
     const uint64_t nblocks = (total + dmmdev::kScanBlock - 1) / dmmdev::kScanBlock;
     return ((total * 4 + 255) & ~uint64_t(255)) + ((total + 31) & ~uint64_t(31)) * 8 + nblocks * 8 + 256;
+}
+
+dmm_status dmm_multisplit_count(const uint32_t* keys, uint64_t n, uint32_t shift, uint32_t nbuckets,
+                                uint64_t* bucket_starts, void* workspace, void* stream) {
+    reset_launches();
+    if (!bucket_starts || !workspace || (n && !keys))
+        return DMM_INVALID_ARGUMENT;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n == 0)
+        return cudaMemsetAsync(bucket_starts, 0, sizeof(uint64_t) * nbuckets, s) == cudaSuccess
+                   ? DMM_OK
+                   : check_launch("cudaMemsetAsync");
+    switch (nbuckets) {
+        case 2: return run_multisplit<1>(keys, n, shift, nullptr, bucket_starts, workspace, s, 1);
+        case 4: return run_multisplit<2>(keys, n, shift, nullptr, bucket_starts, workspace, s, 1);
+        case 8: return run_multisplit<3>(keys, n, shift, nullptr, bucket_starts, workspace, s, 1);
+        case 16: return run_multisplit<4>(keys, n, shift, nullptr, bucket_starts, workspace, s, 1);
+        case 32: return run_multisplit<5>(keys, n, shift, nullptr, bucket_starts, workspace, s, 1);
+        default: break;
+    }
+    set_error("nbuckets must be a power of two in [2, 32]");
+    return DMM_INVALID_ARGUMENT;
+}
+
+dmm_status dmm_multisplit_scatter_to(const uint32_t* keys, uint64_t n, uint32_t shift, uint32_t nbuckets,
+                                     uint32_t* const* dst, const uint64_t* dst_base, void* workspace,
+                                     void* stream) {
+    reset_launches();
+    if (n == 0)
+        return DMM_OK;
+    if (!keys || !dst || !dst_base || !workspace)
+        return DMM_INVALID_ARGUMENT;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    switch (nbuckets) {
+        case 2: return run_multisplit<1>(keys, n, shift, nullptr, nullptr, workspace, s, 2, dst, dst_base);
+        case 4: return run_multisplit<2>(keys, n, shift, nullptr, nullptr, workspace, s, 2, dst, dst_base);
+        case 8: return run_multisplit<3>(keys, n, shift, nullptr, nullptr, workspace, s, 2, dst, dst_base);
+        case 16: return run_multisplit<4>(keys, n, shift, nullptr, nullptr, workspace, s, 2, dst, dst_base);
+        case 32: return run_multisplit<5>(keys, n, shift, nullptr, nullptr, workspace, s, 2, dst, dst_base);
+        default: break;
+    }
+    set_error("nbuckets must be a power of two in [2, 32]");
+    return DMM_INVALID_ARGUMENT;
 }
 
 dmm_status dmm_multisplit(const uint32_t* keys, uint64_t n, uint32_t shift, uint32_t nbuckets, uint32_t* out,

@@ -446,6 +446,26 @@ def multisplit(keys: torch.Tensor, nbuckets: int = 8, shift: int = 29, out=None,
     return res, starts
 
 
+def multisplit_count(keys: torch.Tensor, nbuckets: int, shift: int, starts: torch.Tensor, workspace: torch.Tensor,
+                     stream=None) -> None:
+    """First half of the fused partition + exchange: bucket starts of the local bucket-major
+    order into ``starts`` (int64 [nbuckets], device); the tile offsets stay in ``workspace``
+    (dmm_multisplit_workspace_bytes) for multisplit_scatter_to."""
+    k = keys.reshape(-1)
+    _check(lib().dmm_multisplit_count(k.data_ptr(), k.numel(), shift, nbuckets, starts.data_ptr(),
+                                      workspace.data_ptr(), _stream(stream)), "multisplit_count")
+
+
+def multisplit_scatter_to(keys: torch.Tensor, nbuckets: int, shift: int, dst_ptrs: torch.Tensor,
+                          dst_base: torch.Tensor, workspace: torch.Tensor, stream=None) -> None:
+    """Second half: bucket b's keys (stable) to the device array at dst_ptrs[b] (int64 device
+    pointers, e.g. peer receive buffers) from element dst_base[b] on."""
+    k = keys.reshape(-1)
+    _check(lib().dmm_multisplit_scatter_to(k.data_ptr(), k.numel(), shift, nbuckets, dst_ptrs.data_ptr(),
+                                           dst_base.data_ptr(), workspace.data_ptr(), _stream(stream)),
+           "multisplit_scatter_to")
+
+
 def version() -> str:
     return lib().dmm_version().decode()
 

@@ -39,3 +39,47 @@ def test_global_partition_single_rank():
     out, counts = global_partition(keys)
     h = dmm.as_uint32(out)
     assert (np.diff((h >> 29).astype(np.int64)) >= 0).all() and sum(counts) == 1 << 18
+
+
+def test_fused_p2p_single_rank_matches_nccl_path():
+    from paper_1507_01391_b200.distributed import PeerBuffers, global_partition_p2p
+    keys = dmm.gen_keys(11, (1 << 22) + 5)
+    ref, _ = global_partition(keys)
+    peers = PeerBuffers(keys.numel())
+    got, counts = global_partition_p2p(keys, peers)
+    assert torch.equal(got, ref)
+    assert int(counts.sum()) == keys.numel()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_fused_scatter_simulated_ranks(world):
+    # `world` ranks' fused scatters on one GPU into `world` receive buffers: the kernel and the
+    # destination arithmetic give the all-to-all's (source rank, source index) order per owner
+    from paper_1507_01391_b200.distributed import bucket_owner, p2p_destinations, recv_counts
+    nb, shift = 8, 29
+    keys = [dmm.gen_keys(1000 * s, 300000 + 1234 * s) for s in range(world)]
+    wss, starts = [], []
+    for k in keys:
+        ws = torch.empty(int(dmm.lib().dmm_multisplit_workspace_bytes(k.numel(), nb)), dtype=torch.uint8,
+                         device="cuda")
+        st = torch.empty(nb, dtype=torch.int64, device="cuda")
+        dmm.multisplit_count(k, nb, shift, st, ws)
+        wss.append(ws)
+        starts.append(st)
+    all_counts = torch.stack([torch.cat([st[1:], torch.tensor([k.numel()], device="cuda")]) - st
+                              for st, k in zip(starts, keys)])
+    recv = recv_counts(all_counts).tolist()
+    bufs = [torch.full((recv[r],), -1, dtype=torch.int32, device="cuda") for r in range(world)]
+    owner = [bucket_owner(b, nb, world) for b in range(nb)]
+    for s in range(world):
+        ptrs = torch.tensor([bufs[owner[b]].data_ptr() for b in range(nb)], dtype=torch.int64, device="cuda")
+        dmm.multisplit_scatter_to(keys[s], nb, shift, ptrs, p2p_destinations(all_counts, s), wss[s])
+    torch.cuda.synchronize()
+    for r in range(world):
+        exp = []
+        for k in keys:
+            h = dmm.as_uint32(k)
+            lab = h >> shift
+            loc = h[np.argsort(lab, kind="stable")]
+            exp.append(loc[np.isin(loc >> shift, [b for b in range(nb) if owner[b] == r])])
+        assert (dmm.as_uint32(bufs[r]) == np.concatenate(exp)).all()
