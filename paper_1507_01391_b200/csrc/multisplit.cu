@@ -12,8 +12,10 @@
 //      a key's destination is offset[bucket][tile] + keys of its bucket in earlier rows + keys
 //      of its bucket in lower lanes of this row (a warp prefix scan of byte-packed counters),
 //      i.e. stable by source index, and a warp store writes at most nbuckets contiguous runs.
-// The cross-GPU exchange (bucket j -> rank owning j) is an NCCL all-to-all in
-// paper_1507_01391_b200/distributed.py.
+// The cross-GPU exchange (bucket j -> rank owning j) is either fused into pass 3
+// (dmm_multisplit_count + dmm_multisplit_scatter_to: k_ms_scatter<LB, true> stores each key
+// straight into its owner's receive buffer, peer memory over NVLink) or an NCCL all-to-all
+// after dmm_multisplit (paper_1507_01391_b200/distributed.py).
 #include "capi_common.h"
 
 namespace dmmdev {
