@@ -20,7 +20,8 @@
 // host code after the call sees the same stream as with the reference.
 //
 // Not reproduced (GPU kernels have no DMM step meter): Machine::steps()/work() do not
-// advance; PartitionProbe hooks are replayed from the kernel's snapshots (the caller's
+// advance (run_algorithm reports the modelled count for the data-independent algorithms,
+// dmm_modelled_steps); PartitionProbe hooks are replayed from the kernel's snapshots (the caller's
 // machine holds the reference's window at each call), ShortWideHook calls likewise; traces
 // are unsupported (TraceIncomplete); permute() reproduces
 // the output region, the report and the Rng position, not the scratch/counter cells.
@@ -433,7 +434,8 @@ inline PermuteReport permute(Machine& mach, Rng& rng, const PermuteParams& param
 /// RunOutcome run_algorithm(Algorithm, const Instance&, const RunOptions&)  instance.hpp:277-363
 /// The dispatcher the reference's CLI and acceptance harness use, over the B200 kernels: the
 /// same instance checks, views, verification and report fields.  The GPU has no DMM step
-/// meter: report.steps / work stay 0 and conflicts counts the model's violations (0: every
+/// meter: report.steps / work are the reference's counts for the data-independent algorithms
+/// (dmm_modelled_steps) and 0 otherwise; conflicts counts the model's violations (0: every
 /// kernel relayout is checked conflict-free at compile time); record_trace throws
 /// TraceIncomplete.
 inline RunOutcome run_algorithm(Algorithm alg, const Instance& in, const RunOptions& opt = {}) {
@@ -508,8 +510,9 @@ inline RunOutcome run_algorithm(Algorithm alg, const Instance& in, const RunOpti
             break;
         }
     }
-    out.report.steps = 0;
-    out.report.work = 0;
+    // the reference's Machine::steps() where it does not depend on the data (0 otherwise)
+    out.report.steps = dmm_modelled_steps(algorithm_name(alg), in.w, in.m);
+    out.report.work = out.report.steps * in.w;
     out.report.conflicts = 0;
     return out;
 }

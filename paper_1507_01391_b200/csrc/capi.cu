@@ -59,4 +59,18 @@ int dmm_supported(const char* algorithm, uint32_t w, uint32_t m) {
     return 0;
 }
 
+uint64_t dmm_modelled_steps(const char* algorithm, uint32_t w, uint32_t m) {
+    if (!algorithm || w < 2 || m < 1)
+        return 0;
+    const std::string a(algorithm);
+    if (a == "partition_short_wide" && uint64_t(w) * w <= m)
+        return 76ull * m;  // radix rows: hist 1m + count 3m + prefix 2m + scatter 4m + copy-back 2m
+    if (a == "partition_square" && w == m) {
+        const uint32_t h = dmmhost::isqrt_floor(m);
+        if (h * h == m)
+            return 196ull * m - 8;
+    }
+    return 0;
+}
+
 }  // extern "C"

@@ -16,7 +16,8 @@ reference's independent verifiers (instance.hpp:236-273) and runs on the device.
 Differences from the reference, by construction: words are 32-bit on the device (a loaded
 instance holding a word >= 2^32 raises KeyOutOfRange); ``gen_instance("sort", ...)`` emits
 the uint32 sort tile of include/dmm_gpu.h (the reference's sort kind draws 64-bit words);
-``RunReport.steps`` / ``work`` are 0 (the kernels have no DMM step meter) and
+``RunReport.steps`` / ``work`` are the reference's exact counts for the data-independent
+algorithms (``modelled_steps``) and 0 otherwise (the kernels have no DMM step meter);
 ``record_trace=True`` raises TraceIncomplete.
 """
 from __future__ import annotations
@@ -197,6 +198,13 @@ class RunOutcome:
     result: np.ndarray | None = None
 
 
+def modelled_steps(alg: str, w: int, m: int) -> int:
+    """Machine::steps() of one run of a data-independent algorithm (dmm_modelled_steps:
+    partition_short_wide 76 m, partition_square 196 m - 8); 0 where the reference's count
+    depends on the data (merge row sorts, cleanup retries, the permutation's iterations)."""
+    return int(dmm.lib().dmm_modelled_steps(alg.encode(), w, m))
+
+
 def run_algorithms(alg: str, instances: list[Instance], *, strict: bool = True, alpha: int = 4,
                    seeds=None, record_trace: bool = False) -> list[RunOutcome]:
     """run_algorithm (instance.hpp:283-363) over a batch of same-shape instances in one launch.
@@ -262,11 +270,12 @@ def run_algorithms(alg: str, instances: list[Instance], *, strict: bool = True, 
         ids = torch.arange(w * m, device=o.device, dtype=torch.int64).view(1, w, m)
         ok = (o == ids).all(dim=2).all(dim=1)
     ok = ok.cpu().tolist()
+    steps = modelled_steps(alg, w, m)
     res = o.cpu().numpy().astype(np.uint64)
     outs = []
     for k in range(count):
-        rep = RunReport(algorithm=alg, w=w, m=m, seed=seeds[k], correct=bool(ok[k]), iterations=int(iters[k]),
-                        fallback=bool(fallback[k]), cleanup_retries=int(retries[k]))
+        rep = RunReport(algorithm=alg, w=w, m=m, seed=seeds[k], steps=steps, work=steps * w, correct=bool(ok[k]),
+                        iterations=int(iters[k]), fallback=bool(fallback[k]), cleanup_retries=int(retries[k]))
         outs.append(RunOutcome(rep, pipeline[k], res[k]))
     return outs
 

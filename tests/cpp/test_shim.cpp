@@ -321,6 +321,8 @@ static void run_algorithm_cases() {
             CHECK(ra.report.algorithm == rb.report.algorithm && ra.report.seed == rb.report.seed);
             CHECK(ra.report.cleanup_retries == rb.report.cleanup_retries);
             CHECK(ra.report.iterations == rb.report.iterations && ra.report.fallback == rb.report.fallback);
+            if (c.a == Algorithm::partition_square || c.a == Algorithm::partition_short_wide)  // modelled meters
+                CHECK(ra.report.steps == rb.report.steps && ra.report.work == rb.report.work);
             if (c.a == Algorithm::permute) {
                 CHECK(ra.pipeline.random_words == rb.pipeline.random_words);
                 CHECK(ra.pipeline.leftover_history == rb.pipeline.leftover_history);

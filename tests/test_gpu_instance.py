@@ -44,6 +44,8 @@ def test_run_algorithm_matches_reference(ref, alg, w, m):
         assert (rep.iterations, rep.fallback, rep.cleanup_retries) == \
             (rr["iterations"], rr["fallback"], rr["cleanup_retries"])
         assert rep.conflicts == rr["conflicts"] == 0
+        if I.modelled_steps(alg, w, m):  # data-independent meters are reproduced exactly
+            assert (rep.steps, rep.work) == (rr["steps"], rr["steps"] * w)
         assert (out.result == ref_grid).all()
         if alg == "permute":
             assert out.pipeline == rr["pipeline"]

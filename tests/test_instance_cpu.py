@@ -100,3 +100,26 @@ def test_run_algorithm_host_checks(ref):
     with pytest.raises(ValueError):
         I.run_algorithm("quicksort", _inst(ref, "sort", 4, 16, 2))
     assert [I.instance_kind_for(a) for a in I.ALGORITHMS] == ["sort"] * 3 + ["partition"] * 3 + ["permute"] * 2
+
+
+@pytest.mark.parametrize("alg,shapes", [
+    ("partition_short_wide", [(2, 4), (2, 8), (3, 9), (4, 16), (8, 64), (2, 5), (5, 25), (32, 1024)]),
+    ("partition_square", [(4, 4), (16, 16), (64, 64)]),
+])
+def test_modelled_steps_match_reference(ref, alg, shapes):
+    # Machine::steps() of the data-independent algorithms (test_partition.cpp:92-108 pins 684
+    # for partition_short_wide 3 x 9): the closed forms equal the reference's meter
+    from oracle.oracle import ALGORITHMS as REF_ALG
+    for w, m in shapes:
+        for seed in (1, 2):
+            s, _, rr = ref.run_algorithm(REF_ALG[alg], ref.gen_instance(1, w, m, seed), seed)
+            assert s == 0 and I.modelled_steps(alg, w, m) == rr["steps"]
+    assert I.modelled_steps("partition_short_wide", 3, 9) == 684
+
+
+def test_unmodelled_steps_are_zero():
+    for alg in ("partition_general", "integer_sort_general", "permute", "sort_tall", "sort_square",
+                "sort_short_wide"):
+        assert I.modelled_steps(alg, 32, 32) == 0
+    assert I.modelled_steps("partition_square", 32, 32) == 0  # not a perfect square
+    assert I.modelled_steps("partition_short_wide", 32, 32) == 0  # w^2 > m
