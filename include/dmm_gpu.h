@@ -63,11 +63,11 @@ const char* dmm_last_error(void);
 int dmm_supported(const char* algorithm, uint32_t w, uint32_t m);
 /* Number of kernel launches the last call on this thread issued (for bench accounting). */
 uint32_t dmm_last_launch_count(void);
-/* Machine::steps() the reference meters for one run of a data-independent algorithm on a w x m
- * instance (instance.hpp:357): partition_short_wide 76 m (5 radix row sorts of 12 m accesses +
- * 4 conversions of 4 m, w^2 <= m), partition_square 196 m - 8 (w = m a perfect square).
- * 0 = not modelled (the step count of the other algorithms depends on the data through their
- * merge row sorts and retries); work = steps * w. */
+/* Machine::steps() the reference meters for run_algorithm on a w x m instance
+ * (instance.hpp:357) where it does not depend on the data: the radix leaves of
+ * partition_short_wide, partition_square and of partition_general / integer_sort_general with
+ * w <= m (short-wide or square skeleton; closed forms in capi.cu).  0 = not modelled (merge
+ * segment sorts, cleanup retries and the permutation depend on the data); work = steps * w. */
 uint64_t dmm_modelled_steps(const char* algorithm, uint32_t w, uint32_t m);
 
 /* ---- instance generation -------------------------------------------------- */

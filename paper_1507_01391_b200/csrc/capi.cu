@@ -60,16 +60,43 @@ int dmm_supported(const char* algorithm, uint32_t w, uint32_t m) {
 }
 
 uint64_t dmm_modelled_steps(const char* algorithm, uint32_t w, uint32_t m) {
-    if (!algorithm || w < 2 || m < 1)
+    // The reference meters a bank-local section by its busiest row (core.hpp rows_lockstep);
+    // where every row does the same accesses the count is a closed form of the schedule:
+    //  * radix row sort of m keys < domain (partition.hpp:37-85), p = radix_pass_count(m,
+    //    domain) passes of 10 m accesses (histogram clear m, count 3 m, prefix 2 m, scatter
+    //    4 m) plus a 2 m copy-back when p is odd;
+    //  * to_column_major / to_row_major 4 m (layout.hpp:316-405); transpose_square 2 (s - 1);
+    //  * partition_leaf (partition.hpp:156-172): short-wide skeleton = 5 row sorts + 4
+    //    conversions (sort.hpp:200-218); square skeleton with w = m = h^2 = 13 row sorts
+    //    (two short-wide super-row passes, two transposed column sorts, the final pass)
+    //    + 8 conversions + 4 transposes (sort.hpp:250-280).
+    // Shearsort leaves, blocked column sorts (merge segments), the recursion's cleanup retries
+    // and the permutation depend on the data: 0 (not modelled).
+    if (!algorithm || w < 2 || m < 2)
         return 0;
     const std::string a(algorithm);
-    if (a == "partition_short_wide" && uint64_t(w) * w <= m)
-        return 76ull * m;  // radix rows: hist 1m + count 3m + prefix 2m + scatter 4m + copy-back 2m
-    if (a == "partition_square" && w == m) {
+    auto radix = [&](uint64_t domain) -> uint64_t {
+        uint32_t p = 1;
+        for (uint64_t reach = m; reach < domain; reach *= m)
+            ++p;
+        return 10ull * m * p + ((p & 1) ? 2ull * m : 0);
+    };
+    auto leaf = [&](uint64_t domain) -> uint64_t {
+        if (uint64_t(w) * w <= m)
+            return 5 * radix(domain) + 4 * 4ull * m;
         const uint32_t h = dmmhost::isqrt_floor(m);
-        if (h * h == m)
-            return 196ull * m - 8;
-    }
+        if (w == m && h * h == m)
+            return 13 * radix(domain) + 8 * 4ull * m + 4 * 2ull * (m - 1);
+        return 0;
+    };
+    if (a == "partition_short_wide")
+        return uint64_t(w) * w <= m ? leaf(w) : 0;
+    if (a == "partition_square")
+        return w == m ? leaf(w) : 0;
+    if (a == "partition_general")
+        return w <= m ? leaf(w) : 0;
+    if (a == "integer_sort_general")
+        return w <= m ? leaf(uint64_t(w) * m) : 0;
     return 0;
 }
 

@@ -199,9 +199,10 @@ class RunOutcome:
 
 
 def modelled_steps(alg: str, w: int, m: int) -> int:
-    """Machine::steps() of one run of a data-independent algorithm (dmm_modelled_steps:
-    partition_short_wide 76 m, partition_square 196 m - 8); 0 where the reference's count
-    depends on the data (merge row sorts, cleanup retries, the permutation's iterations)."""
+    """Machine::steps() of one run where the reference's count does not depend on the data
+    (dmm_modelled_steps: radix leaves -- partition_short_wide, partition_square, and
+    partition_general / integer_sort_general with w <= m on short-wide or square shapes);
+    0 otherwise (merge segment sorts, cleanup retries, the permutation's iterations)."""
     return int(dmm.lib().dmm_modelled_steps(alg.encode(), w, m))
 
 

@@ -104,7 +104,9 @@ def test_run_algorithm_host_checks(ref):
 
 @pytest.mark.parametrize("alg,shapes", [
     ("partition_short_wide", [(2, 4), (2, 8), (3, 9), (4, 16), (8, 64), (2, 5), (5, 25), (32, 1024)]),
-    ("partition_square", [(4, 4), (16, 16), (64, 64)]),
+    ("partition_square", [(4, 4), (9, 9), (16, 16), (25, 25), (64, 64)]),
+    ("partition_general", [(2, 4), (3, 9), (4, 16), (8, 64), (4, 4), (16, 16), (64, 64), (16, 256)]),
+    ("integer_sort_general", [(2, 4), (3, 9), (4, 32), (8, 64), (4, 4), (16, 16), (64, 64)]),
 ])
 def test_modelled_steps_match_reference(ref, alg, shapes):
     # Machine::steps() of the data-independent algorithms (test_partition.cpp:92-108 pins 684
@@ -112,14 +114,19 @@ def test_modelled_steps_match_reference(ref, alg, shapes):
     from oracle.oracle import ALGORITHMS as REF_ALG
     for w, m in shapes:
         for seed in (1, 2):
-            s, _, rr = ref.run_algorithm(REF_ALG[alg], ref.gen_instance(1, w, m, seed), seed)
+            kind = 2 if alg == "integer_sort_general" else 1
+            s, _, rr = ref.run_algorithm(REF_ALG[alg], ref.gen_instance(kind, w, m, seed), seed)
             assert s == 0 and I.modelled_steps(alg, w, m) == rr["steps"]
     assert I.modelled_steps("partition_short_wide", 3, 9) == 684
 
 
 def test_unmodelled_steps_are_zero():
+    # shearsort leaves (32 x 32), blocked merges (32 x 64), the recursion (32 x 16), comparison
+    # sorts and the permutation depend on the data
     for alg in ("partition_general", "integer_sort_general", "permute", "sort_tall", "sort_square",
                 "sort_short_wide"):
         assert I.modelled_steps(alg, 32, 32) == 0
+    assert I.modelled_steps("partition_general", 32, 64) == 0
+    assert I.modelled_steps("partition_general", 32, 16) == 0
     assert I.modelled_steps("partition_square", 32, 32) == 0  # not a perfect square
     assert I.modelled_steps("partition_short_wide", 32, 32) == 0  # w^2 > m
