@@ -69,6 +69,13 @@ uint32_t dmm_last_launch_count(void);
  * w <= m (short-wide or square skeleton; closed forms in capi.cu).  0 = not modelled (merge
  * segment sorts, cleanup retries and the permutation depend on the data); work = steps * w. */
 uint64_t dmm_modelled_steps(const char* algorithm, uint32_t w, uint32_t m);
+/* The same meter for the data-dependent leaves of partition_general / integer_sort_general with
+ * w <= m (shearsort_rect sort.hpp:288, square skeleton with w < m sort.hpp:250: their blocked
+ * column sorts merge-sort bank segments): steps[k] for input instance k (device [count][w][m],
+ * keys < domain; domain = w for the partition, w*m for run_algorithm's integer sort).  A
+ * replay of the leaf's states on the device (off the hot path); 2 <= w <= 32, m <= 128. */
+dmm_status dmm_leaf_steps(const uint32_t* in, uint32_t w, uint32_t m, uint64_t count, uint64_t domain,
+                          uint64_t* steps, void* stream);
 
 /* ---- instance generation -------------------------------------------------- */
 /* Instance gen_instance(kind, w, m, seed)                        instance.hpp:48-76

@@ -16,8 +16,10 @@ reference's independent verifiers (instance.hpp:236-273) and runs on the device.
 Differences from the reference, by construction: words are 32-bit on the device (a loaded
 instance holding a word >= 2^32 raises KeyOutOfRange); ``gen_instance("sort", ...)`` emits
 the uint32 sort tile of include/dmm_gpu.h (the reference's sort kind draws 64-bit words);
-``RunReport.steps`` / ``work`` are the reference's exact counts for the data-independent
-algorithms (``modelled_steps``) and 0 otherwise (the kernels have no DMM step meter);
+``RunReport.steps`` / ``work`` are the reference's exact counts where the schedule is
+data-independent (``modelled_steps``) and for the w <= m leaves of the general partition /
+integer sort (``leaf_steps``, replayed on the device); 0 otherwise (the recursion with w > m,
+the comparison sorts and the permutation);
 ``record_trace=True`` raises TraceIncomplete.
 """
 from __future__ import annotations
@@ -206,6 +208,26 @@ def modelled_steps(alg: str, w: int, m: int) -> int:
     return int(dmm.lib().dmm_modelled_steps(alg.encode(), w, m))
 
 
+def leaf_metered(w: int, m: int) -> bool:
+    """dmm_leaf_steps meters this w <= m leaf (shearsort, or square skeleton with w < m)."""
+    if not (2 <= w <= 32 and m <= 128 and w <= m) or w * w <= m:
+        return False
+    h = int(round(m ** 0.5))
+    if h * h == m:
+        return w < m and w % h == 0
+    return m % w == 0
+
+
+def leaf_steps(grid: torch.Tensor, domain: int) -> torch.Tensor:
+    """Machine::steps() of the general partition / integer sort leaf (w <= m) for each input
+    instance of ``grid`` ([count, w, m] device), replayed on the device (dmm_leaf_steps)."""
+    count, w, m = grid.shape
+    out = torch.empty(count, dtype=torch.int64, device=grid.device)
+    dmm._check(dmm.lib().dmm_leaf_steps(grid.data_ptr(), w, m, count, domain, out.data_ptr(),
+                                        dmm._stream(None)), "leaf_steps")
+    return out
+
+
 def run_algorithms(alg: str, instances: list[Instance], *, strict: bool = True, alpha: int = 4,
                    seeds=None, record_trace: bool = False) -> list[RunOutcome]:
     """run_algorithm (instance.hpp:283-363) over a batch of same-shape instances in one launch.
@@ -271,11 +293,14 @@ def run_algorithms(alg: str, instances: list[Instance], *, strict: bool = True, 
         ids = torch.arange(w * m, device=o.device, dtype=torch.int64).view(1, w, m)
         ok = (o == ids).all(dim=2).all(dim=1)
     ok = ok.cpu().tolist()
-    steps = modelled_steps(alg, w, m)
+    steps = [modelled_steps(alg, w, m)] * count
+    if steps[0] == 0 and alg in ("partition_general", "integer_sort_general") and leaf_metered(w, m):
+        steps = leaf_steps(grid, w if alg == "partition_general" else w * m).cpu().tolist()
     res = o.cpu().numpy().astype(np.uint64)
     outs = []
     for k in range(count):
-        rep = RunReport(algorithm=alg, w=w, m=m, seed=seeds[k], steps=steps, work=steps * w, correct=bool(ok[k]),
+        rep = RunReport(algorithm=alg, w=w, m=m, seed=seeds[k], steps=int(steps[k]), work=int(steps[k]) * w,
+                        correct=bool(ok[k]),
                         iterations=int(iters[k]), fallback=bool(fallback[k]), cleanup_retries=int(retries[k]))
         outs.append(RunOutcome(rep, pipeline[k], res[k]))
     return outs

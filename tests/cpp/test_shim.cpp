@@ -308,7 +308,8 @@ static void run_algorithm_cases() {
                           {Algorithm::integer_sort_general, 32, 32}, {Algorithm::partition_square, 16, 16},
                           {Algorithm::partition_short_wide, 8, 64}, {Algorithm::partition_short_wide, 3, 9},
                           {Algorithm::sort_square, 16, 16}, {Algorithm::partition_general, 16, 16},
-                          {Algorithm::integer_sort_general, 8, 64},
+                          {Algorithm::integer_sort_general, 8, 64}, {Algorithm::partition_general, 32, 32},
+                          {Algorithm::partition_general, 32, 64}, {Algorithm::integer_sort_general, 32, 128},
                           {Algorithm::sort_short_wide, 4, 16}, {Algorithm::sort_tall, 128, 32},
                           {Algorithm::permute, 32, 32}, {Algorithm::permute, 128, 64}};
     for (const Case& c : cases) {
@@ -322,7 +323,9 @@ static void run_algorithm_cases() {
             CHECK(ra.report.algorithm == rb.report.algorithm && ra.report.seed == rb.report.seed);
             CHECK(ra.report.cleanup_retries == rb.report.cleanup_retries);
             CHECK(ra.report.iterations == rb.report.iterations && ra.report.fallback == rb.report.fallback);
-            if (dmm_modelled_steps(algorithm_name(c.a), c.w, c.m))  // data-independent meters
+            if (dmm_modelled_steps(algorithm_name(c.a), c.w, c.m) ||
+                ((c.a == Algorithm::partition_general || c.a == Algorithm::integer_sort_general) && c.w <= c.m))
+                // modelled / replayed meters
                 CHECK(ra.report.steps == rb.report.steps && ra.report.work == rb.report.work);
             if (c.a == Algorithm::permute) {
                 CHECK(ra.pipeline.random_words == rb.pipeline.random_words);

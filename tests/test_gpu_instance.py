@@ -1,8 +1,10 @@
 """run_algorithm over the B200 kernels (paper_1507_01391_b200/instance.py) against the
 reference's own run_algorithm (instance.hpp:283-363, oracle/_ref) on the same instances:
-every report field except the step meter, the permute pipeline report, and the final grid.
+every report field (the step meter where it is modelled or replayed), the permute pipeline
+report, and the final grid.
 Also the reference harness's run_algorithm cases (tests/test_harness.cpp:54-83)."""
 import numpy as np
+import torch
 import pytest
 
 import paper_1507_01391_b200 as dmm
@@ -44,8 +46,12 @@ def test_run_algorithm_matches_reference(ref, alg, w, m):
         assert (rep.iterations, rep.fallback, rep.cleanup_retries) == \
             (rr["iterations"], rr["fallback"], rr["cleanup_retries"])
         assert rep.conflicts == rr["conflicts"] == 0
-        if I.modelled_steps(alg, w, m):  # data-independent meters are reproduced exactly
+        metered = I.modelled_steps(alg, w, m) or (alg in ("partition_general", "integer_sort_general")
+                                                 and I.leaf_metered(w, m))
+        if metered:  # the reference's meter, reproduced exactly
             assert (rep.steps, rep.work) == (rr["steps"], rr["steps"] * w)
+        else:
+            assert rep.steps == 0
         assert (out.result == ref_grid).all()
         if alg == "permute":
             assert out.pipeline == rr["pipeline"]
@@ -85,3 +91,18 @@ def test_wide_words_rejected():
     inst = I.Instance("sort", 4, 16, 0, np.full(64, 1 << 40, dtype=np.uint64))
     with pytest.raises(dmm.KeyOutOfRange):
         I.run_algorithm("sort_short_wide", inst)
+
+
+@pytest.mark.parametrize("alg,w,m", [("partition_general", 32, 32), ("integer_sort_general", 32, 32),
+                                     ("partition_general", 32, 64), ("integer_sort_general", 32, 128),
+                                     ("partition_general", 16, 32), ("partition_general", 8, 16),
+                                     ("partition_general", 8, 8), ("integer_sort_general", 16, 64)])
+def test_leaf_steps_match_reference(ref, alg, w, m):
+    # data-dependent meter of the w <= m leaf (merge segment sorts), replayed on the device,
+    # against the reference's Machine::steps() instance by instance
+    kind = 1 if alg == "partition_general" else 2
+    insts = np.stack([ref.gen_instance(kind, w, m, seed) for seed in range(1, 25)]).astype(np.uint32)
+    got = I.leaf_steps(torch.from_numpy(insts.view(np.int32)).cuda(), w if kind == 1 else w * m).cpu().tolist()
+    exp = [ref.run_algorithm(REF_ALG[alg], insts[k].astype(np.uint64), k + 1)[2]["steps"] for k in range(len(insts))]
+    assert got == exp
+    assert len(set(exp)) > 1 or (w, m) == (16, 64)  # genuinely data-dependent
