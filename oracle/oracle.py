@@ -220,6 +220,10 @@ class Ref:
                                             C.c_uint64]
         L.dmmr_instance_to_text.restype = C.c_uint64
         L.dmmr_instance_from_text.argtypes = [C.c_char_p, u64p, u64p, C.c_uint64]
+        L.dmmr_trace_text.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, C.c_char_p, C.c_uint64]
+        L.dmmr_trace_text.restype = C.c_uint64
+        L.dmmr_verify_trace_text.argtypes = [C.c_char_p]
+        L.dmmr_verify_trace_text.restype = C.c_int64
         L.dmmr_offline_schedule.argtypes = [C.c_uint32, C.c_uint32, u32p, u32p, u32p, u32p]
         L.dmmr_schedule_to_text.argtypes = [u32p, u32p, C.c_uint32, C.c_char_p, C.c_uint64]
         L.dmmr_schedule_to_text.restype = C.c_uint64
@@ -252,6 +256,15 @@ class Ref:
             rounds.append([tuple(int(x) for x in moves[4 * j: 4 * j + 4]) for j in range(k, k + int(lens[r]))])
             k += int(lens[r])
         return s, rounds
+
+    def trace_text(self, alg: int, w: int, m: int, seed: int) -> str:
+        n = self.lib.dmmr_trace_text(alg, w, m, seed, None, 0)
+        buf = C.create_string_buffer(max(n, 1))
+        self.lib.dmmr_trace_text(alg, w, m, seed, buf, n)
+        return buf.raw[:n].decode()
+
+    def verify_trace_text(self, text: str) -> int:
+        return int(self.lib.dmmr_verify_trace_text(text.encode()))
 
     def schedule_to_text(self, rounds) -> str:
         mv = np.array([x for r in rounds for x in r], dtype=np.uint32).reshape(-1)

@@ -430,4 +430,32 @@ uint64_t dmmr_schedule_to_text(const uint32_t* moves, const uint32_t* round_len,
     return t.size();
 }
 
+// trace_to_text (instance.hpp:369-382) of run_algorithm(alg, gen_instance(kind_for(alg), w, m,
+// seed), record_trace); returns the full length, copies up to cap bytes.
+uint64_t dmmr_trace_text(int alg, uint32_t w, uint32_t m, uint64_t seed, char* buf, uint64_t cap) {
+    try {
+        RunOptions opt;
+        opt.record_trace = true;
+        const Algorithm a = alg_of(alg);
+        RunOutcome out = run_algorithm(a, gen_instance(instance_kind_for(a), w, m, seed), opt);
+        const std::string t = trace_to_text(out.trace);
+        if (buf && cap)
+            std::memcpy(buf, t.data(), std::min<uint64_t>(cap, t.size()));
+        return t.size();
+    } catch (...) {
+        return 0;
+    }
+}
+
+// verify_trace (core.hpp:221-237) of a parsed trace text: number of (step, bank) violations,
+// or -1 if the text does not parse
+int64_t dmmr_verify_trace_text(const char* text) {
+    try {
+        std::istringstream is(text);
+        return int64_t(verify_trace(trace_from_text(is)).size());
+    } catch (...) {
+        return -1;
+    }
+}
+
 }  // extern "C"

@@ -18,3 +18,4 @@ from .instance import (  # noqa: F401,E402
 from . import schedule  # noqa: F401,E402  (layout.hpp offline schedules)
 from .schedule import (  # noqa: F401,E402
     DeviceSchedule, Move, Schedule, apply_schedule, offline_schedule, schedule_from_text, schedule_to_text)
+from . import trace  # noqa: F401,E402  (reference trace files: text format + offline audit)
