@@ -524,6 +524,18 @@ inline RunOutcome run_algorithm(Algorithm alg, const Instance& in, const RunOpti
             to_host(st, ds);
             out.report.steps = st[0];
         }
+    } else if (alg == Algorithm::sort_short_wide || alg == Algorithm::sort_square) {
+        std::vector<uint32_t> g(in.grid.size());
+        for (std::size_t i = 0; i < g.size(); ++i)
+            g[i] = static_cast<uint32_t>(in.grid[i]);  // 32-bit (checked by the sort above)
+        DeviceBuffer dg(sizeof(uint32_t) * g.size()), ds(sizeof(uint64_t));
+        to_device(dg, g);
+        if (dmm_sort_steps(algorithm_name(alg), dg.as<uint32_t>(), in.w, in.m, 1, ds.as<uint64_t>(), nullptr) ==
+            DMM_OK) {
+            std::vector<uint64_t> st(1);
+            to_host(st, ds);
+            out.report.steps = st[0];
+        }
     }
     out.report.work = out.report.steps * in.w;
     out.report.conflicts = 0;

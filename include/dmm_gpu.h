@@ -76,6 +76,10 @@ uint64_t dmm_modelled_steps(const char* algorithm, uint32_t w, uint32_t m);
  * replay of the leaf's states on the device (off the hot path); 2 <= w <= 32, m <= 128. */
 dmm_status dmm_leaf_steps(const uint32_t* in, uint32_t w, uint32_t m, uint64_t count, uint64_t domain,
                           uint64_t* steps, void* stream);
+/* The same meter for the comparison sorts sort_short_wide (sort.hpp:225, w^2 <= m <= 64) and
+ * sort_square (sort.hpp:337, w = m = h^2 <= 64): every row sort merge-sorts its banks. */
+dmm_status dmm_sort_steps(const char* algorithm, const uint32_t* in, uint32_t w, uint32_t m, uint64_t count,
+                          uint64_t* steps, void* stream);
 
 /* ---- instance generation -------------------------------------------------- */
 /* Instance gen_instance(kind, w, m, seed)                        instance.hpp:48-76

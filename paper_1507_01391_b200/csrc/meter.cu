@@ -1,6 +1,6 @@
-// meter.cu -- the reference's DMM step count (Machine::steps(), core.hpp rows_lockstep) for the
-// leaf of the general partition / integer sort, w <= m (partition.hpp:156-172), where it depends
-// on the data.
+// meter.cu -- the reference's DMM step count (Machine::steps(), core.hpp rows_lockstep) where it
+// depends on the data: the leaf of the general partition / integer sort, w <= m
+// (partition.hpp:156-172), and the comparison sorts sort_short_wide / sort_square (below).
 //
 // The leaf's row sorts are radix sorts (shape-determined access counts) and its transposes and
 // conversions are fixed, but its blocked column sorts run merge_sort_segments (sort.hpp:44-70,
@@ -18,6 +18,8 @@
 //
 // Metering is off the hot path: one warp per instance, the machine in shared memory, simple
 // insertion sorts.
+#include <string>
+
 #include "capi_common.h"
 
 namespace dmmdev {
@@ -147,6 +149,152 @@ __global__ void __launch_bounds__(32) k_leaf_steps(const uint32_t* __restrict__ 
         steps[k] = total;
 }
 
+// ---- comparison sorts: sort_short_wide (sort.hpp:225) and sort_square (sort.hpp:337) --------
+// Every row sort is sort_rows (row_merge_sort, data-dependent); conversions cost 4 m,
+// transposes 2 (m - 1).  The square skeleton's super-row groups run in merged lockstep, which
+// the reference meters as the longest group's own total (measured: the max over groups of the
+// per-group sums, not the sum of per-section maxima).
+
+constexpr int kSortMaxM = 64;
+
+// accesses of row_merge_sort (sort.hpp:44-70) on x[0..L), direction asc; sorts x in place
+__device__ uint32_t merge_row(uint32_t* x, uint32_t stride, uint32_t L, bool asc) {
+    uint32_t a[kSortMaxM], b[kSortMaxM];
+    for (uint32_t i = 0; i < L; ++i)
+        a[i] = x[i * stride];
+    uint32_t cost = 0, levels = 0;
+    for (uint32_t width = 1; width < L; width *= 2, ++levels) {
+        for (uint32_t lo = 0; lo < L; lo += 2 * width) {
+            const uint32_t mid = min(lo + width, L), hi = min(lo + 2 * width, L);
+            uint32_t i = lo, j = mid, o = lo;
+            while (i < mid && j < hi) {
+                const bool take_a = asc ? a[i] <= a[j] : a[i] >= a[j];
+                b[o++] = take_a ? a[i++] : a[j++];
+                cost += 3;
+            }
+            while (i < mid) {
+                b[o++] = a[i++];
+                cost += 2;
+            }
+            while (j < hi) {
+                b[o++] = a[j++];
+                cost += 2;
+            }
+        }
+        for (uint32_t i = 0; i < L; ++i)
+            a[i] = b[i];
+    }
+    if (levels & 1)
+        cost += 2 * L;
+    for (uint32_t i = 0; i < L; ++i)
+        x[i * stride] = a[i];
+    return cost;
+}
+
+// short-wide skeleton (sort.hpp:200-218) on the h-row group starting at row g0 of the machine
+// g (row stride m), direction dir; thread r = row g0 + lr; returns the group's total via red
+__device__ void short_wide_group(uint32_t* g, uint32_t* tmp, uint32_t m, uint32_t h, uint32_t grp, uint32_t lr,
+                                 bool active, bool dir, uint32_t* red, uint64_t* total) {
+    uint32_t* base = g + grp * h * m;
+    uint32_t* t = tmp + grp * h * m;
+    auto rows = [&](bool alternate) {
+        if (active)
+            red[grp] = 0;
+        __syncthreads();
+        if (active) {
+            const bool asc = alternate ? ((lr % 2 == 0) == dir) : dir;
+            atomicMax(&red[grp], merge_row(base + lr * m, 1, m, asc));
+        }
+        __syncthreads();
+        if (active && lr == 0)
+            total[grp] += red[grp];
+        __syncthreads();
+    };
+    auto convert = [&](bool to_col) {
+        // to_column_major: row-major index v -> cell (v mod h, v div h); to_row_major inverse
+        if (active)
+            for (uint32_t c = 0; c < m; ++c) {
+                const uint32_t v = lr * m + c;  // this thread moves its own row's cells
+                if (to_col)
+                    t[(v % h) * m + v / h] = base[v];
+                else
+                    t[v] = base[(v % h) * m + v / h];
+            }
+        __syncthreads();
+        if (active)
+            for (uint32_t c = 0; c < m; ++c)
+                base[lr * m + c] = t[lr * m + c];
+        if (active && lr == 0)
+            total[grp] += 4ull * m;
+        __syncthreads();
+    };
+    for (int pass = 0; pass < 2; ++pass) {
+        rows(true);
+        convert(true);
+        rows(false);
+        convert(false);
+    }
+    rows(false);
+}
+
+// kind 0: sort_short_wide (w^2 <= m, one group of w rows), 1: sort_square (w = m = h^2)
+__global__ void k_sort_steps(const uint32_t* __restrict__ in, uint32_t W, uint32_t M, int kind,
+                             uint64_t* __restrict__ steps) {
+    extern __shared__ uint32_t sm[];
+    __shared__ uint32_t red[64];
+    __shared__ uint64_t total[64];
+    uint32_t* g = sm;
+    uint32_t* tmp = sm + W * M;
+    const uint32_t r = threadIdx.x;
+    const bool row = r < W;
+    const uint64_t k = blockIdx.x;
+    for (uint32_t i = r; i < W * M; i += blockDim.x)
+        g[i] = in[k * W * M + i];
+    const uint32_t h = kind == 0 ? W : (uint32_t)sqrtf((float)M);
+    const uint32_t ngroups = W / h;
+    uint64_t acc = 0;
+    auto super_rows = [&](bool alternate) {
+        if (r < ngroups)
+            total[r] = 0;
+        __syncthreads();
+        const uint32_t grp = r / h, lr = r % h;
+        const bool dir = alternate ? (grp % 2 == 0) : true;
+        short_wide_group(g, tmp, M, h, grp, lr, row, dir, red, total);
+        if (r == 0) {
+            uint64_t mx = 0;
+            for (uint32_t q = 0; q < ngroups; ++q)
+                mx = total[q] > mx ? total[q] : mx;
+            acc += mx;
+        }
+        __syncthreads();
+    };
+    auto uniform_rows = [&](bool columns) {
+        // columns: after a transpose row r is column r; sorting column r in place and
+        // transposing back is the same state
+        if (r == 0)
+            red[0] = 0;
+        __syncthreads();
+        if (row)
+            atomicMax(&red[0], columns ? merge_row(g + r, M, W, true) : merge_row(g + r * M, 1, M, true));
+        __syncthreads();
+        if (r == 0)
+            acc += red[0] + (columns ? 4ull * (M - 1) : 0);
+        __syncthreads();
+    };
+    __syncthreads();
+    if (kind == 0) {
+        super_rows(false);
+    } else {
+        super_rows(false);
+        uniform_rows(true);
+        super_rows(true);
+        uniform_rows(true);
+        uniform_rows(false);
+    }
+    if (r == 0)
+        steps[k] = acc;
+}
+
 }  // namespace dmmdev
 
 extern "C" {
@@ -172,6 +320,36 @@ dmm_status dmm_leaf_steps(const uint32_t* in, uint32_t w, uint32_t m, uint64_t c
     dmmdev::k_leaf_steps<<<unsigned(count), 32, smem, static_cast<cudaStream_t>(stream)>>>(in, w, m, count, domain,
                                                                                          steps);
     return dmmhost::check_launch("k_leaf_steps");
+}
+
+dmm_status dmm_sort_steps(const char* algorithm, const uint32_t* in, uint32_t w, uint32_t m, uint64_t count,
+                          uint64_t* steps, void* stream) {
+    dmmhost::reset_launches();
+    if (!algorithm)
+        return DMM_INVALID_ARGUMENT;
+    const std::string a(algorithm);
+    const uint32_t h = dmmhost::isqrt_floor(m);
+    int kind = -1;
+    if (a == "sort_short_wide" && w >= 2 && uint64_t(w) * w <= m && m <= dmmdev::kSortMaxM)
+        kind = 0;
+    else if (a == "sort_square" && w == m && h * h == m && w >= 2 && m <= dmmdev::kSortMaxM)
+        kind = 1;
+    if (kind < 0) {
+        dmmhost::set_error("sort metering: sort_short_wide (w^2 <= m <= 64) or sort_square (w = m = h^2 <= 64)");
+        return DMM_UNSUPPORTED_SHAPE;
+    }
+    if (count == 0)
+        return DMM_OK;
+    if (!in || !steps || count > 0x7FFFFFFFull)
+        return DMM_INVALID_ARGUMENT;
+    const unsigned threads = w <= 32 ? 32 : 64;
+    const size_t smem = 2 * sizeof(uint32_t) * w * m;
+    static std::atomic<uint64_t> configured{0};
+    if (dmm_status e = dmmhost::configure_kernel(dmmdev::k_sort_steps, smem, configured); e != DMM_OK)
+        return e;
+    dmmdev::k_sort_steps<<<unsigned(count), threads, smem, static_cast<cudaStream_t>(stream)>>>(in, w, m, kind,
+                                                                                              steps);
+    return dmmhost::check_launch("k_sort_steps");
 }
 
 }  // extern "C"

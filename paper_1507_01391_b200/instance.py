@@ -228,6 +228,24 @@ def leaf_steps(grid: torch.Tensor, domain: int) -> torch.Tensor:
     return out
 
 
+def sort_metered(alg: str, w: int, m: int) -> bool:
+    """dmm_sort_steps meters this comparison sort (sort_short_wide w^2 <= m <= 64,
+    sort_square w = m = h^2 <= 64)."""
+    h = int(round(m ** 0.5))
+    if alg == "sort_short_wide":
+        return w >= 2 and w * w <= m <= 64
+    return alg == "sort_square" and w == m and h * h == m and 2 <= m <= 64
+
+
+def sort_steps(alg: str, grid: torch.Tensor) -> torch.Tensor:
+    """Machine::steps() of sort_short_wide / sort_square for each input instance (device)."""
+    count, w, m = grid.shape
+    out = torch.empty(count, dtype=torch.int64, device=grid.device)
+    dmm._check(dmm.lib().dmm_sort_steps(alg.encode(), grid.data_ptr(), w, m, count, out.data_ptr(),
+                                        dmm._stream(None)), "sort_steps")
+    return out
+
+
 def run_algorithms(alg: str, instances: list[Instance], *, strict: bool = True, alpha: int = 4,
                    seeds=None, record_trace: bool = False) -> list[RunOutcome]:
     """run_algorithm (instance.hpp:283-363) over a batch of same-shape instances in one launch.
@@ -296,6 +314,8 @@ def run_algorithms(alg: str, instances: list[Instance], *, strict: bool = True, 
     steps = [modelled_steps(alg, w, m)] * count
     if steps[0] == 0 and alg in ("partition_general", "integer_sort_general") and leaf_metered(w, m):
         steps = leaf_steps(grid, w if alg == "partition_general" else w * m).cpu().tolist()
+    elif alg in ("sort_short_wide", "sort_square") and sort_metered(alg, w, m):
+        steps = sort_steps(alg, grid).cpu().tolist()
     res = o.cpu().numpy().astype(np.uint64)
     outs = []
     for k in range(count):

@@ -46,8 +46,8 @@ def test_run_algorithm_matches_reference(ref, alg, w, m):
         assert (rep.iterations, rep.fallback, rep.cleanup_retries) == \
             (rr["iterations"], rr["fallback"], rr["cleanup_retries"])
         assert rep.conflicts == rr["conflicts"] == 0
-        metered = I.modelled_steps(alg, w, m) or (alg in ("partition_general", "integer_sort_general")
-                                                 and I.leaf_metered(w, m))
+        metered = (I.modelled_steps(alg, w, m) or I.sort_metered(alg, w, m)
+                   or (alg in ("partition_general", "integer_sort_general") and I.leaf_metered(w, m)))
         if metered:  # the reference's meter, reproduced exactly
             assert (rep.steps, rep.work) == (rr["steps"], rr["steps"] * w)
         else:
@@ -106,3 +106,15 @@ def test_leaf_steps_match_reference(ref, alg, w, m):
     exp = [ref.run_algorithm(REF_ALG[alg], insts[k].astype(np.uint64), k + 1)[2]["steps"] for k in range(len(insts))]
     assert got == exp
     assert len(set(exp)) > 1 or (w, m) == (16, 64)  # genuinely data-dependent
+
+
+@pytest.mark.parametrize("alg,w,m", [("sort_short_wide", 2, 4), ("sort_short_wide", 4, 16),
+                                     ("sort_short_wide", 3, 9), ("sort_short_wide", 8, 64),
+                                     ("sort_square", 4, 4), ("sort_square", 16, 16), ("sort_square", 64, 64)])
+def test_sort_steps_match_reference(ref, alg, w, m):
+    # the comparison sorts' merge row sorts, replayed on the device (incl. the square skeleton's
+    # merged-lockstep groups), against the reference's Machine::steps() instance by instance
+    insts = np.stack([ref.gen_instance(0, w, m, seed) >> np.uint64(32) for seed in range(1, 17)]).astype(np.uint32)
+    got = I.sort_steps(alg, torch.from_numpy(insts.view(np.int32)).cuda()).cpu().tolist()
+    exp = [ref.run_algorithm(REF_ALG[alg], insts[k].astype(np.uint64), k + 1)[2]["steps"] for k in range(len(insts))]
+    assert got == exp
