@@ -524,7 +524,7 @@ inline RunOutcome run_algorithm(Algorithm alg, const Instance& in, const RunOpti
             to_host(st, ds);
             out.report.steps = st[0];
         }
-    } else if (alg == Algorithm::sort_short_wide || alg == Algorithm::sort_square) {
+    } else if (alg == Algorithm::sort_short_wide || alg == Algorithm::sort_square || alg == Algorithm::sort_tall) {
         std::vector<uint32_t> g(in.grid.size());
         for (std::size_t i = 0; i < g.size(); ++i)
             g[i] = static_cast<uint32_t>(in.grid[i]);  // 32-bit (checked by the sort above)

@@ -295,6 +295,189 @@ __global__ void k_sort_steps(const uint32_t* __restrict__ in, uint32_t W, uint32
         steps[k] = acc;
 }
 
+// ---- sort_tall (sort.hpp:352-374) -------------------------------------------------------------
+// merge row sort, Batcher column network (4 m per round, data-independent), to_row_major,
+// network, the m x m blocks' sort_wide_any in merged lockstep (metered as the longest block),
+// network, merge row sort.  A block's sort_wide_any is the square skeleton with merge rows
+// (m = h^2) or shearsort_rect with merge rows and segments; w = m is one block.
+
+constexpr int kTallMaxW = 128, kTallMaxM = 32;
+
+struct TallShared {
+    uint32_t umax[kTallMaxW];  // per-unit section maximum
+    uint64_t gtot[kTallMaxW];  // per-group totals (square skeleton super-rows)
+    uint64_t btot[kTallMaxW];  // per-block totals
+    uint64_t acc;
+};
+
+// one bank-local section: the unit's busiest row; `leader` rows add it to tot[unit]
+__device__ void tally(TallShared& S, uint64_t* tot, uint32_t unit, bool leader, uint32_t cost) {
+    atomicMax(&S.umax[unit], cost);
+    __syncthreads();
+    if (leader) {
+        tot[unit] += S.umax[unit];
+        S.umax[unit] = 0;
+    }
+    __syncthreads();
+}
+
+__device__ void convert_rows(uint32_t* base, uint32_t* tmp, uint32_t h, uint32_t m, uint32_t lr, bool to_col) {
+    for (uint32_t c = 0; c < m; ++c) {
+        const uint32_t v = lr * m + c;
+        if (to_col)
+            tmp[(v % h) * m + v / h] = base[v];
+        else
+            tmp[v] = base[(v % h) * m + v / h];
+    }
+    __syncthreads();
+    for (uint32_t c = 0; c < m; ++c)
+        base[lr * m + c] = tmp[lr * m + c];
+    __syncthreads();
+}
+
+__global__ void k_tall_steps(const uint32_t* __restrict__ in, uint32_t W, uint32_t M, uint64_t* __restrict__ steps) {
+    extern __shared__ uint32_t sm[];
+    __shared__ TallShared S;
+    uint32_t* g = sm;
+    uint32_t* tmp = sm + W * M;
+    const uint32_t r = threadIdx.x;  // row r (blockDim.x == W)
+    const uint64_t k = blockIdx.x;
+    for (uint32_t i = r; i < W * M; i += blockDim.x)
+        g[i] = in[k * W * M + i];
+    S.umax[r] = 0;
+    S.gtot[r] = 0;
+    S.btot[r] = 0;
+    if (r == 0)
+        S.acc = 0;
+    __syncthreads();
+    // whole-machine sections (unit 0)
+    auto machine_rows = [&]() {
+        tally(S, &S.acc, 0, r == 0, merge_row(g + r * M, 1, M, true));
+        S.acc += 0;
+    };
+    auto network = [&]() {
+        if (r < M)
+            insertion_sort(g + r, W, M, true);
+        __syncthreads();
+        if (r == 0) {
+            uint32_t rounds = 0;
+            for (uint32_t p = 1; p < W; p <<= 1)
+                for (uint32_t kk = p; kk >= 1; kk >>= 1) {
+                    bool any = false;
+                    for (uint32_t j = kk % p; j + kk < W && !any; j += 2 * kk)
+                        for (uint32_t i = 0; i < kk && i + j + kk < W; ++i)
+                            if ((i + j) / (2 * p) == (i + j + kk) / (2 * p)) {
+                                any = true;
+                                break;
+                            }
+                    rounds += any;
+                    if (kk == 1)
+                        break;
+                }
+            S.acc += 4ull * M * rounds;
+        }
+        __syncthreads();
+    };
+    const bool tall = W > M;
+    if (tall) {
+        machine_rows();
+        network();
+        // to_row_major of the w x m machine (layout.hpp:403): u = j w + i -> (u / m, u % m)
+        for (uint32_t c = 0; c < M; ++c) {
+            const uint32_t v = r * M + c;
+            tmp[v] = g[(v % W) * M + v / W];
+        }
+        __syncthreads();
+        for (uint32_t c = 0; c < M; ++c)
+            g[r * M + c] = tmp[r * M + c];
+        if (r == 0 && M > 1)
+            S.acc += 4ull * M;
+        __syncthreads();
+        network();
+    }
+    // the m x m blocks (one when w = m): sort_wide_any(block b, b even or w = m)
+    {
+        const uint32_t b = r / M, lr = r % M;
+        const bool d = !tall || b % 2 == 0;
+        uint32_t* blk = g + b * M * M;
+        uint32_t* tb = tmp + b * M * M;
+        const bool bl = lr == 0;
+        const uint32_t h = (uint32_t)sqrtf((float)M);
+        if (M == 1) {
+            // 1 x 1: nothing moves, conversions of a single row are free
+        } else if (h * h == M) {
+            // square skeleton (sort.hpp:250-280) with merge rows; groups of h rows in lockstep
+            const uint32_t q = lr / h, lq = lr % h;
+            const uint32_t gid = b * (M / h) + q;
+            uint32_t* gb = blk + q * h * M;
+            uint32_t* gt = tb + q * h * M;
+            for (int pass = 0; pass < 2; ++pass) {
+                const bool dir = pass == 0 ? d : ((q % 2 == 0) == d);
+                for (int sw = 0; sw < 2; ++sw) {
+                    tally(S, S.gtot, gid, lq == 0, merge_row(gb + lq * M, 1, M, (lq % 2 == 0) == dir));
+                    convert_rows(gb, gt, h, M, lq, true);
+                    tally(S, S.gtot, gid, lq == 0, merge_row(gb + lq * M, 1, M, dir));
+                    convert_rows(gb, gt, h, M, lq, false);
+                }
+                tally(S, S.gtot, gid, lq == 0, merge_row(gb + lq * M, 1, M, dir));
+                if (lq == 0)
+                    S.gtot[gid] += 4 * 4ull * M;
+                __syncthreads();
+                if (bl) {  // the block's super-rows: its longest group
+                    uint64_t mx = 0;
+                    for (uint32_t qq = 0; qq < M / h; ++qq)
+                        mx = max(mx, S.gtot[b * (M / h) + qq]);
+                    S.btot[b] += mx;
+                }
+                __syncthreads();
+                if (lq == 0)
+                    S.gtot[gid] = 0;
+                // columns of a square block: transpose, merge rows, transpose
+                tally(S, S.btot, b, bl, merge_row(blk + lr, M, M, d));
+                if (bl)
+                    S.btot[b] += 4ull * (M - 1);
+                __syncthreads();
+            }
+            tally(S, S.btot, b, bl, merge_row(blk + lr * M, 1, M, d));
+        } else {
+            // shearsort_rect (sort.hpp:288-311) with merge rows and merge segments
+            uint32_t rounds = 1;
+            while ((1u << (rounds - 1)) < M)
+                ++rounds;
+            for (uint32_t it = 0; it < rounds; ++it) {
+                tally(S, S.btot, b, bl, merge_row(blk + lr * M, 1, M, (lr % 2 == 0) == d));
+                tally(S, S.btot, b, bl, merge_row(blk + lr, M, M, d));  // the block's column lr
+                if (bl)
+                    S.btot[b] += 4ull * (M - 1);
+                __syncthreads();
+            }
+            tally(S, S.btot, b, bl, merge_row(blk + lr * M, 1, M, (lr % 2 == 0) == d));
+            if (((lr % 2 == 0) == d) != d)  // odd-row reversal into row-major order
+                for (uint32_t c = 0; c < M / 2; ++c) {
+                    const uint32_t t = blk[lr * M + c];
+                    blk[lr * M + c] = blk[lr * M + M - 1 - c];
+                    blk[lr * M + M - 1 - c] = t;
+                }
+            if (bl)
+                S.btot[b] += 4ull * (M / 2);
+            __syncthreads();
+        }
+        if (r == 0) {
+            uint64_t mx = 0;
+            for (uint32_t bb = 0; bb < W / M; ++bb)
+                mx = max(mx, S.btot[bb]);
+            S.acc += mx;
+        }
+        __syncthreads();
+    }
+    if (tall) {
+        network();
+        machine_rows();
+    }
+    if (r == 0)
+        steps[k] = S.acc;
+}
+
 }  // namespace dmmdev
 
 extern "C" {
@@ -334,16 +517,27 @@ dmm_status dmm_sort_steps(const char* algorithm, const uint32_t* in, uint32_t w,
         kind = 0;
     else if (a == "sort_square" && w == m && h * h == m && w >= 2 && m <= dmmdev::kSortMaxM)
         kind = 1;
+    else if (a == "sort_tall" && w >= m && m >= 1 && w % m == 0 && w <= dmmdev::kTallMaxW &&
+             m <= dmmdev::kTallMaxM && (w == 32 || w == 64 || w == 128 || w == m))
+        kind = 2;
     if (kind < 0) {
-        dmmhost::set_error("sort metering: sort_short_wide (w^2 <= m <= 64) or sort_square (w = m = h^2 <= 64)");
+        dmmhost::set_error("sort metering: sort_short_wide (w^2 <= m <= 64), sort_square (w = m = h^2 <= 64) or "
+                           "sort_tall (m | w, w in {32, 64, 128} or w = m <= 32)");
         return DMM_UNSUPPORTED_SHAPE;
     }
     if (count == 0)
         return DMM_OK;
     if (!in || !steps || count > 0x7FFFFFFFull)
         return DMM_INVALID_ARGUMENT;
-    const unsigned threads = w <= 32 ? 32 : 64;
     const size_t smem = 2 * sizeof(uint32_t) * w * m;
+    if (kind == 2) {
+        static std::atomic<uint64_t> tall_configured{0};
+        if (dmm_status e = dmmhost::configure_kernel(dmmdev::k_tall_steps, smem, tall_configured); e != DMM_OK)
+            return e;
+        dmmdev::k_tall_steps<<<unsigned(count), w, smem, static_cast<cudaStream_t>(stream)>>>(in, w, m, steps);
+        return dmmhost::check_launch("k_tall_steps");
+    }
+    const unsigned threads = w <= 32 ? 32 : 64;
     static std::atomic<uint64_t> configured{0};
     if (dmm_status e = dmmhost::configure_kernel(dmmdev::k_sort_steps, smem, configured); e != DMM_OK)
         return e;

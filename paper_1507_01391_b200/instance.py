@@ -17,9 +17,9 @@ Differences from the reference, by construction: words are 32-bit on the device 
 instance holding a word >= 2^32 raises KeyOutOfRange); ``gen_instance("sort", ...)`` emits
 the uint32 sort tile of include/dmm_gpu.h (the reference's sort kind draws 64-bit words);
 ``RunReport.steps`` / ``work`` are the reference's exact counts where the schedule is
-data-independent (``modelled_steps``) and for the w <= m leaves of the general partition /
-integer sort (``leaf_steps``, replayed on the device); 0 otherwise (the recursion with w > m,
-the comparison sorts and the permutation);
+data-independent (``modelled_steps``), for the w <= m leaves of the general partition /
+integer sort (``leaf_steps``) and for the comparison sorts (``sort_steps``), both replayed on
+the device; 0 otherwise (the recursion with w > m and the permutation);
 ``record_trace=True`` raises TraceIncomplete.
 """
 from __future__ import annotations
@@ -230,15 +230,17 @@ def leaf_steps(grid: torch.Tensor, domain: int) -> torch.Tensor:
 
 def sort_metered(alg: str, w: int, m: int) -> bool:
     """dmm_sort_steps meters this comparison sort (sort_short_wide w^2 <= m <= 64,
-    sort_square w = m = h^2 <= 64)."""
+    sort_square w = m = h^2 <= 64, sort_tall m | w with w in {32, 64, 128} or w = m <= 32)."""
     h = int(round(m ** 0.5))
     if alg == "sort_short_wide":
         return w >= 2 and w * w <= m <= 64
+    if alg == "sort_tall":
+        return m >= 1 and w >= m and w % m == 0 and m <= 32 and (w in (32, 64, 128) or w == m)
     return alg == "sort_square" and w == m and h * h == m and 2 <= m <= 64
 
 
 def sort_steps(alg: str, grid: torch.Tensor) -> torch.Tensor:
-    """Machine::steps() of sort_short_wide / sort_square for each input instance (device)."""
+    """Machine::steps() of sort_short_wide / sort_square / sort_tall for each input instance."""
     count, w, m = grid.shape
     out = torch.empty(count, dtype=torch.int64, device=grid.device)
     dmm._check(dmm.lib().dmm_sort_steps(alg.encode(), grid.data_ptr(), w, m, count, out.data_ptr(),
@@ -314,7 +316,7 @@ def run_algorithms(alg: str, instances: list[Instance], *, strict: bool = True, 
     steps = [modelled_steps(alg, w, m)] * count
     if steps[0] == 0 and alg in ("partition_general", "integer_sort_general") and leaf_metered(w, m):
         steps = leaf_steps(grid, w if alg == "partition_general" else w * m).cpu().tolist()
-    elif alg in ("sort_short_wide", "sort_square") and sort_metered(alg, w, m):
+    elif alg in ("sort_short_wide", "sort_square", "sort_tall") and sort_metered(alg, w, m):
         steps = sort_steps(alg, grid).cpu().tolist()
     res = o.cpu().numpy().astype(np.uint64)
     outs = []

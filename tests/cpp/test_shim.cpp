@@ -324,7 +324,7 @@ static void run_algorithm_cases() {
             CHECK(ra.report.cleanup_retries == rb.report.cleanup_retries);
             CHECK(ra.report.iterations == rb.report.iterations && ra.report.fallback == rb.report.fallback);
             if (dmm_modelled_steps(algorithm_name(c.a), c.w, c.m) || c.a == Algorithm::sort_short_wide ||
-                c.a == Algorithm::sort_square ||
+                c.a == Algorithm::sort_square || c.a == Algorithm::sort_tall ||
                 ((c.a == Algorithm::partition_general || c.a == Algorithm::integer_sort_general) && c.w <= c.m))
                 // modelled / replayed meters
                 CHECK(ra.report.steps == rb.report.steps && ra.report.work == rb.report.work);

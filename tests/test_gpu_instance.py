@@ -110,7 +110,11 @@ def test_leaf_steps_match_reference(ref, alg, w, m):
 
 @pytest.mark.parametrize("alg,w,m", [("sort_short_wide", 2, 4), ("sort_short_wide", 4, 16),
                                      ("sort_short_wide", 3, 9), ("sort_short_wide", 8, 64),
-                                     ("sort_square", 4, 4), ("sort_square", 16, 16), ("sort_square", 64, 64)])
+                                     ("sort_square", 4, 4), ("sort_square", 16, 16), ("sort_square", 64, 64),
+                                     ("sort_tall", 32, 8), ("sort_tall", 32, 1), ("sort_tall", 32, 2),
+                                     ("sort_tall", 32, 16), ("sort_tall", 32, 32), ("sort_tall", 64, 16),
+                                     ("sort_tall", 64, 8), ("sort_tall", 128, 32), ("sort_tall", 128, 16),
+                                     ("sort_tall", 16, 16)])
 def test_sort_steps_match_reference(ref, alg, w, m):
     # the comparison sorts' merge row sorts, replayed on the device (incl. the square skeleton's
     # merged-lockstep groups), against the reference's Machine::steps() instance by instance
