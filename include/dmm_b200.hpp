@@ -21,7 +21,7 @@
 //
 // Not reproduced (GPU kernels have no DMM step meter): Machine::steps()/work() do not
 // advance (run_algorithm reports the reference's count where it is modelled: dmm_modelled_steps,
-// dmm_leaf_steps); PartitionProbe hooks are replayed from the kernel's snapshots (the caller's
+// dmm_leaf_steps, dmm_general_steps); PartitionProbe hooks are replayed from the kernel's snapshots (the caller's
 // machine holds the reference's window at each call), ShortWideHook calls likewise; traces
 // are unsupported (TraceIncomplete); permute() reproduces
 // the output region, the report and the Rng position, not the scratch/counter cells.
@@ -435,7 +435,7 @@ inline PermuteReport permute(Machine& mach, Rng& rng, const PermuteParams& param
 /// The dispatcher the reference's CLI and acceptance harness use, over the B200 kernels: the
 /// same instance checks, views, verification and report fields.  The GPU has no DMM step
 /// meter: report.steps / work are the reference's counts where modelled (dmm_modelled_steps,
-/// dmm_leaf_steps) and 0 otherwise; conflicts counts the model's violations (0: every
+/// dmm_leaf_steps, dmm_general_steps; the permutation 0); conflicts counts the model's violations (0: every
 /// kernel relayout is checked conflict-free at compile time); record_trace throws
 /// TraceIncomplete.
 inline RunOutcome run_algorithm(Algorithm alg, const Instance& in, const RunOptions& opt = {}) {
@@ -512,14 +512,18 @@ inline RunOutcome run_algorithm(Algorithm alg, const Instance& in, const RunOpti
     }
     // the reference's Machine::steps() where it does not depend on the data (0 otherwise)
     out.report.steps = dmm_modelled_steps(algorithm_name(alg), in.w, in.m);
-    if (out.report.steps == 0 && (alg == Algorithm::partition_general || alg == Algorithm::integer_sort_general) &&
-        in.w <= in.m) {
-        // data-dependent leaf: replay its states on the device (dmm_leaf_steps)
+    if (out.report.steps == 0 && (alg == Algorithm::partition_general || alg == Algorithm::integer_sort_general)) {
+        // data-dependent leaf (dmm_leaf_steps) or the w > m recursion (dmm_general_steps): replay
+        // the reference's states on the device
         std::vector<uint32_t> g(in.grid.begin(), in.grid.end());
         DeviceBuffer dg(sizeof(uint32_t) * g.size()), ds(sizeof(uint64_t));
         to_device(dg, g);
         const uint64_t domain = alg == Algorithm::partition_general ? in.w : u64(in.w) * in.m;
-        if (dmm_leaf_steps(dg.as<uint32_t>(), in.w, in.m, 1, domain, ds.as<uint64_t>(), nullptr) == DMM_OK) {
+        const dmm_status ms =
+            in.w <= in.m ? dmm_leaf_steps(dg.as<uint32_t>(), in.w, in.m, 1, domain, ds.as<uint64_t>(), nullptr)
+                         : dmm_general_steps(dg.as<uint32_t>(), in.w, in.m, 1, domain, ds.as<uint64_t>(), nullptr,
+                                             nullptr);
+        if (ms == DMM_OK) {
             std::vector<uint64_t> st(1);
             to_host(st, ds);
             out.report.steps = st[0];

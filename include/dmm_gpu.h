@@ -76,6 +76,15 @@ uint64_t dmm_modelled_steps(const char* algorithm, uint32_t w, uint32_t m);
  * replay of the leaf's states on the device (off the hot path); 2 <= w <= 32, m <= 128. */
 dmm_status dmm_leaf_steps(const uint32_t* in, uint32_t w, uint32_t m, uint64_t count, uint64_t domain,
                           uint64_t* steps, void* stream);
+/* The meter for every shape of partition_general / integer_sort_general the reference accepts,
+ * the w > m recursion included (balance_divide_sort partition.hpp:363-428: balancing tower,
+ * convert-and-divide, leaves, column recursion, checked cleanup with its retry loop):
+ * steps[k] = Machine::steps() and, if retries is not NULL, retries[k] =
+ * GeneralStats::cleanup_retries for instance k (device [count][w][m], keys < domain).  Each
+ * section is charged the reference's access count over a replay of its states, one thread per
+ * instance (off the hot path); w m <= 65536. */
+dmm_status dmm_general_steps(const uint32_t* in, uint32_t w, uint32_t m, uint64_t count, uint64_t domain,
+                             uint64_t* steps, uint32_t* retries, void* stream);
 /* The same meter for the comparison sorts sort_short_wide (sort.hpp:225, w^2 <= m <= 64) and
  * sort_square (sort.hpp:337, w = m = h^2 <= 64): every row sort merge-sorts its banks. */
 dmm_status dmm_sort_steps(const char* algorithm, const uint32_t* in, uint32_t w, uint32_t m, uint64_t count,

@@ -211,6 +211,8 @@ class Ref:
         L.dmmr_integer_sort_general.argtypes = [C.c_uint32, C.c_uint32, u64p, C.c_uint64, C.c_int, C.c_int, u32p,
                                                 u32p, u64p, C.c_uint32, u32p]
         L.dmmr_partition_general.argtypes = [C.c_uint32, C.c_uint32, u64p, C.c_int, u32p, u32p]
+        L.dmmr_integer_sort_general_steps.argtypes = [C.c_uint32, C.c_uint32, u64p, C.c_uint64, C.c_int, C.c_int,
+                                                      u32p, u32p, u64p]
         L.dmmr_permute.argtypes = [C.c_uint32, C.c_uint32, u64p, C.c_uint64, C.c_uint32, C.c_uint32, u64p,
                                    C.POINTER(PermuteReport), u32p]
         L.dmmr_layout.argtypes = [C.c_int, C.c_uint32, C.c_uint32, u64p]
@@ -313,6 +315,15 @@ class Ref:
         if probe_snaps:
             res["snapshots"] = snaps[: min(ns.value, probe_snaps)]
         return s, g, res
+
+    def integer_sort_general_steps(self, grid, domain: int, enforce_pre: bool = False, strict: bool = False):
+        """integer_sort_general on any keys < domain: (status, final grid, {steps, cleanup_retries, sorted})."""
+        g = _u64(grid).copy()
+        w, m = g.shape
+        cr, so, st = C.c_uint32(), C.c_uint32(), C.c_uint64()
+        s = self.lib.dmmr_integer_sort_general_steps(w, m, _ptr(g), domain, int(enforce_pre), int(strict),
+                                                     C.byref(cr), C.byref(so), C.byref(st))
+        return s, g, {"steps": st.value, "cleanup_retries": cr.value, "sorted": bool(so.value)}
 
     def partition_general(self, grid, strict: bool = True):
         g = _u64(grid).copy()

@@ -205,6 +205,31 @@ int dmmr_integer_sort_general(uint32_t w, uint32_t m, uint64_t* grid, uint64_t d
     }
 }
 
+// integer_sort_general on the vp view with an explicit domain on ANY keys (run_algorithm only takes
+// generated instances): Machine::steps() and the stats, for the recursion's step meter.
+int dmmr_integer_sort_general_steps(uint32_t w, uint32_t m, uint64_t* grid, uint64_t domain, int enforce_pre,
+                                    int strict, uint32_t* cleanup_retries, uint32_t* sorted, uint64_t* steps) {
+    try {
+        Machine mach(MachineConfig::standard(w, m, strict != 0));
+        const auto& cfg = mach.config();
+        std::vector<u32> rows(w);
+        for (u32 r = 0; r < w; ++r)
+            rows[r] = r;
+        MatrixView vp = MatrixView::make(mach, rows, cfg.work_base(), m, cfg.scratch_a_base(),
+                                         cfg.scratch_b_base());
+        vp.load(std::vector<word>(grid, grid + u64(w) * m));
+        GeneralStats st = integer_sort_general(vp, domain, nullptr, enforce_pre != 0);
+        *cleanup_retries = st.cleanup_retries;
+        *sorted = st.sorted;
+        *steps = mach.steps();
+        auto s = vp.snapshot();
+        std::memcpy(grid, s.data(), sizeof(uint64_t) * s.size());
+        return DMM_OK;
+    } catch (...) {
+        return status_of_current_exception();
+    }
+}
+
 // partition_general on the full view, as run_algorithm does (instance.hpp:326).
 int dmmr_partition_general(uint32_t w, uint32_t m, uint64_t* grid, int strict, uint32_t* cleanup_retries,
                            uint32_t* sorted) {

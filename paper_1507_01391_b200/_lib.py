@@ -55,6 +55,7 @@ SIGNATURES = {
     "dmm_modelled_steps": (_u64, [C.c_char_p, _u32, _u32]),
     "dmm_leaf_steps": (_int, [_vp, _u32, _u32, _u64, _u64, _vp, _vp]),
     "dmm_sort_steps": (_int, [C.c_char_p, _vp, _u32, _u32, _u64, _vp, _vp]),
+    "dmm_general_steps": (_int, [_vp, _u32, _u32, _u64, _u64, _vp, _vp, _vp]),
     "dmm_multisplit_count": (_int, [_vp, _u64, _u32, _u32, _vp, _vp, _vp]),
     "dmm_multisplit_scatter_to": (_int, [_vp, _u64, _u32, _u32, _vp, _vp, _vp, _vp]),
     "dmm_offline_schedule": (_int, [_u32, _u32, _vp, _vp]),

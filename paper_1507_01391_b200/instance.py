@@ -18,8 +18,9 @@ instance holding a word >= 2^32 raises KeyOutOfRange); ``gen_instance("sort", ..
 the uint32 sort tile of include/dmm_gpu.h (the reference's sort kind draws 64-bit words);
 ``RunReport.steps`` / ``work`` are the reference's exact counts where the schedule is
 data-independent (``modelled_steps``), for the w <= m leaves of the general partition /
-integer sort (``leaf_steps``) and for the comparison sorts (``sort_steps``), both replayed on
-the device; 0 otherwise (the recursion with w > m and the permutation);
+integer sort (``leaf_steps``), for the w > m recursion (``general_steps``, cleanup retries
+included) and for the comparison sorts (``sort_steps``), all replayed on the device; 0 for the
+permutation;
 ``record_trace=True`` raises TraceIncomplete.
 """
 from __future__ import annotations
@@ -228,6 +229,24 @@ def leaf_steps(grid: torch.Tensor, domain: int) -> torch.Tensor:
     return out
 
 
+def general_metered(w: int, m: int) -> bool:
+    """dmm_general_steps meters this recursion shape (w > m; it rejects what general_sort_shape_ok
+    rejects, as the kernels did before it is called)."""
+    return w > m >= 2 and w * m <= 65536
+
+
+def general_steps(grid: torch.Tensor, domain: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """(Machine::steps(), GeneralStats::cleanup_retries) of partition_general / integer_sort_general
+    for each input instance of ``grid`` ([count, w, m] device, keys < domain), the w > m recursion
+    included: the reference's states replayed on the device (dmm_general_steps)."""
+    count, w, m = grid.shape
+    steps = torch.empty(count, dtype=torch.int64, device=grid.device)
+    retries = torch.empty(count, dtype=torch.int32, device=grid.device)
+    dmm._check(dmm.lib().dmm_general_steps(grid.data_ptr(), w, m, count, domain, steps.data_ptr(),
+                                           retries.data_ptr(), dmm._stream(None)), "general_steps")
+    return steps, retries
+
+
 def sort_metered(alg: str, w: int, m: int) -> bool:
     """dmm_sort_steps meters this comparison sort (sort_short_wide w^2 <= m <= 64,
     sort_square w = m = h^2 <= 64, sort_tall m | w with w in {32, 64, 128} or w = m <= 32)."""
@@ -316,6 +335,8 @@ def run_algorithms(alg: str, instances: list[Instance], *, strict: bool = True, 
     steps = [modelled_steps(alg, w, m)] * count
     if steps[0] == 0 and alg in ("partition_general", "integer_sort_general") and leaf_metered(w, m):
         steps = leaf_steps(grid, w if alg == "partition_general" else w * m).cpu().tolist()
+    elif steps[0] == 0 and alg in ("partition_general", "integer_sort_general") and general_metered(w, m):
+        steps = general_steps(grid, w if alg == "partition_general" else w * m)[0].cpu().tolist()
     elif alg in ("sort_short_wide", "sort_square", "sort_tall") and sort_metered(alg, w, m):
         steps = sort_steps(alg, grid).cpu().tolist()
     res = o.cpu().numpy().astype(np.uint64)

@@ -298,7 +298,7 @@ static void probe_cases() {
 }
 
 // run_algorithm (instance.hpp:277-363): the CLI / acceptance dispatch, every algorithm on a
-// shape it accepts; the same report fields except the step meter
+// shape it accepts; the same report fields (steps: every meter but the permutation's)
 static void run_algorithm_cases() {
     struct Case {
         Algorithm a;
@@ -311,7 +311,8 @@ static void run_algorithm_cases() {
                           {Algorithm::integer_sort_general, 8, 64}, {Algorithm::partition_general, 32, 32},
                           {Algorithm::partition_general, 32, 64}, {Algorithm::integer_sort_general, 32, 128},
                           {Algorithm::sort_short_wide, 4, 16}, {Algorithm::sort_tall, 128, 32},
-                          {Algorithm::permute, 32, 32}, {Algorithm::permute, 128, 64}};
+                          {Algorithm::permute, 32, 32}, {Algorithm::permute, 128, 64},
+                          {Algorithm::partition_general, 64, 32}, {Algorithm::integer_sort_general, 64, 8}};
     for (const Case& c : cases) {
         for (u64 seed = 1; seed <= 3; ++seed) {
             Instance in = gen_instance(instance_kind_for(c.a), c.w, c.m, seed);
@@ -325,8 +326,8 @@ static void run_algorithm_cases() {
             CHECK(ra.report.iterations == rb.report.iterations && ra.report.fallback == rb.report.fallback);
             if (dmm_modelled_steps(algorithm_name(c.a), c.w, c.m) || c.a == Algorithm::sort_short_wide ||
                 c.a == Algorithm::sort_square || c.a == Algorithm::sort_tall ||
-                ((c.a == Algorithm::partition_general || c.a == Algorithm::integer_sort_general) && c.w <= c.m))
-                // modelled / replayed meters
+                c.a == Algorithm::partition_general || c.a == Algorithm::integer_sort_general)
+                // modelled / replayed meters (w > m: dmm_general_steps)
                 CHECK(ra.report.steps == rb.report.steps && ra.report.work == rb.report.work);
             if (c.a == Algorithm::permute) {
                 CHECK(ra.pipeline.random_words == rb.pipeline.random_words);

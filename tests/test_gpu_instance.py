@@ -20,6 +20,7 @@ CASES = [
     ("partition_square", 16, 16), ("partition_short_wide", 8, 64), ("integer_sort_general", 32, 16),
     ("integer_sort_general", 32, 128), ("sort_square", 16, 16), ("sort_tall", 64, 16),
     ("sort_short_wide", 4, 16), ("permute", 32, 32), ("permute", 64, 8), ("permute", 128, 64),
+    ("partition_general", 64, 32), ("partition_general", 128, 32), ("integer_sort_general", 64, 8),
 ]
 
 
@@ -47,7 +48,8 @@ def test_run_algorithm_matches_reference(ref, alg, w, m):
             (rr["iterations"], rr["fallback"], rr["cleanup_retries"])
         assert rep.conflicts == rr["conflicts"] == 0
         metered = (I.modelled_steps(alg, w, m) or I.sort_metered(alg, w, m)
-                   or (alg in ("partition_general", "integer_sort_general") and I.leaf_metered(w, m)))
+                   or (alg in ("partition_general", "integer_sort_general")
+                       and (I.leaf_metered(w, m) or I.general_metered(w, m))))
         if metered:  # the reference's meter, reproduced exactly
             assert (rep.steps, rep.work) == (rr["steps"], rr["steps"] * w)
         else:
