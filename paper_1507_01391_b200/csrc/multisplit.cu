@@ -10,7 +10,7 @@
 //   2. k_ms_scan_*: exclusive scan of the per-tile counts, bucket-major (two levels);
 //   3. k_ms_scatter: the warp re-reads its tile in rows of 32 consecutive keys (one per lane);
 //      a key's destination is offset[bucket][tile] + keys of its bucket in earlier rows + keys
-//      of its bucket in lower lanes of this row (a warp prefix scan of byte-packed counters),
+//      of its bucket in lower lanes of this row (popc of the label-bit ballots' match mask),
 //      i.e. stable by source index, and a warp store writes at most nbuckets contiguous runs.
 // The cross-GPU exchange (bucket j -> rank owning j) is either fused into pass 3
 // (dmm_multisplit_count + dmm_multisplit_scatter_to: k_ms_scatter<LB, true> stores each key
@@ -199,6 +199,65 @@ __global__ void k_ms_scan_add(uint64_t* __restrict__ out, uint64_t total, const 
         out[i] += block_sums[blockIdx.x];
 }
 
+// Rows of 32 consecutive keys, one per lane (coalesced 128-byte loads): the keys of one bucket
+// in one row go to consecutive output words, so every warp store writes at most NB contiguous
+// runs.  Rows go in groups of kG; the next group's loads are issued before the current group
+// is ranked (2 kG rows in flight per warp: the kernel is load-latency bound).  A key's rank
+// among its row's bucket-mates = popc of the lower lanes whose LB label bits all match (LB
+// ballots); the row's per-bucket totals are the same masks for bucket = lane.  Lane b < NB
+// holds bucket b's next output address (`cur`), so a key needs one 64-bit shuffle.  FULL: the
+// whole tile is in range (no per-key bounds).
+constexpr int kG = 16;  // rows per group (4: 223, 8: 255, 16: 295, 32: 276 G keys/s on cfg5)
+
+template <int LB, bool FULL>
+__device__ __forceinline__ void scatter_tile(const uint32_t* __restrict__ keys, uint64_t n, uint32_t shift,
+                                             uint64_t base, uint32_t* cur, int lane) {
+    constexpr int NB = 1 << LB;
+    const uint32_t lt = (1u << lane) - 1u;  // lanes below this one
+    uint32_t k[kG];
+    bool valid[kG];
+    auto load_group = [&](int r, uint32_t (&kk)[kG], bool (&vv)[kG]) {
+#pragma unroll
+        for (int j = 0; j < kG; ++j) {
+            const uint64_t i = base + (uint64_t)(r + j) * 32 + lane;
+            vv[j] = FULL || i < n;
+            kk[j] = vv[j] ? __ldg(keys + i) : 0u;
+        }
+    };
+    load_group(0, k, valid);
+#pragma unroll 1
+    for (int r = 0; r < kMsRows * 4; r += kG) {
+        uint32_t kn[kG];
+        bool vn[kG];
+        if (r + kG < kMsRows * 4)
+            load_group(r + kG, kn, vn);
+#pragma unroll
+        for (int j = 0; j < kG; ++j) {
+            const uint32_t b = (k[j] >> shift) & (NB - 1);
+            uint32_t mo = FULL ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, valid[j]);
+            uint32_t ml = mo;
+#pragma unroll
+            for (int i = 0; i < LB; ++i) {
+                const uint32_t bi = __ballot_sync(0xFFFFFFFFu, (b >> i) & 1u);
+                mo &= ((b >> i) & 1u) ? bi : ~bi;
+                ml &= ((lane >> i) & 1) ? bi : ~bi;
+            }
+            uint32_t* d = reinterpret_cast<uint32_t*>(
+                __shfl_sync(0xFFFFFFFFu, reinterpret_cast<unsigned long long>(cur), (int)b));
+            if (valid[j])
+                d[__popc(mo & lt)] = k[j];
+            cur += lane < NB ? __popc(ml) : 0u;
+        }
+        if (r + kG < kMsRows * 4) {
+#pragma unroll
+            for (int j = 0; j < kG; ++j) {
+                k[j] = kn[j];
+                valid[j] = vn[j];
+            }
+        }
+    }
+}
+
 // REMOTE: bucket b goes to its own destination array dst[b] (a peer GPU's receive buffer over
 // NVLink, or any device pointer) starting at dst_base[b] -- the all-to-all fused into the
 // scatter: keys leave the SM straight for the owner's memory, no staging copy, no NCCL pass.
@@ -208,72 +267,24 @@ __global__ void __launch_bounds__(256) k_ms_scatter(const uint32_t* __restrict__
                                                     uint32_t* __restrict__ out, uint32_t* const* __restrict__ dst = nullptr,
                                                     const uint64_t* __restrict__ dst_base = nullptr) {
     constexpr int NB = 1 << LB;
-    constexpr int H = Packed<NB>::H;
     const int lane = threadIdx.x & 31;
     const uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (tile >= ntiles)
         return;
-    // lane b < NB holds the running output position of bucket b
-    uint64_t pos = lane < NB ? offsets[(uint64_t)lane * ntiles + tile] : 0;
-    uint32_t* my_dst = out;  // lane b < NB: bucket b's destination array
-    if constexpr (REMOTE) {
-        if (lane < NB) {
-            pos = pos - offsets[(uint64_t)lane * ntiles] + dst_base[lane];  // rank within the bucket
-            my_dst = dst[lane];
-        }
+    // lane b < NB: bucket b's next output address (its tile offset in the bucket-major scan)
+    uint32_t* cur = out;
+    if (lane < NB) {
+        const uint64_t pos = offsets[(uint64_t)lane * ntiles + tile];
+        if constexpr (REMOTE)
+            cur = dst[lane] + (pos - offsets[(uint64_t)lane * ntiles] + dst_base[lane]);  // rank within the bucket
+        else
+            cur = out + pos;
     }
     const uint64_t base = tile * kMsTile;
-    // rows of 32 consecutive keys, one per lane (coalesced 128-byte loads, 4 rows in flight):
-    // the keys of one bucket in one row go to consecutive output words, so every warp store
-    // writes at most NB contiguous runs
-#pragma unroll 1
-    for (int r = 0; r < kMsRows * 4; r += 4) {
-        uint32_t k[4];
-        bool valid[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint64_t i = base + (uint64_t)(r + j) * 32 + lane;
-            valid[j] = i < n;
-            k[j] = valid[j] ? __ldg(keys + i) : 0u;
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t b = (k[j] >> shift) & (NB - 1);
-            Packed<NB> own;
-            own.clear();
-            if (valid[j])
-                own.add(b);
-            // exclusive warp prefix: keys of each bucket held by lower lanes in this row
-            uint32_t lower = 0, tot_mine = 0;
-#pragma unroll
-            for (int h = 0; h < H; ++h) {
-                uint32_t x = own.p[h];
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-                    if (lane >= o)
-                        x += y;
-                }
-                const uint32_t excl = x - own.p[h];
-                if ((b >> 2) == (uint32_t)h)
-                    lower = (excl >> (8 * (b & 3))) & 0xFFu;
-                const uint32_t t = __shfl_sync(0xFFFFFFFFu, x, 31);  // row totals (inclusive, lane 31)
-                if ((lane >> 2) == h)
-                    tot_mine = (t >> (8 * (lane & 3))) & 0xFFu;
-            }
-            const uint64_t p0 = __shfl_sync(0xFFFFFFFFu, pos, (int)b);
-            if constexpr (REMOTE) {
-                uint32_t* d = reinterpret_cast<uint32_t*>(
-                    __shfl_sync(0xFFFFFFFFu, reinterpret_cast<unsigned long long>(my_dst), (int)b));
-                if (valid[j])
-                    d[p0 + lower] = k[j];
-            } else {
-                if (valid[j])
-                    out[p0 + lower] = k[j];
-            }
-            pos += tot_mine;
-        }
-    }
+    if (base + kMsTile <= n)
+        scatter_tile<LB, true>(keys, n, shift, base, cur, lane);
+    else
+        scatter_tile<LB, false>(keys, n, shift, base, cur, lane);
 }
 
 }  // namespace dmmdev
