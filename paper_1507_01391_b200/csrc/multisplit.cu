@@ -214,6 +214,11 @@ __device__ __forceinline__ void scatter_tile(const uint32_t* __restrict__ keys, 
                                              uint64_t base, uint32_t* cur, int lane) {
     constexpr int NB = 1 << LB;
     const uint32_t lt = (1u << lane) - 1u;  // lanes below this one
+    const uint32_t lane_nb = lane < NB ? 0xFFFFFFFFu : 0u;  // lanes that carry a bucket total
+    uint32_t sl[LB > 0 ? LB : 1];                            // this lane's bucket bits as masks
+#pragma unroll
+    for (int i = 0; i < LB; ++i)
+        sl[i] = ((lane >> i) & 1) ? 0xFFFFFFFFu : 0u;
     uint32_t k[kG];
     bool valid[kG];
     auto load_group = [&](int r, uint32_t (&kk)[kG], bool (&vv)[kG]) {
@@ -235,18 +240,20 @@ __device__ __forceinline__ void scatter_tile(const uint32_t* __restrict__ keys, 
         for (int j = 0; j < kG; ++j) {
             const uint32_t b = (k[j] >> shift) & (NB - 1);
             uint32_t mo = FULL ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, valid[j]);
-            uint32_t ml = mo;
+            uint32_t ml = mo & lane_nb;
 #pragma unroll
             for (int i = 0; i < LB; ++i) {
-                const uint32_t bi = __ballot_sync(0xFFFFFFFFu, (b >> i) & 1u);
-                mo &= ((b >> i) & 1u) ? bi : ~bi;
-                ml &= ((lane >> i) & 1) ? bi : ~bi;
+                // si: all ones iff label bit i is set; x & ~(bi ^ si) keeps the lanes that agree
+                const uint32_t si = uint32_t(int32_t(k[j] << (31 - int(shift) - i)) >> 31);
+                const uint32_t bi = __ballot_sync(0xFFFFFFFFu, si != 0u);
+                mo &= ~(bi ^ si);
+                ml &= ~(bi ^ sl[i]);
             }
             uint32_t* d = reinterpret_cast<uint32_t*>(
                 __shfl_sync(0xFFFFFFFFu, reinterpret_cast<unsigned long long>(cur), (int)b));
             if (valid[j])
                 d[__popc(mo & lt)] = k[j];
-            cur += lane < NB ? __popc(ml) : 0u;
+            cur += __popc(ml);
         }
         if (r + kG < kMsRows * 4) {
 #pragma unroll
