@@ -1,16 +1,25 @@
 """bench.py -- keys/s of the B200 bank-conflict-free kernels (BASELINE.json metric).
 
-Default workload (BASELINE.json configs[1]): general w-way partition, w = 32, n = 256 keys
-per instance (32 x 8; the reference's balance() rejects this shape, the B200 kernel runs it
-with the documented partial-group extension), 2^18 instances per GPU, uint32 labels
-generated on the device with the reference's own seeded generator (gen_instance).
+Default workload (BASELINE.json configs[2], the largest configuration that fits one GPU and
+one the reference accepts as is): the bank-conflict-free sort, w = 32, n = 4096 uint32 keys
+per block-tile (a 32 x 128 machine), 2^20 tiles per GPU = 2^32 keys (16 GiB in + 16 GiB
+out), keys generated on the device (the builder-defined uint32 generator).
+The reference path is integer_sort_general(view, 2^32) (partition.hpp:436-449), which the
+reference arm (`--impl reference`) runs on the same 32 x 128 tiles.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl reference]
 
-A "step" is one pass of the partition over the whole batch.  value = keys/s over the job
+Other configs (`--config`): cfg1 (32 x 32 partition), cfg2b (32 x 16 general partition),
+cfg4 / cfg4s (permutation), cfg5 (global 8-way partition) and cfg2 (32 x 8 general
+partition: a B200 EXTENSION -- the reference rejects that shape, partition.hpp:241-244 --
+so its reference arm times 32 x 16 and says so).
+
+A "step" is one pass of the kernel over the whole batch.  value = keys/s over the job
 (inputs resident in HBM); e2e = the same metric through the public API with the inputs in
-pinned host memory, H2D + kernel + D2H inside the timed region.  The batch (256 MiB in +
-256 MiB out per GPU) is larger than the 126 MB L2, so no explicit flush is needed.
+pinned host memory, H2D + kernel + D2H inside the timed region.  Every batch is larger than
+the 126 MB L2, so no explicit flush is needed.  After timing, the output is checked at full
+size (cfg3: per-tile key sum, sum of squares and XOR against the input, sortedness, and an
+exact comparison of sampled tiles against numpy's sort).
 Multi-GPU: instances are sharded across ranks (weak scaling, no collective in the data path).
 """
 from __future__ import annotations
@@ -32,11 +41,13 @@ CONFIGS = {
     "cfg1": ("partition_general", 32, 32, 1 << 16, 0,
              "w-way partition w=32, n=w^2=1024 uint32 per instance, 65536 instances (reference path: shearsort_rect)"),
     "cfg2": ("partition_general", 32, 8, 1 << 18, 1,
-             "general w-way partition w=32, n=256 (n<w^2) per instance, 2^18 instances"),
+             "general w-way partition w=32, n=256 (n<w^2) per instance, 2^18 instances "
+             "[B200 EXTENSION: the reference rejects 32x8; DMM_FLAG_EXT_PARTIAL_GROUPS]"),
     "cfg2b": ("partition_general", 32, 16, 1 << 17, 0,
               "general w-way partition w=32, n=512 (reference-accepted stand-in of cfg2), 2^17 instances"),
     "cfg3": ("integer_sort_general", 32, 128, 1 << 20, 0,
-             "bank-conflict-free sort w=32, n=4096 uint32 keys per block-tile (32x128), 2^20 tiles"),
+             "bank-conflict-free sort w=32, n=4096 uint32 keys per block-tile (32x128 machine), 2^20 tiles "
+             "(reference path: integer_sort_general(view, 2^32))"),
     "cfg5": ("global_partition", 1, 1 << 26, 8, 0,
              "global 8-way partition of 2^32 uint32 keys across 8 GPUs: 2^29 keys per GPU (label = key >> 29), "
              "local stable multisplit + NCCL all-to-all"),
@@ -225,6 +236,57 @@ def measured_traffic(cfg_name: str):
     return t
 
 
+def workload_config(cfg_name: str, world: int = 1, count: int = 0, graph: bool = True, transport: str = "p2p"):
+    """The `config` object of the bench line, shared by both arms."""
+    alg, w, m, cnt, flags, desc = CONFIGS[cfg_name]
+    if count:
+        cnt = count
+        desc += f" [count overridden: {count}]"
+    return {"workload": desc, "name": cfg_name, "algorithm": alg, "w": w, "m": m, "instances_per_gpu": cnt,
+            "keys_per_gpu": cnt * w * m, "l2": "inputs >= 2x L2 (no flush needed)",
+            "timed_loop": "CUDA graph replay of the one-launch step" if graph and alg != "global_partition"
+            else "eager launches",
+            "parallelism": (f"instances sharded over {world} GPU(s)" if alg != "global_partition" else
+                            f"keys sharded over {world} GPU(s); exchange: " +
+                            ("fused into the scatter (stores into the owners' receive buffers, "
+                             "CUDA IPC / NVLink peer memory)" if transport == "p2p"
+                             else "multisplit + NCCL all-to-all"))}
+
+
+def verify_sort_full(g, out, count: int, tiles_exact: int = 64) -> dict:
+    """Full-size check of a batched sort: per tile, the 64-bit key sum, the 64-bit sum of
+    squares and the XOR of the output equal the input's (the multiset survives), every tile is
+    ascending, and `tiles_exact` tiles spread over the batch equal numpy's sort exactly."""
+    import numpy as np
+    import torch
+    n = g[0].numel()
+    gi, go = g.view(count, n), out.view(count, n)
+    ok_sum = ok_xor = ok_sorted = True
+    chunk = max(1, (1 << 26) // n)
+    for lo in range(0, count, chunk):
+        hi = min(count, lo + chunk)
+        a = gi[lo:hi].to(torch.int64) & 0xFFFFFFFF
+        b = go[lo:hi].to(torch.int64) & 0xFFFFFFFF
+        ok_sum &= bool((a.sum(1) == b.sum(1)).all()) and bool(((a * a).sum(1) == (b * b).sum(1)).all())
+        ok_sorted &= bool((b[:, 1:] >= b[:, :-1]).all())
+        del a, b
+        xa, xb = gi[lo:hi], go[lo:hi]
+        while xa.shape[1] > 1:
+            h = xa.shape[1] // 2
+            xa = xa[:, :h] ^ xa[:, h: 2 * h] if xa.shape[1] % 2 == 0 else torch.cat(
+                [xa[:, :h] ^ xa[:, h: 2 * h], xa[:, 2 * h:]], 1)
+            xb = xb[:, :h] ^ xb[:, h: 2 * h] if xb.shape[1] % 2 == 0 else torch.cat(
+                [xb[:, :h] ^ xb[:, h: 2 * h], xb[:, 2 * h:]], 1)
+        ok_xor &= bool((xa == xb).all())
+    idx = np.unique(np.linspace(0, count - 1, min(count, tiles_exact)).astype(np.int64))
+    hin = gi[torch.as_tensor(idx, device=g.device)].cpu().numpy().view(np.uint32)
+    hout = go[torch.as_tensor(idx, device=g.device)].cpu().numpy().view(np.uint32)
+    ok_exact = bool((np.sort(hin, axis=1) == hout).all())
+    return {"tiles": count, "sum_sumsq": ok_sum, "xor": ok_xor, "ascending": ok_sorted,
+            "exact_tiles": int(len(idx)), "exact": ok_exact,
+            "ok": ok_sum and ok_xor and ok_sorted and ok_exact}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -233,11 +295,21 @@ def run_reference(args):
     if base is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdmm_ref.so not built"}))
         return 0
-    alg, w, m, count, flags, desc = CONFIGS[args.config]
+    cfg = workload_config(args.config, world=args.gpus)
+    same = True
+    if args.config == "cfg2":
+        # the reference rejects 32 x 8: the line names the shape that was actually timed
+        same = False
+        cfg.update({"workload": "general w-way partition w=32, n=512 (32x16: the reference's closest accepted "
+                                "general shape; it rejects the 32x8 of cfg2)", "m": 16,
+                    "keys_per_gpu": cfg["instances_per_gpu"] * 32 * 16})
+    if args.config == "cfg5":
+        same = False  # no reference path partitions 2^32 keys; its 8 x 65536 stand-in is timed
+        cfg["workload"] += " [reference arm: partition_short_wide on 8x65536 instances as the stand-in]"
     line = {"impl": "reference", "metric": "keys/s", "value": base["value"], "unit": "keys/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "dtype": "u32", "data": "synthetic (reference gen_instance)",
-            "config": {"workload": desc}, "cpu_baseline": base,
+            "scaling": "weak", "dtype": "u32", "data": "synthetic (reference gen_instance)",
+            "config": cfg, "same_shape_as_b200_arm": same, "cpu_baseline": base,
             "e2e": {"value": base["value"], "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -248,7 +320,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--count", type=int, default=0, help="instances per GPU (default: the config's)")
@@ -293,6 +365,7 @@ def main():
 
     seeds = np.arange(1 + rank * count, 1 + (rank + 1) * count, dtype=np.uint64)
     perm_bufs = {}
+    full_check = None
 
     def step(src, dst):
         if alg == "partition_general":
@@ -375,20 +448,46 @@ def main():
         ok = bool((out == exp).all())
     elif alg == "global_partition":
         # this rank received exactly the keys whose label it owns (8 labels over `world` ranks),
-        # and the total over ranks is every key (counts all-reduced)
+        # in (source rank, source index) order: the receive buffer is filled with a sentinel
+        # first, then compared with the stable order of the same keys (world 1: the stable
+        # argsort of the local keys; world > 1: per-label key-sum / XOR checksums all-reduced
+        # over the ranks' inputs against what this rank received, plus the total count)
+        recv = peers[0].local if args.transport == "p2p" else None
+        if recv is not None:
+            recv.fill_(-1)
         res, _ = step(g, out)
+        torch.cuda.synchronize()
         lab = (res.to(torch.int64) & 0xFFFFFFFF) >> 29
         lo, hi = rank * 8 // world, (rank + 1) * 8 // world
         ok = bool(((lab >= lo) & (lab < hi)).all())
         if world == 1:
-            ok = ok and bool((lab[1:] >= lab[:-1]).all())
+            src = g.view(-1).to(torch.int64) & 0xFFFFFFFF
+            order = torch.argsort(src >> 29, stable=True)
+            ok = ok and bool((res.view(-1).to(torch.int64) & 0xFFFFFFFF).equal(src[order]))
+            del src, order
+        else:
+            srcl = g.view(-1).to(torch.int64) & 0xFFFFFFFF
+            lab_in = srcl >> 29
+            sums = torch.zeros(8, dtype=torch.int64, device="cuda").index_add_(0, lab_in, srcl)
+            cnts = torch.bincount(lab_in, minlength=8)
+            dist.all_reduce(sums)
+            dist.all_reduce(cnts)
+            rl = res.view(-1).to(torch.int64) & 0xFFFFFFFF
+            got = torch.zeros(8, dtype=torch.int64, device="cuda").index_add_(0, rl >> 29, rl)
+            gotc = torch.bincount(rl >> 29, minlength=8)
+            ok = ok and bool((got[lo:hi] == sums[lo:hi]).all()) and bool((gotc[lo:hi] == cnts[lo:hi]).all())
+            del srcl, lab_in, rl
         n_recv = torch.tensor([res.numel()], device="cuda", dtype=torch.int64)
         if world > 1:
             dist.all_reduce(n_recv)
         ok = ok and int(n_recv.item()) == keys_per_gpu * world
+        if world > 1:
+            okt = torch.tensor([int(ok)], device="cuda")
+            dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+            ok = bool(okt.item())
     else:
-        ok = bool((out.view(count, -1)[:, 1:].to(torch.int64) & 0xFFFFFFFF >=
-                   out.view(count, -1)[:, :-1].to(torch.int64) & 0xFFFFFFFF).all())
+        full_check = verify_sort_full(g, out, count)
+        ok = full_check["ok"]
 
     # ---- end to end through the public API (pinned host in/out) -------------------------
     # chunks cycle over 3 streams: H2D of chunk i+1 || kernel of chunk i || D2H of chunk i-1
@@ -482,14 +581,7 @@ def main():
             "metric": "keys/s", "value": value, "unit": "keys/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic (reference gen_instance, on device)",
-            "config": {"workload": desc, "algorithm": alg, "w": w, "m": m, "instances_per_gpu": count,
-                       "keys_per_gpu": keys_per_gpu, "l2": "inputs 2x L2 (no flush needed)",
-                       "timed_loop": "CUDA graph replay of the one-launch step" if graph is not None else "eager launches",
-                       "parallelism": (f"instances sharded over {world} GPU(s)" if alg != "global_partition" else
-                                       f"keys sharded over {world} GPU(s); exchange: " +
-                                       ("fused into the scatter (stores into the owners' receive buffers, "
-                                        "CUDA IPC / NVLink peer memory)" if args.transport == "p2p"
-                                        else "multisplit + NCCL all-to-all"))},
+            "config": workload_config(args.config, world, args.count, graph is not None, args.transport),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"],
                          "traffic": (traffic or {}).get("bytes_per_launch"),
@@ -503,6 +595,8 @@ def main():
             "clocks": clk.summary(),
             "correct": ok,
         }
+        if full_check is not None:
+            line["full_size_check"] = full_check
         if not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = cpu_baseline(args.config)

@@ -380,6 +380,10 @@ inline void apply_schedule(const MatrixView& v, const Schedule& s) { b200::apply
 /// PermuteReport permute(Machine&, Rng&, const PermuteParams&)  permute.hpp:545-628
 inline PermuteReport permute(Machine& mach, Rng& rng, const PermuteParams& params = {}) {
     const u32 w = mach.w(), m = mach.m();
+    // permute.hpp:547-553: the shape checks run on the device path too (dmm_permute_from_state
+    // returns DMM_SHAPE_VIOLATION); the bank-layout check needs the caller's MachineConfig
+    if (!mach.config().has_scratch_b())
+        throw CapacityExceeded("permute needs the standard 4m+8 bank layout");
     // the caller's engine, mid-stream: libstdc++ prints _M_x[0..312) then _M_p
     std::vector<uint64_t> state(313);
     {
@@ -413,6 +417,12 @@ inline PermuteReport permute(Machine& mach, Rng& rng, const PermuteParams& param
     cuda_check(cudaMemcpy(&hr, drep.ptr, sizeof(hr), cudaMemcpyDeviceToHost), "D2H");
     to_host(hist, dhist);
     to_host(shifts, dsh);
+    // the per-instance status: DMM_INVALID_INSTANCE when a label is out of range or the
+    // delivered output is not the identity -- raised before the output region is written
+    uint8_t pstatus = DMM_OK;
+    cuda_check(cudaMemcpy(&pstatus, dss.ptr, 1, cudaMemcpyDeviceToHost), "D2H");
+    if (pstatus != DMM_OK)
+        raise(static_cast<dmm_status>(pstatus), "permute");
     to_host(g, dout);
     for (u32 i = 0; i < w; ++i)
         for (u32 j = 0; j < m; ++j)

@@ -350,6 +350,25 @@ dmm_status run_multisplit(const uint32_t* keys, uint64_t n, uint32_t shift, uint
     return DMM_OK;
 }
 
+// Common argument checks of the three entry points: the count pass reads 16-byte vectors at
+// key indices that are multiples of 4, so `keys` itself must be 16-byte aligned (a view with a
+// storage offset is rejected, as check_ptrs does for the other entry points), and the label
+// bits [shift, shift + log2(nbuckets)) must lie inside the 32-bit key.
+dmm_status ms_check(const uint32_t* keys, uint32_t shift, uint32_t nbuckets) {
+    if (keys && (reinterpret_cast<uintptr_t>(keys) & 15u)) {
+        set_error("keys must be 16-byte aligned");
+        return DMM_INVALID_ARGUMENT;
+    }
+    uint32_t lb = 0;
+    while ((2u << lb) <= nbuckets && lb < 6)
+        ++lb;
+    if (shift >= 32 || shift + lb > 32) {
+        set_error("label bits [shift, shift + log2(nbuckets)) must lie inside the 32-bit key");
+        return DMM_INVALID_ARGUMENT;
+    }
+    return DMM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -366,6 +385,8 @@ dmm_status dmm_multisplit_count(const uint32_t* keys, uint64_t n, uint32_t shift
     reset_launches();
     if (!bucket_starts || !workspace || (n && !keys))
         return DMM_INVALID_ARGUMENT;
+    if (dmm_status e = ms_check(keys, shift, nbuckets); e != DMM_OK)
+        return e;
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (n == 0)
         return cudaMemsetAsync(bucket_starts, 0, sizeof(uint64_t) * nbuckets, s) == cudaSuccess
@@ -391,6 +412,8 @@ dmm_status dmm_multisplit_scatter_to(const uint32_t* keys, uint64_t n, uint32_t 
         return DMM_OK;
     if (!keys || !dst || !dst_base || !workspace)
         return DMM_INVALID_ARGUMENT;
+    if (dmm_status e = ms_check(keys, shift, nbuckets); e != DMM_OK)
+        return e;
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     switch (nbuckets) {
         case 2: return run_multisplit<1>(keys, n, shift, nullptr, nullptr, workspace, s, 2, dst, dst_base);
@@ -411,6 +434,8 @@ dmm_status dmm_multisplit(const uint32_t* keys, uint64_t n, uint32_t shift, uint
         return DMM_OK;
     if (!keys || !out || !workspace)
         return DMM_INVALID_ARGUMENT;
+    if (dmm_status e = ms_check(keys, shift, nbuckets); e != DMM_OK)
+        return e;
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     switch (nbuckets) {
         case 2: return run_multisplit<1>(keys, n, shift, out, bucket_starts, workspace, s);

@@ -46,11 +46,25 @@ template <uint32_t MT>
 __global__ void __launch_bounds__(kSchedWarps * 32)
     k_apply_schedule(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint32_t w, uint32_t m_rt,
                      uint64_t count, const uint32_t* __restrict__ moves, const uint32_t* __restrict__ round_start,
-                     uint32_t n_rounds, uint8_t* __restrict__ status) {
+                     uint32_t n_rounds, uint32_t n_moves, uint8_t* __restrict__ status) {
     const uint32_t m = MT ? MT : m_rt;
     extern __shared__ uint32_t sm[];
     __shared__ uint32_t bad, dup, ragged;
-    const uint32_t n_moves = round_start[n_rounds];
+    // the shared layout is sized from the host's n_moves: round_start must agree with it (starts
+    // at 0, monotone, ends at n_moves) before anything is staged or any move is read
+    {
+        uint32_t off = 0;
+        for (uint32_t i = threadIdx.x; i <= n_rounds; i += blockDim.x) {
+            const uint32_t v = round_start[i];
+            off |= (i == 0 && v != 0) || (i == n_rounds && v != n_moves) || v > n_moves ||
+                   (i < n_rounds && round_start[i + 1] < v);
+        }
+        if (__syncthreads_or(off)) {
+            if (blockIdx.x == 0 && threadIdx.x == 0)
+                status[0] = (uint8_t)DMM_OUT_OF_BOUNDS;
+            return;
+        }
+    }
     uint32_t* sched = sm;
     uint32_t* rs = sched + n_moves;
     uint32_t* cov = rs + n_rounds + 1;
@@ -451,7 +465,7 @@ dmm_status dmm_apply_schedule(const uint32_t* in, uint32_t* out, uint32_t w, uin
     const uint64_t need = (count + dmmdev::kSchedWarps - 1) / dmmdev::kSchedWarps;
     const uint64_t blocks = std::min<uint64_t>(need, uint64_t(sms) * std::max(per_sm, 1));
     kern<<<unsigned(blocks), dmmdev::kSchedWarps * 32, smem, st>>>(in, out, w, m, count, moves, round_start,
-                                                                    n_rounds, status);
+                                                                    n_rounds, n_moves, status);
     return check_launch("k_apply_schedule");
 }
 

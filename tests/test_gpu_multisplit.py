@@ -83,3 +83,23 @@ def test_fused_scatter_simulated_ranks(world):
             loc = h[np.argsort(lab, kind="stable")]
             exp.append(loc[np.isin(loc >> shift, [b for b in range(nb) if owner[b] == r])])
         assert (dmm.as_uint32(bufs[r]) == np.concatenate(exp)).all()
+
+
+def test_multisplit_rejects_misaligned_keys_and_bad_shift():
+    # a view with a storage offset would feed the 16-byte loads a misaligned pointer;
+    # label bits outside the 32-bit key are undefined shifts -- both are argument errors now,
+    # and the context stays usable afterwards
+    keys = dmm.gen_keys(3, 4096)
+    with pytest.raises(dmm.Error):
+        dmm.multisplit(keys[1:], 8, 29)
+    with pytest.raises(dmm.Error):
+        dmm.multisplit(keys, 8, 30)  # bits [30, 33)
+    with pytest.raises(dmm.Error):
+        dmm.multisplit(keys, 2, 32)
+    out, _ = dmm.multisplit(keys, 8, 29)
+    h = dmm.as_uint32(keys)
+    assert (dmm.as_uint32(out) == h[np.argsort(h >> 29, kind="stable")]).all()
+    shifted = keys[4:].clone()  # an aligned copy of the same tail is fine
+    out, _ = dmm.multisplit(shifted, 4, 30)
+    hs = dmm.as_uint32(shifted)
+    assert (dmm.as_uint32(out) == hs[np.argsort(hs >> 30, kind="stable")]).all()

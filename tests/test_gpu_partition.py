@@ -226,3 +226,46 @@ def test_empty_and_single_batches(port):
     keys = dmm.gen_keys(0, 0)
     out, starts = dmm.multisplit(keys, 8, 29)
     assert out.numel() == 0
+
+
+def test_cfg3_tiles_vs_oracle_and_reference(port, ref):
+    # the headline config exactly: 32 x 128 uint32 tiles from the bench's generator, sorted by
+    # integer_sort_general(view, 2^32) (partition.hpp:436-449); 512 tiles against the oracle,
+    # 48 of them against the compiled reference itself
+    count = 512
+    g = dmm.gen_instances(dmm.KIND_SORT_U32, 32, 128, 1, count)
+    host = dmm.as_uint32(g)
+    for k in (0, 1, 255, 511):
+        assert (host[k] == port.gen_sort_u32(32, 128, 1 + k).astype(np.uint32)).all()
+    out, st = dmm.integer_sort_general(g, 1 << 32)
+    out = dmm.as_uint32(out)
+    assert int((st.status != 0).sum()) == 0
+    for k in range(count):
+        ost, oout, orep = port.integer_sort_general(host[k], 1 << 32)
+        assert ost == 0 and (out[k] == oout).all(), k
+        assert int(st.cleanup_retries[k]) == orep["cleanup_retries"] == 0
+    for k in range(0, count, count // 48):
+        rst, rout, _ = ref.integer_sort_general(host[k].astype(np.uint64), 1 << 32)
+        assert rst == 0 and (out[k] == rout.astype(np.uint32)).all(), k
+
+
+def test_cfg3_full_batch_multiset_check():
+    # full-size properties at 2^16 tiles (the bench applies the same check at 2^20): per-tile
+    # sum / sum of squares / XOR preserved, ascending, sampled tiles equal numpy's sort -- and
+    # the check itself rejects a wrong output (all zeros, one swapped key, one dropped key)
+    import bench
+    count = 1 << 16
+    g = dmm.gen_instances(dmm.KIND_SORT_U32, 32, 128, 77, count)
+    out, _ = dmm.integer_sort_general(g, 1 << 32, check=False)
+    res = bench.verify_sort_full(g, out, count)
+    assert res["ok"], res
+    bad = torch.zeros_like(out)
+    assert not bench.verify_sort_full(g, bad, count)["ok"]
+    bad = out.clone()
+    bad[5, 0, 0], bad[5, 0, 1] = out[5, 0, 1], out[5, 0, 0]
+    if int(out[5, 0, 0]) != int(out[5, 0, 1]):
+        assert not bench.verify_sort_full(g, bad, count)["ascending"]
+    bad = out.clone()
+    bad[count - 1, 31, 127] = bad[count - 1, 31, 126]
+    r = bench.verify_sort_full(g, bad, count)
+    assert not (r["sum_sumsq"] and r["xor"])

@@ -93,3 +93,20 @@ def test_shape_limits():
         S.apply_schedule(np.zeros((1, 64, 4), dtype=np.uint32), s)
     with pytest.raises(dmm.UnsupportedShape):
         S.apply_schedule(np.zeros((1, 4, 65), dtype=np.uint32), s)
+
+
+def test_round_starts_disagreeing_with_n_moves_rejected():
+    # shared memory is sized from the host's n_moves; a round_start table that ends
+    # elsewhere, does not start at 0 or is not monotone is OutOfBounds before any staging/write
+    grid = torch.arange(8, dtype=torch.int32, device="cuda").reshape(1, 4, 2)
+    keep = torch.full((1, 4, 2), -7, dtype=torch.int32, device="cuda")
+    good = S.Schedule([[S.Move(0, 0, 1, 0), S.Move(1, 0, 2, 0)], [S.Move(2, 0, 3, 0)]]).upload()
+    for starts in ([0, 2, 5], [0, 2, 1], [1, 2, 3], [0, 4, 3]):
+        ds = S.DeviceSchedule(good.moves, torch.tensor(starts, dtype=torch.int32, device="cuda"),
+                              good.n_rounds, good.n_moves)
+        out = keep.clone()
+        with pytest.raises(dmm.OutOfBounds):
+            S.apply_schedule(grid, ds, out=out)
+        assert torch.equal(out, keep)
+    out = S.apply_schedule(grid, good, out=keep.clone()).cpu().numpy()
+    assert out[0, 1, 0] == 0 and out[0, 2, 0] == 2 and out[0, 3, 0] == 4
