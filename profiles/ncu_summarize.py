@@ -81,6 +81,19 @@ def to_bytes(v, unit):
     return float(v.replace(",", "")) * scale
 
 
+def to_us(v, unit):
+    """ncu prints gpu__time_duration in whatever unit fits (nsecond / usecond / msecond / second)."""
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+             "second": 1e6, "s": 1e6}[unit]
+    return float(v.replace(",", "")) * scale
+
+
+def to_ghz(v, unit):
+    scale = {"hz": 1e-9, "khz": 1e-6, "mhz": 1e-3, "ghz": 1.0, "cycle/second": 1e-9, "cycle/nsecond": 1.0,
+             "cycle/usecond": 1e-3}[unit.lower()]
+    return float(v.replace(",", "")) * scale
+
+
 def traffic(args):
     import json
     import os
@@ -100,10 +113,10 @@ def traffic(args):
         m = raw_metrics(rep)
         rd = to_bytes(*m["dram__bytes_read.sum"])
         wr = to_bytes(*m["dram__bytes_write.sum"])
-        dur_us = float(m["gpu__time_duration.sum"][0].replace(",", ""))
+        dur_us = to_us(*m["gpu__time_duration.sum"])
         wf = float(m["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"][0].replace(",", ""))
         exc = float(m["derived__memory_l1_wavefronts_shared_excessive"][0].replace(",", ""))
-        clk = float(m["sm__cycles_elapsed.avg.per_second"][0].replace(",", ""))  # GHz
+        clk = to_ghz(*m["sm__cycles_elapsed.avg.per_second"])
         # shared memory: one wavefront moves up to 128 B; peak 128 B/clk/SM x 148 SMs
         smem_peak_gbs = 128 * 148 * clk
         out[cfg] = {"kernel": m["Kernel Name"][0][:120], "bytes_per_launch": rd + wr, "read_bytes": rd,
@@ -112,6 +125,11 @@ def traffic(args):
                     "smem_wavefront_bytes_per_launch": wf * 128, "smem_peak_gbs_at_clock": smem_peak_gbs,
                     "smem_frac_of_peak_under_ncu": (wf / (dur_us * 1e-6)) / (148 * clk * 1e9),
                     "issue_active_pct": float(m["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]),
+                    "bank_conflicts_ld": float(m["l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum"][0]
+                                               .replace(",", "")),
+                    "bank_conflicts_st": float(m["l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum"][0]
+                                               .replace(",", "")),
+                    "warp_instructions": float(m["smsp__inst_executed.sum"][0].replace(",", "")),
                     "source": os.path.join(src_dir or os.path.dirname(rep), os.path.basename(rep))}
         print(cfg, out[cfg])
     with open(path, "w") as f:
