@@ -48,6 +48,12 @@ CONFIGS = {
     "cfg3": ("integer_sort_general", 32, 128, 1 << 20, 0,
              "bank-conflict-free sort w=32, n=4096 uint32 keys per block-tile (32x128 machine), 2^20 tiles "
              "(reference path: integer_sort_general(view, 2^32))"),
+    "cfg1sw": ("partition_short_wide", 32, 1024, 1 << 13, 0,
+               "w-way partition at the paper's native mapping w=32, n=32*w^2=32768 uint32 labels per instance "
+               "(the Corollary's short-wide machine 32x1024: partition_short_wide), 2^13 instances"),
+    "cfg3sw": ("sort_short_wide", 32, 1024, 1 << 15, 0,
+               "bank-conflict-free sort w=32, n=32768 uint32 keys per instance (sort_short_wide, Lemma 1 on the "
+               "32x1024 machine), 2^15 instances"),
     "cfg5": ("global_partition", 1, 1 << 26, 8, 0,
              "global 8-way partition of 2^32 uint32 keys across 8 GPUs: 2^29 keys per GPU (label = key >> 29), "
              "local stable multisplit + NCCL all-to-all"),
@@ -59,7 +65,8 @@ CONFIGS = {
               "randomized permutation w=32, n=1024 per instance (one-warp stand-in), seeded Rng per instance, "
               "2^18 instances"),
 }
-ALG_ID = {"partition_general": 5, "integer_sort_general": 6, "permute": 7}
+ALG_ID = {"partition_general": 5, "integer_sort_general": 6, "permute": 7, "partition_short_wide": 3,
+          "sort_short_wide": 0}
 
 
 def _peaks():
@@ -162,7 +169,8 @@ def cpu_baseline(cfg_name: str, seconds: float = 15.0):
     alg, w, m, count, flags, _ = CONFIGS[cfg_name]
     note = ""
     alg_id = ALG_ID.get(alg)
-    kind = {"partition_general": 1, "integer_sort_general": 0, "permute": 2}.get(alg)
+    kind = {"partition_general": 1, "integer_sort_general": 0, "permute": 2, "partition_short_wide": 1,
+            "sort_short_wide": 0}.get(alg)
     if cfg_name == "cfg2":
         # the reference rejects 32 x 8 (balance leftover group, partition.hpp:241-244): time the
         # closest shape it accepts, general partition 32 x 16
@@ -357,7 +365,8 @@ def main():
         g = dmm.gen_keys(rank * keys_per_gpu, keys_per_gpu).view(count, w, m)
     else:
         kind = {"partition_general": dmm.KIND_PARTITION, "integer_sort_general": dmm.KIND_SORT_U32,
-                "permute": dmm.KIND_PERMUTE}[alg]
+                "permute": dmm.KIND_PERMUTE, "partition_short_wide": dmm.KIND_PARTITION,
+                "sort_short_wide": dmm.KIND_SORT_U32}[alg]
         # rank r owns instances [r*count, (r+1)*count): seeds are disjoint across ranks
         g = dmm.gen_instances(kind, w, m, 1 + rank * count, count)
     out = torch.empty_like(g)
@@ -370,6 +379,10 @@ def main():
     def step(src, dst):
         if alg == "partition_general":
             return dmm.partition_general(src, flags=flags, out=dst, check=False)
+        if alg == "partition_short_wide":
+            return dmm.partition_short_wide(src, out=dst, check=False), None
+        if alg == "sort_short_wide":
+            return dmm.sort_short_wide(src, out=dst), None
         if alg == "permute":
             return dmm.permute_into(src, dst, seeds, perm_bufs)
         if alg == "global_partition":
@@ -443,6 +456,9 @@ def main():
     if alg == "partition_general":
         rows = torch.arange(w, device="cuda", dtype=torch.int32).view(1, w, 1)
         ok = bool((out == rows).all()) and int((st.status != 0).sum()) == 0
+    elif alg == "partition_short_wide":
+        rows = torch.arange(w, device="cuda", dtype=torch.int32).view(1, w, 1)
+        ok = bool((out == rows).all())
     elif alg == "permute":
         exp = torch.arange(w * m, device="cuda", dtype=torch.int32).view(1, w, m)
         ok = bool((out == exp).all())
@@ -500,6 +516,10 @@ def main():
     def chunk_fn(din, dout, s, lo):
         if alg == "partition_general":
             dmm.partition_general(din, flags=flags, out=dout, stream=s, check=False)
+        elif alg == "partition_short_wide":
+            dmm.partition_short_wide(din, out=dout, stream=s, check=False)
+        elif alg == "sort_short_wide":
+            dmm.sort_short_wide(din, out=dout, stream=s)
         elif alg == "integer_sort_general":
             dmm.integer_sort_general(din, 1 << 32, out=dout, stream=s, check=False)
         elif alg == "permute":
@@ -559,7 +579,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
-    if alg == "partition_general":
+    if alg in ("partition_general", "partition_short_wide"):
         rows = torch.arange(w, dtype=torch.int32).view(1, w, 1)
         ok = ok and bool((h_out == rows).all())
     elif alg == "global_partition":

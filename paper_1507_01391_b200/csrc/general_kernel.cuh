@@ -288,6 +288,8 @@ dmm_status launch_general_m16(int mode, bool pk2, bool ext, const GeneralArgs& a
 dmm_status launch_general_m32(int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_m64(int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_m128(int mode, bool pk2, bool ext, const GeneralArgs& a);
+// 32 x 1024: the short-wide skeleton on a CTA of 32 warps (short_wide32.cu)
+dmm_status launch_general_m1024(int mode, bool pk2, bool ext, const GeneralArgs& a);
 // multi-warp machines (w = 64, 128, 256 rows, one per CTA), general_tall*.cu
 dmm_status launch_general_tall64(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_tall128(uint32_t m, int mode, bool pk2, bool ext, const GeneralArgs& a);

@@ -1,0 +1,378 @@
+// short_wide32.cu -- kernel 1 at the paper's native mapping: the w = 32 short-wide machine
+// (w^2 <= m; here 32 x 1024 = 32 768 keys per instance), Lemma 1 / Corollary
+// (partition.hpp:178-185, sort.hpp:200-230): two passes of {alternating row sort;
+// to_column_major; row sort; to_row_major} and a final row sort.  Serves
+// partition_short_wide, sort_short_wide, the ShortWideHook probe, and partition_general /
+// integer_sort_general / sort_wide_any at 32 x 1024 (their leaf is this skeleton,
+// partition.hpp:156-172, sort.hpp:321-330).
+//
+// Mapping: one machine per CTA of 32 warps (persistent over the batch).
+//   * DMM processor / bank r = lane r of every warp.  Thread (k, r) = warp k, lane r holds 32
+//     keys of row r in registers, so a warp-wide shared access touches 32 different rows, and
+//     every row-local structure is stored bank = row: conflict-free by construction.
+//   * to_column_major / to_row_major (layout.hpp:316-405) of a 32 x 1024 machine move element
+//     (i, 32a + b) to (b, 32i + a) and back.  With warp k holding row positions 32k..32k+31
+//     (chunk layout) before to_column_major and 32j + k (stride layout) before to_row_major,
+//     both conversions are one 32 x 32 transpose INSIDE warp k: lane i's register b <-> lane
+//     b's register i (padded per-warp slab: conflict-free).
+//   * Row sorts of labels (domain <= 32: partition_short_wide, partition_general and
+//     integer_sort_general with a small domain) are the reference's radix rows, one counting
+//     pass each (radix_sort_rows partition.hpp:37-99 with base m >= domain): per-bank
+//     counting -- thread (k, r) counts its 32 keys into its own counters in bank r --, the
+//     row's histogram summed over its 32 threads, the exclusive prefix of row r in bank r, and
+//     each thread emitting the keys of its row positions from the prefix.  The keys are the
+//     labels, so the counting sort's scatter writes runs.
+//   * Row sorts of full 32-bit keys (sort_short_wide's merge rows sort.hpp:76, integer sorts
+//     with a larger domain) are a bitonic sort of the 1024-key row across its 32 threads:
+//     stages on position bits held in registers run in registers, the others after a row
+//     exchange through shared memory (position e of row r at word 32e + r: bank r).
+//   * HBM <-> shared memory: one TMA bulk copy of the 128 KB machine each way
+//     (cp.async.bulk + mbarrier / bulk group); the next machine is prefetched into L2 while
+//     this one runs.  Threads read and write the row-major staging copy at (row r, column
+//     32j + c) with c = (k + r) mod 32: bank c, distinct across every warp.
+#include <algorithm>
+
+#include "general_kernel.cuh"
+
+namespace dmmdev {
+namespace sw32 {
+
+constexpr int kM = 1024;                  // row width
+constexpr int kWords = 32 * kM;           // machine words
+constexpr uint32_t kBytes = kWords * 4;   // 128 KB
+constexpr int kSlab = 32 * 33;            // per-warp transpose slab (padded rows)
+constexpr int kStage = 32 * kSlab;        // staging / exchange / counters / slabs (>= kWords)
+constexpr int kPre = 33 * 32;             // row prefixes P[l * 32 + r], l = 0..32
+constexpr size_t kSmemBytes = size_t(kStage + kPre) * 4 + 16;
+
+__device__ __forceinline__ uint32_t sptr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sptr(bar)) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load(uint32_t* dst, const uint32_t* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sptr(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(sptr(dst)), "l"(src), "r"(bytes), "r"(sptr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(sptr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store(uint32_t* dst, const uint32_t* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sptr(src)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2(const uint32_t* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// to_column_major / to_row_major on this mapping: lane i's register b <-> lane b's register i
+// inside the warp (slab row b padded to 33 words: the store hits bank (b + i) mod 32, the load
+// bank (i' + b) mod 32)
+__device__ __forceinline__ void warp_transpose(uint32_t (&x)[32], uint32_t* slab, int lane) {
+#pragma unroll
+    for (int b = 0; b < 32; ++b)
+        slab[b * 33 + lane] = x[b];
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+        x[i] = slab[lane * 33 + i];
+    __syncwarp();
+}
+
+// Counting row sort (radix_sort_rows with one pass, partition.hpp:37-99): thread (k, r)
+// emits row r's sorted keys at positions base + step * j (chunk: base 32k, step 1; stride:
+// base c, step 32).  desc: the row descends (SortOrder), i.e. it is the ascending run
+// sequence of the complemented labels 31 - l.  Keys are < 32 (clamped by the caller).
+__device__ __forceinline__ void count_row_sort(uint32_t (&x)[32], uint32_t* S, uint32_t* P, int k, int r, bool desc,
+                                               uint32_t base, uint32_t step) {
+    uint32_t* cnt = S + k * kM + r;  // this thread's counters cnt[32 l]: bank r
+    __syncthreads();                 // S is free (the previous phase's readers are done)
+#pragma unroll
+    for (int l = 0; l < 32; ++l)
+        cnt[l * 32] = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+        atomicAdd(cnt + x[j] * 32, 1u);
+    __syncthreads();
+    // label k's count in row r: sum over the row's 32 threads
+    uint32_t h = 0;
+    const uint32_t* col = S + k * 32 + r;
+#pragma unroll
+    for (int kk = 0; kk < 32; ++kk)
+        h += col[kk * kM];
+    P[k * 32 + r] = h;
+    __syncthreads();
+    if (k == 0) {
+        // exclusive prefix of row r in the row's own order (complemented labels if desc)
+        uint32_t t[32];
+#pragma unroll
+        for (int l = 0; l < 32; ++l)
+            t[l] = P[l * 32 + r];
+        uint32_t s = 0;
+#pragma unroll
+        for (int l = 0; l < 32; ++l) {
+            P[l * 32 + r] = s;
+            s += desc ? t[31 - l] : t[l];
+        }
+        P[32 * 32 + r] = s;  // = m
+    }
+    __syncthreads();
+    const uint32_t* pr = P + r;
+    int l = 0;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1)
+        if (pr[(l + s) * 32] <= base)
+            l += s;
+    uint32_t nb = pr[(l + 1) * 32];
+    const uint32_t dm = desc ? 31u : 0u;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t q = base + step * j;
+        while (q >= nb) {
+            ++l;
+            nb = pr[(l + 1) * 32];
+        }
+        x[j] = (uint32_t)l ^ dm;
+    }
+}
+
+// row exchanges through S (position e of row r at word 32e + r): chunk (e = 32k + j) <->
+// stride (e = 32j + c)
+__device__ __forceinline__ void chunk_to_stride(uint32_t (&x)[32], uint32_t* S, int k, int r, int c) {
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+        S[k * kM + j * 32 + r] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+        x[j] = S[c * 32 + r + j * kM];
+}
+__device__ __forceinline__ void stride_to_chunk(uint32_t (&x)[32], uint32_t* S, int k, int r) {
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+        S[k * 32 + r + j * kM] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+        x[j] = S[k * kM + j * 32 + r];
+}
+
+// one bitonic merge level L (6..10) of the 1024-key row sort, entered and left in chunk layout
+template <int L>
+__device__ __forceinline__ void bitonic_level(uint32_t (&x)[32], uint32_t* S, int k, int r) {
+    chunk_to_stride(x, S, k, r, k);
+    // stride: position bits L-1..5 = register bits L-6..0; block direction = position bit L
+    // = register bit L-5 (the last level ascends)
+    reg_stages<1, 0, 32, L - 6, (L < 10 ? L - 5 : -1)>(x);
+    stride_to_chunk(x, S, k, r);
+    // chunk: position bits 4..0 = register bits; direction = position bit L = warp bit L-5
+    const uint32_t f = (L < 10 && ((k >> (L - 5)) & 1)) ? 0xFFFFFFFFu : 0u;
+    flip<0, 32>(x, f);
+    reg_stages<1, 0, 32, 4, -1>(x);
+    flip<0, 32>(x, f);
+}
+
+// comparison row sort of row r (1024 keys over the row's 32 threads), chunk layout in and out
+__device__ __forceinline__ void bitonic_row_sort(uint32_t (&x)[32], uint32_t* S, int k, int r, bool desc) {
+    const uint32_t fr = desc ? 0xFFFFFFFFu : 0u;  // x ^ ~0 reverses the order
+    const uint32_t f0 = (k & 1) ? 0xFFFFFFFFu : 0u;
+    flip<0, 32>(x, fr ^ f0);
+    sort_net<1, 0, 32>(x);  // levels 1..5: the thread's 32 positions, direction = warp bit 0
+    flip<0, 32>(x, f0);
+    bitonic_level<6>(x, S, k, r);
+    bitonic_level<7>(x, S, k, r);
+    bitonic_level<8>(x, S, k, r);
+    bitonic_level<9>(x, S, k, r);
+    bitonic_level<10>(x, S, k, r);
+    flip<0, 32>(x, fr);
+}
+
+// a ShortWideHook snapshot of the machine from the registers, row-major into dst:
+// stride = false: thread (k, r) holds row r positions 32k + j; true: positions 32j + c
+__device__ __forceinline__ void snap(uint32_t* dst, const uint32_t (&x)[32], int k, int r, bool stride, int c) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+        dst[r * kM + (stride ? 32 * j + c : 32 * k + j)] = x[j];
+}
+
+// COUNT: label row sorts (domain <= 32); else comparison row sorts.  CHECK_PART: the
+// partition instance check (check_partition_instance partition.hpp:112-124); otherwise keys
+// >= domain are KeyOutOfRange (integer sorts).
+template <bool COUNT, int MODE>
+__global__ void __launch_bounds__(1024, 1)
+    k_short_wide32(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count, uint64_t domain,
+                   int ascending, dmm_general_stats* __restrict__ stats, uint8_t* __restrict__ status,
+                   uint32_t* __restrict__ probe) {
+    extern __shared__ __align__(128) uint32_t smem[];
+    uint32_t* S = smem;
+    uint32_t* P = smem + kStage;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(P + kPre);
+    const int tid = threadIdx.x, k = tid >> 5, r = tid & 31;
+    const bool asc = ascending != 0;
+    const bool part = MODE == kModePartition || (MODE == kModeSortAny && domain < (1ull << 32));
+    const int c = (k + r) & 31;  // rotated stride column: bank c on the row-major staging copy
+    uint32_t* slab = S + k * kSlab;
+    if (tid == 0)
+        mbar_init(bar);
+    __syncthreads();
+    uint32_t parity = 0;
+    for (uint64_t inst = blockIdx.x; inst < count; inst += gridDim.x) {
+        if (tid == 0) {
+            bulk_wait_read();  // the previous machine's store has read S
+            const uint64_t nxt = inst + gridDim.x;
+            if (nxt < count)
+                prefetch_l2(in + nxt * kWords, kBytes);
+            tma_load(S, in + inst * kWords, kBytes, bar);
+        }
+        mbar_wait(bar, parity);
+        parity ^= 1;
+        uint32_t x[32];
+        {
+            const uint32_t* src = S + r * kM + c;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                x[j] = src[32 * j];
+        }
+        // keys outside [0, domain); labels are clamped to 31 for the counters
+        uint32_t bad = 0;
+        if (domain < (1ull << 32)) {
+            const uint32_t d = (uint32_t)domain;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                bad |= x[j] >= d ? 1u : 0u;
+                if constexpr (COUNT)
+                    x[j] = min(x[j], 31u);
+            }
+        }
+        bad = __syncthreads_or(bad);  // (also: every thread has read its staging words)
+        uint32_t* snaps = probe != nullptr ? probe + inst * 3 * kWords : nullptr;
+
+        for (int pass = 0; pass < 2; ++pass) {
+            // alternating row sort (SortOrder::alternating(asc)), chunk layout out
+            const bool desc_alt = ((r & 1) == 0) != asc;
+            if constexpr (COUNT)
+                count_row_sort(x, S, P, k, r, desc_alt, 32u * k, 1u);
+            else
+                bitonic_row_sort(x, S, k, r, desc_alt);
+            __syncthreads();  // S -> slabs
+            warp_transpose(x, slab, r);  // to_column_major
+            if (pass == 0 && snaps)
+                snap(snaps, x, k, r, true, k);  // after_first_convert: row r, positions 32j + k
+            // row sort (asc or desc), stride layout out
+            if constexpr (COUNT) {
+                count_row_sort(x, S, P, k, r, !asc, (uint32_t)k, 32u);
+            } else {
+                bitonic_row_sort(x, S, k, r, !asc);
+                chunk_to_stride(x, S, k, r, k);
+            }
+            __syncthreads();
+            warp_transpose(x, slab, r);  // to_row_major: chunk layout out
+            if (pass == 0 && snaps)
+                snap(snaps + kWords, x, k, r, false, 0);  // after_first_pass
+        }
+        // final row sort, rotated stride layout (positions 32j + c) for the staging copy
+        if constexpr (COUNT) {
+            count_row_sort(x, S, P, k, r, !asc, (uint32_t)c, 32u);
+        } else {
+            bitonic_row_sort(x, S, k, r, !asc);
+            chunk_to_stride(x, S, k, r, c);
+        }
+        if (snaps)
+            snap(snaps + 2 * kWords, x, k, r, true, c);  // done
+        uint32_t mism = 0;
+        if (part) {
+            // labels in [0, w) with m copies each <=> the sorted machine has row i = i
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                mism |= x[j] ^ (uint32_t)r;
+        }
+        __syncthreads();  // S free
+        {
+            uint32_t* dst = S + r * kM + c;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                dst[32 * j] = x[j];
+        }
+        fence_async_smem();
+        const uint32_t invalid = __syncthreads_or(mism != 0) | bad;
+        if (tid == 0) {
+            tma_store(out + inst * kWords, S, kBytes);
+            uint8_t s = DMM_OK;
+            if (part && invalid)
+                s = DMM_INVALID_INSTANCE;
+            else if (bad)
+                s = DMM_KEY_OUT_OF_RANGE;
+            if (status)
+                status[inst] = s;
+            if (stats) {
+                stats[inst].cleanup_retries = 0;  // w <= m: partition_leaf only
+                stats[inst].sorted = 1;
+            }
+        }
+    }
+    if (tid == 0)
+        bulk_wait_all();
+}
+
+}  // namespace sw32
+}  // namespace dmmdev
+
+namespace dmmhost {
+
+namespace {
+template <bool COUNT, int MODE>
+dmm_status launch_sw32(const GeneralArgs& a) {
+    auto kern = dmmdev::sw32::k_short_wide32<COUNT, MODE>;
+    static std::atomic<uint64_t> configured{0};
+    if (dmm_status e = configure_kernel(kern, dmmdev::sw32::kSmemBytes, configured); e != DMM_OK)
+        return e;
+    if (a.count == 0)
+        return DMM_OK;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t grid = std::min<uint64_t>(a.count, uint64_t(sms));
+    kern<<<unsigned(grid), 1024, dmmdev::sw32::kSmemBytes, a.stream>>>(a.in, a.out, a.count, a.domain, a.ascending,
+                                                                       a.stats, a.status, a.probe);
+    return check_launch("k_short_wide32");
+}
+}  // namespace
+
+// 32 x 1024 machines: every entry point's leaf is the short-wide skeleton (w^2 <= m)
+dmm_status launch_general_m1024(int mode, bool /*pk2*/, bool ext, const GeneralArgs& a) {
+    if (ext) {
+        set_error("extension kernels are only built where the reference rejects the shape");
+        return DMM_UNSUPPORTED_SHAPE;
+    }
+    if (a.probe && a.probe_max != 3) {
+        set_error("32 x 1024 machines capture the three ShortWideHook stages only");
+        return DMM_INVALID_ARGUMENT;
+    }
+    const bool count = a.domain <= 32;
+    switch (mode) {
+        case dmmdev::kModePartition:
+            return launch_sw32<true, dmmdev::kModePartition>(a);
+        case dmmdev::kModeIntegerSort:
+            return count ? launch_sw32<true, dmmdev::kModeIntegerSort>(a)
+                         : launch_sw32<false, dmmdev::kModeIntegerSort>(a);
+        default:
+            return count ? launch_sw32<true, dmmdev::kModeSortAny>(a) : launch_sw32<false, dmmdev::kModeSortAny>(a);
+    }
+}
+
+}  // namespace dmmhost

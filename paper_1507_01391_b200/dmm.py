@@ -299,6 +299,22 @@ def partition_short_wide(grid, *, out=None, stream=None, check: bool = True):
     return _partition_entry("partition_short_wide", grid, out, stream, check)
 
 
+def short_wide_probe(grid, *, partition: bool, ascending: bool = True, stream=None, check: bool = True):
+    """The ShortWideHook stages (sort.hpp:189-218) of partition_short_wide (partition=True) or
+    sort_short_wide(ascending): -> (result [count, w, m], snapshots [count, 3, w, m]) with the
+    machine after_first_convert, after_first_pass and done."""
+    t, single = _as_batch(grid)
+    count, w, m = t.shape
+    res = torch.empty_like(t)
+    snaps = torch.empty((count, 3, w, m), dtype=torch.int32, device=t.device)
+    status = torch.zeros((count,), dtype=torch.uint8, device=t.device)
+    _check(lib().dmm_short_wide_probe(t.data_ptr(), res.data_ptr(), w, m, count, int(partition), int(ascending),
+                                      status.data_ptr(), snaps.data_ptr(), _stream(stream)), "short_wide_probe")
+    if check:
+        _raise_first(status, "short_wide_probe")
+    return (res[0], snaps[0]) if single else (res, snaps)
+
+
 # --------------------------------------------------------------------------------------
 # Comparison sorts (sort.hpp) and layout primitives (layout.hpp)
 # --------------------------------------------------------------------------------------

@@ -312,7 +312,10 @@ static void run_algorithm_cases() {
                           {Algorithm::partition_general, 32, 64}, {Algorithm::integer_sort_general, 32, 128},
                           {Algorithm::sort_short_wide, 4, 16}, {Algorithm::sort_tall, 128, 32},
                           {Algorithm::permute, 32, 32}, {Algorithm::permute, 128, 64},
-                          {Algorithm::partition_general, 64, 32}, {Algorithm::integer_sort_general, 64, 8}};
+                          {Algorithm::partition_general, 64, 32}, {Algorithm::integer_sort_general, 64, 8},
+                          // the w = 32 short-wide machine (32 x 1024: the CTA kernel, short_wide32.cu)
+                          {Algorithm::partition_short_wide, 32, 1024}, {Algorithm::partition_general, 32, 1024},
+                          {Algorithm::integer_sort_general, 32, 1024}};
     for (const Case& c : cases) {
         for (u64 seed = 1; seed <= 3; ++seed) {
             Instance in = gen_instance(instance_kind_for(c.a), c.w, c.m, seed);
@@ -348,7 +351,7 @@ static void run_algorithm_cases() {
 
 // ShortWideHook (sort.hpp:189-218): the same three calls with the same machine contents
 static void short_wide_hook_cases() {
-    for (auto [w, m] : {std::pair<u32, u32>{8, 64}, {4, 16}, {2, 8}, {3, 9}}) {
+    for (auto [w, m] : {std::pair<u32, u32>{8, 64}, {4, 16}, {2, 8}, {3, 9}, {32, 1024}}) {
         for (int part = 0; part < 2; ++part) {
             for (bool asc : {true, false}) {
                 if (part && !asc)
