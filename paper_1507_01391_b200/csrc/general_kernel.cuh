@@ -42,6 +42,19 @@ __device__ __forceinline__ void store_row(uint32_t* __restrict__ p, const uint32
 
 enum : int { kModeIntegerSort = 0, kModePartition = 1, kModeSortAny = 2 };
 
+// Bank-conflict attribution build (-DDMM_NO_GLOBAL_IO, profiles/r02/conflicts_ab.sh): the batch
+// kernels synthesise their keys in registers instead of loading them, and their stores are
+// predicated off at run time (count == ~0 never holds), so the L1 data banks serve shared
+// memory only.  Not a product build: its outputs are garbage.
+#ifdef DMM_NO_GLOBAL_IO
+constexpr bool kIoOff = true;
+#else
+constexpr bool kIoOff = false;
+#endif
+__device__ __forceinline__ uint32_t synth_key(uint64_t k, int row, int c) {
+    return (uint32_t)((k * 0x9E3779B9ull + (uint64_t)row * 0x85EBCA6Bu + (uint64_t)c * 0xC2B2AE35u) >> 7) & 31u;
+}
+
 // CTA shape: warps per CTA and the occupancy target handed to ptxas (register cap)
 template <int M, int PK, int WM = kWarp>
 constexpr int warps_per_block() { return WM > kWarp ? WM / kWarp : (M >= 128 ? 4 : 8); }
@@ -95,6 +108,12 @@ __global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_
 #pragma unroll
             for (int c = 0; c < M; ++c)
                 v[c] = 0;
+            return;
+        }
+        if constexpr (kIoOff) {
+#pragma unroll
+            for (int c = 0; c < M; ++c)
+                v[c] = synth_key(k, row, c);
             return;
         }
         if constexpr (kAnyLayout) {
@@ -202,6 +221,8 @@ __global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_
     for (int h = 0; h < PK; ++h) {
         const uint64_t k = inst_of(h);
         if (k >= count || !live_lane)
+            continue;
+        if (kIoOff && count != ~0ull)
             continue;
         if constexpr (M % 4 == 0) {
             // unpack one 16-byte vector at a time (register budget)

@@ -26,10 +26,12 @@
 //     with a larger domain) are a bitonic sort of the 1024-key row across its 32 threads:
 //     stages on position bits held in registers run in registers, the others after a row
 //     exchange through shared memory (position e of row r at word 32e + r: bank r).
-//   * HBM <-> shared memory: one TMA bulk copy of the 128 KB machine each way
-//     (cp.async.bulk + mbarrier / bulk group); the next machine is prefetched into L2 while
-//     this one runs.  Threads read and write the row-major staging copy at (row r, column
-//     32j + c) with c = (k + r) mod 32: bank c, distinct across every warp.
+//   * HBM -> shared memory: one TMA bulk copy of the 128 KB machine (cp.async.bulk +
+//     mbarrier), issued for the next machine as soon as the current one stops reading shared
+//     memory (its final row sort's count phase), after an L2 prefetch of it at the start of the
+//     current machine.  Threads read the row-major staging copy at (row r, column 32j + c)
+//     with c = (k + r) mod 32: bank c, distinct across every warp.  The result leaves from
+//     the registers (chunk layout: row r, columns 32k .. 32k + 31, 16-byte stores).
 #include <algorithm>
 
 #include "general_kernel.cuh"
@@ -42,7 +44,7 @@ constexpr int kWords = 32 * kM;           // machine words
 constexpr uint32_t kBytes = kWords * 4;   // 128 KB
 constexpr int kSlab = 32 * 33;            // per-warp transpose slab (padded rows)
 constexpr int kStage = 32 * kSlab;        // staging / exchange / counters / slabs (>= kWords)
-constexpr int kPre = 33 * 32;             // row prefixes P[l * 32 + r], l = 0..32
+constexpr int kPre = 2 * 32 * 32;         // row run tables E[l * 32 + r], NX[l * 32 + r]
 constexpr size_t kSmemBytes = size_t(kStage + kPre) * 4 + 16;
 
 __device__ __forceinline__ uint32_t sptr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -66,13 +68,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void tma_store(uint32_t* dst, const uint32_t* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sptr(src)), "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void prefetch_l2(const uint32_t* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
@@ -93,13 +88,21 @@ __device__ __forceinline__ void warp_transpose(uint32_t (&x)[32], uint32_t* slab
 }
 
 // Counting row sort (radix_sort_rows with one pass, partition.hpp:37-99): thread (k, r)
-// emits row r's sorted keys at positions base + step * j (chunk: base 32k, step 1; stride:
-// base c, step 32).  desc: the row descends (SortOrder), i.e. it is the ascending run
-// sequence of the complemented labels 31 - l.  Keys are < 32 (clamped by the caller).
-__device__ __forceinline__ void count_row_sort(uint32_t (&x)[32], uint32_t* S, uint32_t* P, int k, int r, bool desc,
-                                               uint32_t base, uint32_t step) {
+// emits row r's sorted keys at its chunk positions 32k .. 32k + 31.  desc: the row descends
+// (SortOrder), i.e. it is the ascending run sequence of the complemented labels 31 - l.
+// Keys are < 32 (clamped by the caller).  `after_count` runs once S is no longer read (the
+// caller may start the next machine's TMA load into S there).
+//
+// Per row r the run tables live in bank r: E[l] = end of run l (row order), NX[l] = (n << 16) |
+// E[n] for the next non-empty run n after l.  A thread finds the run holding its first
+// position by binary search on E, then walks its 32 consecutive positions: a position crosses
+// at most one run boundary (runs on the walk are non-empty), so the walk is a compare, two
+// selects and a predicated table load per key -- no divergent loop.
+template <class AfterCount>
+__device__ __forceinline__ void count_row_sort(uint32_t (&x)[32], uint32_t* S, uint32_t* E, uint32_t* NX, int k, int r,
+                                               bool desc, AfterCount&& after_count) {
     uint32_t* cnt = S + k * kM + r;  // this thread's counters cnt[32 l]: bank r
-    __syncthreads();                 // S is free (the previous phase's readers are done)
+    __syncthreads();                 // S and the tables are free (the previous phase is done)
 #pragma unroll
     for (int l = 0; l < 32; ++l)
         cnt[l * 32] = 0;
@@ -107,45 +110,58 @@ __device__ __forceinline__ void count_row_sort(uint32_t (&x)[32], uint32_t* S, u
     for (int j = 0; j < 32; ++j)
         atomicAdd(cnt + x[j] * 32, 1u);
     __syncthreads();
-    // label k's count in row r: sum over the row's 32 threads
+    // label k's count in row r: sum over the row's 32 threads (the count matrix transposed:
+    // thread (k, r) reads column k of row r's counters, all in bank r)
     uint32_t h = 0;
     const uint32_t* col = S + k * 32 + r;
 #pragma unroll
     for (int kk = 0; kk < 32; ++kk)
         h += col[kk * kM];
-    P[k * 32 + r] = h;
+    E[k * 32 + r] = h;
     __syncthreads();
+    after_count();
     if (k == 0) {
-        // exclusive prefix of row r in the row's own order (complemented labels if desc)
+        // run ends and next-non-empty links of row r, in the row's order
         uint32_t t[32];
 #pragma unroll
         for (int l = 0; l < 32; ++l)
-            t[l] = P[l * 32 + r];
-        uint32_t s = 0;
+            t[l] = E[(desc ? 31 - l : l) * 32 + r];
+        uint32_t sum = 0;
 #pragma unroll
         for (int l = 0; l < 32; ++l) {
-            P[l * 32 + r] = s;
-            s += desc ? t[31 - l] : t[l];
+            sum += t[l];
+            t[l] = sum;  // end of run l
+            E[l * 32 + r] = sum;
         }
-        P[32 * 32 + r] = s;  // = m
+        uint32_t nxt = (32u << 16) | kM;
+#pragma unroll
+        for (int l = 31; l >= 0; --l) {
+            NX[l * 32 + r] = nxt;
+            const uint32_t start = l ? t[l - 1] : 0u;
+            if (t[l] > start)
+                nxt = ((uint32_t)l << 16) | t[l];
+        }
     }
     __syncthreads();
-    const uint32_t* pr = P + r;
-    int l = 0;
+    const uint32_t base = 32u * (uint32_t)k;
+    const uint32_t* er = E + r;
+    const uint32_t* nr = NX + r;
+    int cur = 0;  // first run whose end exceeds base
 #pragma unroll
     for (int s = 16; s >= 1; s >>= 1)
-        if (pr[(l + s) * 32] <= base)
-            l += s;
-    uint32_t nb = pr[(l + 1) * 32];
+        if (er[(cur + s - 1) * 32] <= base)
+            cur += s;
+    uint32_t e = er[cur * 32];
+    uint32_t jn = nr[cur * 32];
     const uint32_t dm = desc ? 31u : 0u;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-        const uint32_t q = base + step * j;
-        while (q >= nb) {
-            ++l;
-            nb = pr[(l + 1) * 32];
-        }
-        x[j] = (uint32_t)l ^ dm;
+        const bool cross = base + j >= e;
+        cur = cross ? (int)(jn >> 16) : cur;
+        e = cross ? (jn & 0xFFFFu) : e;
+        const uint32_t jn2 = nr[cur * 32];
+        jn = cross ? jn2 : jn;
+        x[j] = (uint32_t)cur ^ dm;
     }
 }
 
@@ -210,9 +226,9 @@ __device__ __forceinline__ void snap(uint32_t* dst, const uint32_t (&x)[32], int
         dst[r * kM + (stride ? 32 * j + c : 32 * k + j)] = x[j];
 }
 
-// COUNT: label row sorts (domain <= 32); else comparison row sorts.  CHECK_PART: the
-// partition instance check (check_partition_instance partition.hpp:112-124); otherwise keys
-// >= domain are KeyOutOfRange (integer sorts).
+// COUNT: label row sorts (domain <= 32); else comparison row sorts.  Partition semantics
+// (check_partition_instance partition.hpp:112-124) for MODE partition and for the probe of
+// partition_short_wide (sort-any with domain w); otherwise keys >= domain are KeyOutOfRange.
 template <bool COUNT, int MODE>
 __global__ void __launch_bounds__(1024, 1)
     k_short_wide32(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count, uint64_t domain,
@@ -220,25 +236,32 @@ __global__ void __launch_bounds__(1024, 1)
                    uint32_t* __restrict__ probe) {
     extern __shared__ __align__(128) uint32_t smem[];
     uint32_t* S = smem;
-    uint32_t* P = smem + kStage;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(P + kPre);
+    uint32_t* E = smem + kStage;
+    uint32_t* NX = E + 32 * 32;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kStage + kPre);
     const int tid = threadIdx.x, k = tid >> 5, r = tid & 31;
     const bool asc = ascending != 0;
     const bool part = MODE == kModePartition || (MODE == kModeSortAny && domain < (1ull << 32));
     const int c = (k + r) & 31;  // rotated stride column: bank c on the row-major staging copy
     uint32_t* slab = S + k * kSlab;
-    if (tid == 0)
+    if (tid == 0) {
         mbar_init(bar);
+        if (blockIdx.x < count)
+            tma_load(S, in + (uint64_t)blockIdx.x * kWords, kBytes, bar);
+    }
     __syncthreads();
     uint32_t parity = 0;
     for (uint64_t inst = blockIdx.x; inst < count; inst += gridDim.x) {
-        if (tid == 0) {
-            bulk_wait_read();  // the previous machine's store has read S
-            const uint64_t nxt = inst + gridDim.x;
-            if (nxt < count)
-                prefetch_l2(in + nxt * kWords, kBytes);
-            tma_load(S, in + inst * kWords, kBytes, bar);
-        }
+        const uint64_t nxt = inst + gridDim.x;
+        if (tid == 0 && nxt < count)
+            prefetch_l2(in + nxt * kWords, kBytes);
+        // the next machine's load into S, once this machine no longer reads S
+        auto load_next = [&]() {
+            if (tid == 0 && nxt < count) {
+                fence_async_smem();
+                tma_load(S, in + nxt * kWords, kBytes, bar);
+            }
+        };
         mbar_wait(bar, parity);
         parity ^= 1;
         uint32_t x[32];
@@ -261,39 +284,40 @@ __global__ void __launch_bounds__(1024, 1)
         }
         bad = __syncthreads_or(bad);  // (also: every thread has read its staging words)
         uint32_t* snaps = probe != nullptr ? probe + inst * 3 * kWords : nullptr;
+        auto nothing = []() {};
 
         for (int pass = 0; pass < 2; ++pass) {
             // alternating row sort (SortOrder::alternating(asc)), chunk layout out
             const bool desc_alt = ((r & 1) == 0) != asc;
             if constexpr (COUNT)
-                count_row_sort(x, S, P, k, r, desc_alt, 32u * k, 1u);
+                count_row_sort(x, S, E, NX, k, r, desc_alt, nothing);
             else
                 bitonic_row_sort(x, S, k, r, desc_alt);
             __syncthreads();  // S -> slabs
             warp_transpose(x, slab, r);  // to_column_major
             if (pass == 0 && snaps)
                 snap(snaps, x, k, r, true, k);  // after_first_convert: row r, positions 32j + k
-            // row sort (asc or desc), stride layout out
-            if constexpr (COUNT) {
-                count_row_sort(x, S, P, k, r, !asc, (uint32_t)k, 32u);
-            } else {
+            // row sort (asc or desc) into the stride layout to_row_major takes
+            if constexpr (COUNT)
+                count_row_sort(x, S, E, NX, k, r, !asc, nothing);
+            else
                 bitonic_row_sort(x, S, k, r, !asc);
-                chunk_to_stride(x, S, k, r, k);
-            }
+            chunk_to_stride(x, S, k, r, k);
             __syncthreads();
             warp_transpose(x, slab, r);  // to_row_major: chunk layout out
             if (pass == 0 && snaps)
                 snap(snaps + kWords, x, k, r, false, 0);  // after_first_pass
         }
-        // final row sort, rotated stride layout (positions 32j + c) for the staging copy
+        // final row sort, chunk layout; the next machine streams into S meanwhile
         if constexpr (COUNT) {
-            count_row_sort(x, S, P, k, r, !asc, (uint32_t)c, 32u);
+            count_row_sort(x, S, E, NX, k, r, !asc, load_next);
         } else {
             bitonic_row_sort(x, S, k, r, !asc);
-            chunk_to_stride(x, S, k, r, c);
+            __syncthreads();
+            load_next();
         }
         if (snaps)
-            snap(snaps + 2 * kWords, x, k, r, true, c);  // done
+            snap(snaps + 2 * kWords, x, k, r, false, 0);  // done
         uint32_t mism = 0;
         if (part) {
             // labels in [0, w) with m copies each <=> the sorted machine has row i = i
@@ -301,32 +325,22 @@ __global__ void __launch_bounds__(1024, 1)
             for (int j = 0; j < 32; ++j)
                 mism |= x[j] ^ (uint32_t)r;
         }
-        __syncthreads();  // S free
-        {
-            uint32_t* dst = S + r * kM + c;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                dst[32 * j] = x[j];
-        }
-        fence_async_smem();
+        store_row<32>(out + inst * kWords + r * kM + 32 * k, x);
         const uint32_t invalid = __syncthreads_or(mism != 0) | bad;
         if (tid == 0) {
-            tma_store(out + inst * kWords, S, kBytes);
-            uint8_t s = DMM_OK;
+            uint8_t st = DMM_OK;
             if (part && invalid)
-                s = DMM_INVALID_INSTANCE;
+                st = DMM_INVALID_INSTANCE;
             else if (bad)
-                s = DMM_KEY_OUT_OF_RANGE;
+                st = DMM_KEY_OUT_OF_RANGE;
             if (status)
-                status[inst] = s;
+                status[inst] = st;
             if (stats) {
                 stats[inst].cleanup_retries = 0;  // w <= m: partition_leaf only
                 stats[inst].sorted = 1;
             }
         }
     }
-    if (tid == 0)
-        bulk_wait_all();
 }
 
 }  // namespace sw32

@@ -68,6 +68,12 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
         const bool dom_pow2 = (domain & (domain - 1)) == 0;
         const uint32_t dom_mask = dom32 && dom_pow2 ? ~(uint32_t)(domain - 1) : 0u;
         auto load = [&](uint64_t t, uint32_t (&v)[32]) -> uint32_t {
+            if constexpr (kIoOff) {
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                    v[c] = synth_key(t, threadIdx.x, c) * 0x9E3779B9u;
+                return 0u;
+            }
             const uint4* q = reinterpret_cast<const uint4*>(in + t * (32 * M)) + warp * 256 + lane;
             uint32_t acc_or = 0, acc_max = 0;
 #pragma unroll
@@ -170,6 +176,8 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
 #pragma unroll
     for (int h = 0; h < PK; ++h) {
         if (h == 1 && !hasB)
+            break;
+        if (kIoOff && count != ~0ull)
             break;
         const uint64_t k = tile0 + h;
         uint32_t v[32];
