@@ -351,9 +351,28 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU over NCCL; DMM_BENCH_BACKEND=gloo runs the same sharded path with
+    # several ranks on one GPU (tests/test_gpu_multiproc.py: no kernel waits on another rank)
+    backend = os.environ.get("DMM_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+
+    def all_reduce(t, op=dist.ReduceOp.SUM):
+        # gloo reduces host tensors; NCCL device tensors
+        if world == 1:
+            return t
+        if backend == "nccl":
+            dist.all_reduce(t, op=op)
+            return t
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+        return t
 
     alg, w, m, count, flags, desc = CONFIGS[args.config]
     if args.count:
@@ -448,9 +467,7 @@ def main():
         st = st_graph
     ms = e0.elapsed_time(e1) / args.steps
     barrier()
-    t = torch.tensor([ms], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = all_reduce(torch.tensor([ms], device="cuda"), dist.ReduceOp.MAX)
     ms_max = float(t.item())
     # correctness of the timed output (verify_partition_result instance.hpp:249)
     if alg == "partition_general":
@@ -486,21 +503,15 @@ def main():
             lab_in = srcl >> 29
             sums = torch.zeros(8, dtype=torch.int64, device="cuda").index_add_(0, lab_in, srcl)
             cnts = torch.bincount(lab_in, minlength=8)
-            dist.all_reduce(sums)
-            dist.all_reduce(cnts)
+            all_reduce(sums)
+            all_reduce(cnts)
             rl = res.view(-1).to(torch.int64) & 0xFFFFFFFF
             got = torch.zeros(8, dtype=torch.int64, device="cuda").index_add_(0, rl >> 29, rl)
             gotc = torch.bincount(rl >> 29, minlength=8)
             ok = ok and bool((got[lo:hi] == sums[lo:hi]).all()) and bool((gotc[lo:hi] == cnts[lo:hi]).all())
             del srcl, lab_in, rl
-        n_recv = torch.tensor([res.numel()], device="cuda", dtype=torch.int64)
-        if world > 1:
-            dist.all_reduce(n_recv)
+        n_recv = all_reduce(torch.tensor([res.numel()], device="cuda", dtype=torch.int64))
         ok = ok and int(n_recv.item()) == keys_per_gpu * world
-        if world > 1:
-            okt = torch.tensor([int(ok)], device="cuda")
-            dist.all_reduce(okt, op=dist.ReduceOp.MIN)
-            ok = bool(okt.item())
     else:
         full_check = verify_sort_full(g, out, count)
         ok = full_check["ok"]
@@ -575,9 +586,7 @@ def main():
         ee1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = ee0.elapsed_time(ee1) / e2e_steps
-    t = torch.tensor([e2e_ms], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = all_reduce(torch.tensor([e2e_ms], device="cuda"), dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
     if alg in ("partition_general", "partition_short_wide"):
         rows = torch.arange(w, dtype=torch.int32).view(1, w, 1)
@@ -590,6 +599,11 @@ def main():
         if world == 1:
             ok = ok and bool((lab[1:] >= lab[:-1]).all())
 
+    # every rank's verdict (its own instances / received keys), and the seed range each rank
+    # generated its instances from (disjoint shards)
+    ok = bool(all_reduce(torch.tensor([int(ok)], device="cuda"), dist.ReduceOp.MIN).item())
+    seed_ranges = [[1 + r * count, (r + 1) * count] for r in range(world)] if alg != "global_partition" else \
+        [[r * keys_per_gpu, (r + 1) * keys_per_gpu] for r in range(world)]
     if rank == 0:
         peaks, peak_kind = _peaks()
         total_keys = keys_per_gpu * world
@@ -617,6 +631,8 @@ def main():
         }
         if full_check is not None:
             line["full_size_check"] = full_check
+        line["config"]["shards"] = {"backend": backend if world > 1 else None,
+                                    ("seed_ranges" if alg != "global_partition" else "key_index_ranges"): seed_ranges}
         if not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = cpu_baseline(args.config)

@@ -174,7 +174,12 @@ def global_partition_p2p(keys: torch.Tensor, peers: PeerBuffers, nbuckets: int =
     world = peers.world
     if world > 1:
         all_counts = torch.empty((world, nbuckets), dtype=torch.int64, device=dev)
-        dist.all_gather_into_tensor(all_counts, counts, group=group)
+        if dist.get_backend(group) == "gloo":  # host collective (several ranks on one GPU in tests)
+            h = torch.empty((world, nbuckets), dtype=torch.int64)
+            dist.all_gather_into_tensor(h, counts.cpu(), group=group)
+            all_counts.copy_(h)
+        else:
+            dist.all_gather_into_tensor(all_counts, counts, group=group)
     else:
         all_counts = counts.view(1, -1)
     recv = recv_counts(all_counts).tolist()  # the one host sync: sizes for the capacity check
