@@ -4,6 +4,9 @@
 
 #include "capi_common.h"
 #include "dmm_algos.cuh"
+#include "tma.cuh"
+
+#include <algorithm>
 
 namespace dmmdev {
 
@@ -74,8 +77,21 @@ constexpr int staging_words() { return relayout_buf_words(M) * (WM > kWarp ? WM 
 // WM > 32 (64, 128, 256): one machine per CTA of WM / 32 warps; thread t holds row t, the
 // algorithms get the row index where they take a lane, relayouts go through the CTA's
 // staging buffer between CTA barriers, and per-machine reductions combine the warps.
-template <int M, int PK, bool EXT, int MODE, int WM = kWarp>
-__global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_per_sm<M, PK>())
+// PIPE (one-warp machines whose instances load in any layout, no probe): persistent warps, and
+// each warp's next task streams into its own shared-memory input slot by one TMA bulk copy
+// (cp.async.bulk + a per-warp mbarrier) while the current task runs -- the HBM latency hides
+// behind the sorting network without spending registers; lanes read their 16-byte chunks back
+// from the slot (a quarter-warp covers 128 contiguous bytes: conflict-free).
+template <int M, int WM>
+constexpr int pipe_slot_words(int PK) { return PK * WM * M; }
+template <int M, int WM>
+constexpr int pipe_staging_words() { return (staging_words<M, WM>() + 3) & ~3; }  // 16-byte aligned slot
+template <int M, int PK, int WM>
+constexpr int pipe_warp_words() { return pipe_staging_words<M, WM>() + pipe_slot_words<M, WM>(PK) + 4; }
+constexpr int kPipeWarps = 4;
+
+template <int M, int PK, bool EXT, int MODE, int WM = kWarp, bool PIPE = false>
+__global__ void __launch_bounds__((PIPE ? kPipeWarps : warps_per_block<M, PK, WM>()) * 32, min_blocks_per_sm<M, PK>())
     k_general_sort(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count, uint64_t domain,
                    int strict, int ascending, dmm_general_stats* __restrict__ stats, uint8_t* __restrict__ status,
                    uint32_t* __restrict__ probe, uint32_t probe_max) {
@@ -88,11 +104,30 @@ __global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_
     const int warp = kMulti ? 0 : (int)(threadIdx.x >> 5);
     const int grp = kMulti ? 0 : lane / WM, row = kMulti ? lane : lane % WM;
     const bool live_lane = ((kMask >> (lane & 31)) & 1u) != 0;
-    uint32_t* buf = smem + warp * staging_words<M, WM>();
-    const uint64_t first = kMulti ? (uint64_t)blockIdx.x * PK
-                                  : ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * (PK * G);  // half 0, group 0
+    static_assert(!PIPE || (!kMulti && G == 1), "the TMA pipeline runs one-warp machines");
+    uint32_t* buf = smem + warp * (PIPE ? pipe_warp_words<M, PK, WM>() : staging_words<M, WM>());
+    uint32_t* slot = buf + pipe_staging_words<M, WM>();               // PIPE: the next task's input
+    uint64_t* bar = reinterpret_cast<uint64_t*>(slot + pipe_slot_words<M, WM>(PK));
+    const uint64_t task_stride = (uint64_t)gridDim.x * (blockDim.x >> 5) * (PK * G);
+    uint64_t first = kMulti ? (uint64_t)blockIdx.x * PK
+                            : ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * (PK * G);  // half 0, group 0
     if (first >= count)
         return;
+    uint32_t parity = 0;
+    auto issue = [&](uint64_t f) {  // lane 0: TMA of the task starting at instance f into the slot
+        const uint64_t n = count - f < (uint64_t)PK ? count - f : (uint64_t)PK;
+        tma_load(slot, in + f * WM * M, (uint32_t)(n * WM * M * 4), bar);
+    };
+    if constexpr (PIPE) {
+        if (lane == 0) {
+            mbar_init(bar);
+            issue(first);
+        }
+        __syncwarp();
+    }
+    for (;; first += task_stride) {
+    if (first >= count)
+        break;
     // half h of this lane's machine: instance first + h*G + grp (absent past count)
     auto inst_of = [&](int h) -> uint64_t { return first + (uint64_t)h * G + grp; };
     const bool hasB = PK == 2 && first + G < count;  // any machine of half 1 present
@@ -114,6 +149,18 @@ __global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_
 #pragma unroll
             for (int c = 0; c < M; ++c)
                 v[c] = synth_key(k, row, c);
+            return;
+        }
+        if constexpr (PIPE) {
+            const uint4* q = reinterpret_cast<const uint4*>(slot + (uint64_t)h * WM * M);
+#pragma unroll
+            for (int i = 0; i < M / 4; ++i) {
+                const uint4 t = q[row + WM * i];
+                v[4 * i] = t.x;
+                v[4 * i + 1] = t.y;
+                v[4 * i + 2] = t.z;
+                v[4 * i + 3] = t.w;
+            }
             return;
         }
         if constexpr (kAnyLayout) {
@@ -152,6 +199,8 @@ __global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_
     };
 
     uint32_t x[M];
+    if constexpr (PIPE)
+        mbar_wait(bar, parity);
     load(0, x);
     uint32_t bad = keys_bad(x, M);  // bit h: half h holds a key outside [0, domain)
     if constexpr (PK == 2) {
@@ -167,6 +216,15 @@ __global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_
 #pragma unroll
         for (int c = 0; c < M; ++c)
             x[c] = __byte_perm(x[c], b[c], 0x5410);  // (a & 0xFFFF) | (b << 16)
+    }
+    if constexpr (PIPE) {
+        // the slot is read: stream the warp's next task into it while this one runs
+        parity ^= 1;
+        __syncwarp();
+        if (lane == 0 && first + task_stride < count) {
+            fence_async_smem();
+            issue(first + task_stride);
+        }
     }
     auto machine_or = [&](uint32_t v) -> uint32_t {
         if constexpr (kMulti)
@@ -259,6 +317,9 @@ __global__ void __launch_bounds__(warps_per_block<M, PK, WM>() * 32, min_blocks_
             }
         }
     }
+    if constexpr (!PIPE)
+        break;
+    }  // task loop (one task unless PIPE)
 }
 
 }  // namespace dmmdev
@@ -302,6 +363,29 @@ dmm_status launch_general(const GeneralArgs& a) {
     return check_launch("k_general_sort");
 }
 
+
+// PIPE: persistent one-warp machines with the TMA input pipeline (leaf-only shapes, no probe)
+template <int M, int PK, bool EXT, int MODE>
+dmm_status launch_general_pipe(const GeneralArgs& a) {
+    auto kern = dmmdev::k_general_sort<M, PK, EXT, MODE, dmmdev::kWarp, true>;
+    constexpr int kW = dmmdev::kPipeWarps;
+    const size_t smem = size_t(kW) * dmmdev::pipe_warp_words<M, PK, dmmdev::kWarp>() * sizeof(uint32_t);
+    static std::atomic<uint64_t> configured{0};
+    if (dmm_status e = configure_kernel(kern, smem, configured); e != DMM_OK)
+        return e;
+    const uint64_t tasks = (a.count + PK - 1) / PK;
+    if (tasks == 0)
+        return DMM_OK;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kW * 32, smem);
+    const uint64_t blocks = std::min<uint64_t>((tasks + kW - 1) / kW, uint64_t(sms) * std::max(per_sm, 1));
+    kern<<<dim3(unsigned(blocks)), dim3(kW * 32), smem, a.stream>>>(a.in, a.out, a.count, a.domain, a.strict,
+                                                                   a.ascending, a.stats, a.status, a.probe,
+                                                                   a.probe_max);
+    return check_launch("k_general_sort (pipelined)");
+}
 
 // per-width entry points (general_m*.cu)
 dmm_status launch_general_m8(int mode, bool pk2, bool ext, const GeneralArgs& a);

@@ -47,32 +47,6 @@ constexpr int kStage = 32 * kSlab;        // staging / exchange / counters / sla
 constexpr int kPre = 2 * 32 * 32;         // row run tables E[l * 32 + r], NX[l * 32 + r]
 constexpr size_t kSmemBytes = size_t(kStage + kPre) * 4 + 16;
 
-__device__ __forceinline__ uint32_t sptr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sptr(bar)) : "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tma_load(uint32_t* dst, const uint32_t* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sptr(bar)), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(sptr(dst)), "l"(src), "r"(bytes), "r"(sptr(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}\n" ::"r"(sptr(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void prefetch_l2(const uint32_t* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
 // to_column_major / to_row_major on this mapping: lane i's register b <-> lane b's register i
 // inside the warp (slab row b padded to 33 words: the store hits bank (b + i) mod 32, the load
 // bank (i' + b) mod 32)
@@ -156,11 +130,13 @@ __device__ __forceinline__ void count_row_sort(uint32_t (&x)[32], uint32_t* S, u
     const uint32_t dm = desc ? 31u : 0u;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-        const bool cross = base + j >= e;
+        const uint32_t cross = base + j >= e ? 1u : 0u;
         cur = cross ? (int)(jn >> 16) : cur;
         e = cross ? (jn & 0xFFFFu) : e;
-        const uint32_t jn2 = nr[cur * 32];
-        jn = cross ? jn2 : jn;
+        // predicated table load (no branch): only a crossing lane reads its next link
+        asm("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.shared.u32 %0, [%1];\n}\n"
+            : "+r"(jn)
+            : "r"(sptr(nr + cur * 32)), "r"(cross));
         x[j] = (uint32_t)cur ^ dm;
     }
 }

@@ -175,9 +175,9 @@ def global_partition_p2p(keys: torch.Tensor, peers: PeerBuffers, nbuckets: int =
     if world > 1:
         all_counts = torch.empty((world, nbuckets), dtype=torch.int64, device=dev)
         if dist.get_backend(group) == "gloo":  # host collective (several ranks on one GPU in tests)
-            h = torch.empty((world, nbuckets), dtype=torch.int64)
-            dist.all_gather_into_tensor(h, counts.cpu(), group=group)
-            all_counts.copy_(h)
+            parts = [torch.empty(nbuckets, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(parts, counts.cpu(), group=group)
+            all_counts.copy_(torch.stack(parts))
         else:
             dist.all_gather_into_tensor(all_counts, counts, group=group)
     else:
