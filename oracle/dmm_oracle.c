@@ -854,6 +854,11 @@ static int fn_partition_short_wide(const view_t* v, void* p) { /* partition.hpp:
 static int fn_sort_short_wide(const view_t* v, void* p) { return sort_short_wide_v(v, ((algo_ctx*)p)->asc); }
 static int fn_sort_square(const view_t* v, void* p) { return sort_square_v(v, ((algo_ctx*)p)->asc); }
 static int fn_sort_tall(const view_t* v, void* p) { (void)p; return sort_tall_v(v); }
+static int fn_sort_wide_any(const view_t* v, void* p) {
+    if (v->W > v->cols || (v->W > 1 && v->cols % v->W != 0))
+        return DMM_SHAPE_VIOLATION;  /* shearsort_rect sort.hpp:291-292 */
+    return sort_wide_any(v, ((algo_ctx*)p)->asc);
+}
 static int fn_transpose(const view_t* v, void* p) { (void)p; return transpose_square(v); }
 static int fn_to_col(const view_t* v, void* p) { (void)p; return to_column_major(v); }
 static int fn_to_row(const view_t* v, void* p) { (void)p; return to_row_major(v); }
@@ -880,6 +885,10 @@ int dmmo_sort_short_wide(uint32_t w, uint32_t m, uint64_t* grid, int ascending) 
 int dmmo_sort_square(uint32_t w, uint32_t m, uint64_t* grid, int ascending) {
     algo_ctx c = {0, 0, NULL, ascending};
     return run_on_standalone(w, m, grid, 1, 0, fn_sort_square, &c);
+}
+int dmmo_sort_wide_any(uint32_t w, uint32_t m, uint64_t* grid, int ascending) { /* sort.hpp:321 */
+    algo_ctx c = {0, 0, NULL, ascending};
+    return run_on_standalone(w, m, grid, 1, 0, fn_sort_wide_any, &c);
 }
 int dmmo_sort_tall(uint32_t w, uint32_t m, uint64_t* grid) {
     return run_on_standalone(w, m, grid, 1, 0, fn_sort_tall, NULL);

@@ -105,6 +105,7 @@ class Port:
         L.dmmo_transpose_square.argtypes = [C.c_uint32, u64p]
         L.dmmo_sort_short_wide.argtypes = [C.c_uint32, C.c_uint32, u64p, C.c_int]
         L.dmmo_sort_square.argtypes = [C.c_uint32, C.c_uint32, u64p, C.c_int]
+        L.dmmo_sort_wide_any.argtypes = [C.c_uint32, C.c_uint32, u64p, C.c_int]
         L.dmmo_permute.argtypes = [C.c_uint32, C.c_uint32, u64p, C.c_uint64, C.c_uint32, C.c_uint32, u64p,
                                    C.POINTER(PermuteReport), u32p]
         L.dmmo_general_sort_shape_ok.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32]

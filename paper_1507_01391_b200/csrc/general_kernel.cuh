@@ -89,9 +89,15 @@ constexpr int pipe_staging_words() { return (staging_words<M, WM>() + 3) & ~3; }
 template <int M, int PK, int WM>
 constexpr int pipe_warp_words() { return pipe_staging_words<M, WM>() + pipe_slot_words<M, WM>(PK) + 4; }
 constexpr int kPipeWarps = 4;
+#ifndef DMM_PIPE2_MINB
+#define DMM_PIPE2_MINB 3  // CTAs per SM asked of ptxas for the L2-prefetch pipeline (register cap)
+#endif
 
-template <int M, int PK, bool EXT, int MODE, int WM = kWarp, bool PIPE = false>
-__global__ void __launch_bounds__((PIPE ? kPipeWarps : warps_per_block<M, PK, WM>()) * 32, min_blocks_per_sm<M, PK>())
+// PIPE = 1: the TMA smem slot above; PIPE = 2: persistent warps that only prefetch their next task
+// into L2 (cp.async.bulk.prefetch.L2: no shared memory, no registers) and load it with LDG.
+template <int M, int PK, bool EXT, int MODE, int WM = kWarp, int PIPE = 0>
+__global__ void __launch_bounds__((PIPE == 1 ? kPipeWarps : warps_per_block<M, PK, WM>()) * 32,
+                                  (PIPE == 2 ? DMM_PIPE2_MINB : min_blocks_per_sm<M, PK>()))
     k_general_sort(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count, uint64_t domain,
                    int strict, int ascending, dmm_general_stats* __restrict__ stats, uint8_t* __restrict__ status,
                    uint32_t* __restrict__ probe, uint32_t probe_max) {
@@ -105,7 +111,7 @@ __global__ void __launch_bounds__((PIPE ? kPipeWarps : warps_per_block<M, PK, WM
     const int grp = kMulti ? 0 : lane / WM, row = kMulti ? lane : lane % WM;
     const bool live_lane = ((kMask >> (lane & 31)) & 1u) != 0;
     static_assert(!PIPE || (!kMulti && G == 1), "the TMA pipeline runs one-warp machines");
-    uint32_t* buf = smem + warp * (PIPE ? pipe_warp_words<M, PK, WM>() : staging_words<M, WM>());
+    uint32_t* buf = smem + warp * (PIPE == 1 ? pipe_warp_words<M, PK, WM>() : staging_words<M, WM>());
     uint32_t* slot = buf + pipe_staging_words<M, WM>();               // PIPE: the next task's input
     uint64_t* bar = reinterpret_cast<uint64_t*>(slot + pipe_slot_words<M, WM>(PK));
     const uint64_t task_stride = (uint64_t)gridDim.x * (blockDim.x >> 5) * (PK * G);
@@ -118,7 +124,7 @@ __global__ void __launch_bounds__((PIPE ? kPipeWarps : warps_per_block<M, PK, WM
         const uint64_t n = count - f < (uint64_t)PK ? count - f : (uint64_t)PK;
         tma_load(slot, in + f * WM * M, (uint32_t)(n * WM * M * 4), bar);
     };
-    if constexpr (PIPE) {
+    if constexpr (PIPE == 1) {
         if (lane == 0) {
             mbar_init(bar);
             issue(first);
@@ -151,7 +157,7 @@ __global__ void __launch_bounds__((PIPE ? kPipeWarps : warps_per_block<M, PK, WM
                 v[c] = synth_key(k, row, c);
             return;
         }
-        if constexpr (PIPE) {
+        if constexpr (PIPE == 1) {
             const uint4* q = reinterpret_cast<const uint4*>(slot + (uint64_t)h * WM * M);
 #pragma unroll
             for (int i = 0; i < M / 4; ++i) {
@@ -199,8 +205,16 @@ __global__ void __launch_bounds__((PIPE ? kPipeWarps : warps_per_block<M, PK, WM
     };
 
     uint32_t x[M];
-    if constexpr (PIPE)
+    if constexpr (PIPE == 1)
         mbar_wait(bar, parity);
+    if constexpr (PIPE == 2) {
+        // the task after this one heads for L2 while this one sorts
+        if (lane == 0 && first + task_stride < count) {
+            const uint64_t f = first + task_stride;
+            const uint64_t nn = count - f < (uint64_t)PK ? count - f : (uint64_t)PK;
+            prefetch_l2(in + f * WM * M, (uint32_t)(nn * WM * M * 4));
+        }
+    }
     load(0, x);
     uint32_t bad = keys_bad(x, M);  // bit h: half h holds a key outside [0, domain)
     if constexpr (PK == 2) {
@@ -217,7 +231,7 @@ __global__ void __launch_bounds__((PIPE ? kPipeWarps : warps_per_block<M, PK, WM
         for (int c = 0; c < M; ++c)
             x[c] = __byte_perm(x[c], b[c], 0x5410);  // (a & 0xFFFF) | (b << 16)
     }
-    if constexpr (PIPE) {
+    if constexpr (PIPE == 1) {
         // the slot is read: stream the warp's next task into it while this one runs
         parity ^= 1;
         __syncwarp();
@@ -317,7 +331,7 @@ __global__ void __launch_bounds__((PIPE ? kPipeWarps : warps_per_block<M, PK, WM
             }
         }
     }
-    if constexpr (!PIPE)
+    if constexpr (PIPE == 0)
         break;
     }  // task loop (one task unless PIPE)
 }
@@ -365,11 +379,12 @@ dmm_status launch_general(const GeneralArgs& a) {
 
 
 // PIPE: persistent one-warp machines with the TMA input pipeline (leaf-only shapes, no probe)
-template <int M, int PK, bool EXT, int MODE>
+template <int M, int PK, bool EXT, int MODE, int PIPE = 1>
 dmm_status launch_general_pipe(const GeneralArgs& a) {
-    auto kern = dmmdev::k_general_sort<M, PK, EXT, MODE, dmmdev::kWarp, true>;
-    constexpr int kW = dmmdev::kPipeWarps;
-    const size_t smem = size_t(kW) * dmmdev::pipe_warp_words<M, PK, dmmdev::kWarp>() * sizeof(uint32_t);
+    auto kern = dmmdev::k_general_sort<M, PK, EXT, MODE, dmmdev::kWarp, PIPE>;
+    constexpr int kW = PIPE == 1 ? dmmdev::kPipeWarps : dmmdev::warps_per_block<M, PK, dmmdev::kWarp>();
+    const size_t smem = size_t(kW) * (PIPE == 1 ? dmmdev::pipe_warp_words<M, PK, dmmdev::kWarp>()
+                                                : dmmdev::staging_words<M, dmmdev::kWarp>()) * sizeof(uint32_t);
     static std::atomic<uint64_t> configured{0};
     if (dmm_status e = configure_kernel(kern, smem, configured); e != DMM_OK)
         return e;

@@ -10,20 +10,27 @@ dmm_status launch_general_m32(int mode, bool pk2, bool ext, const GeneralArgs& a
         set_error("extension kernels are only built where the reference rejects the shape");
         return DMM_UNSUPPORTED_SHAPE;
     }
-    // w = m: partition_leaf only (any starting layout); without a probe the persistent
-    // TMA-pipelined kernel runs it (DMM_NO_PIPE=1 selects the one-task-per-warp kernel)
-    static const bool no_pipe = getenv("DMM_NO_PIPE") && getenv("DMM_NO_PIPE")[0] == '1';
-    const bool pipe = !a.probe && !no_pipe;
+    // w = m: partition_leaf only (any starting layout); without a probe a persistent kernel
+    // runs it (DMM_PIPE: 2 = L2 prefetch of the next task (default), 1 = TMA into a per-warp
+    // shared-memory slot, 0 = one task per warp)
+    static const int pipe_mode = getenv("DMM_PIPE") ? atoi(getenv("DMM_PIPE")) : 2;
+    const bool pipe = !a.probe && pipe_mode != 0;
     switch (mode) {
         case dmmdev::kModePartition:
+            if (pipe && pipe_mode == 1)
+                return pk2 ? launch_general_pipe<32, 2, false, dmmdev::kModePartition, 1>(a)
+                           : launch_general_pipe<32, 1, false, dmmdev::kModePartition, 1>(a);
             if (pipe)
-                return pk2 ? launch_general_pipe<32, 2, false, dmmdev::kModePartition>(a)
-                           : launch_general_pipe<32, 1, false, dmmdev::kModePartition>(a);
+                return pk2 ? launch_general_pipe<32, 2, false, dmmdev::kModePartition, 2>(a)
+                           : launch_general_pipe<32, 1, false, dmmdev::kModePartition, 2>(a);
             return pk2 ? launch_general<32, 2, false, dmmdev::kModePartition>(a) : launch_general<32, 1, false, dmmdev::kModePartition>(a);
         case dmmdev::kModeIntegerSort:
+            if (pipe && pipe_mode == 1)
+                return pk2 ? launch_general_pipe<32, 2, false, dmmdev::kModeIntegerSort, 1>(a)
+                           : launch_general_pipe<32, 1, false, dmmdev::kModeIntegerSort, 1>(a);
             if (pipe)
-                return pk2 ? launch_general_pipe<32, 2, false, dmmdev::kModeIntegerSort>(a)
-                           : launch_general_pipe<32, 1, false, dmmdev::kModeIntegerSort>(a);
+                return pk2 ? launch_general_pipe<32, 2, false, dmmdev::kModeIntegerSort, 2>(a)
+                           : launch_general_pipe<32, 1, false, dmmdev::kModeIntegerSort, 2>(a);
             return pk2 ? launch_general<32, 2, false, dmmdev::kModeIntegerSort>(a) : launch_general<32, 1, false, dmmdev::kModeIntegerSort>(a);
         default:
             return pk2 ? launch_general<32, 2, false, dmmdev::kModeSortAny>(a) : launch_general<32, 1, false, dmmdev::kModeSortAny>(a);

@@ -17,6 +17,8 @@
 // stages / transpose / register stages, all ascending, and flip back.  The passes share
 // ONE copy of the transpose and of the five single-stage bodies (runtime switch): the
 // straight-line version (64 KB of SASS) stalled on instruction fetch (ncu: no_inst 42 %).
+#include <algorithm>
+
 #include "general_kernel.cuh"
 
 namespace dmmdev {
@@ -47,18 +49,32 @@ __device__ __forceinline__ void cross_warp_stage(uint32_t (&x)[32], uint32_t* sl
     __syncthreads();
 }
 
+// Persistent CTAs: CTA b sorts tiles b*PK, (b + grid)*PK, ...; at the start of each tile thread 0
+// prefetches the CTA's next tile(s) into L2 (cp.async.bulk.prefetch.L2: no registers, no shared
+// memory), so the next tile's loads hit L2 while this one sorts.  MODE kModeSortAny:
+// sort_wide_any (sort.hpp:321-330 -> shearsort_rect) ascending or descending (descending =
+// the ascending sort of the complemented keys).
 template <int PK, int MODE>
 __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* __restrict__ in,
                                                                uint32_t* __restrict__ out, uint64_t count,
-                                                               uint64_t domain, dmm_general_stats* __restrict__ stats,
+                                                               uint64_t domain, int ascending,
+                                                               dmm_general_stats* __restrict__ stats,
                                                                uint8_t* __restrict__ status) {
     __shared__ __align__(16) uint32_t smem[kTileWarps * relayout_buf_words(32)];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     uint32_t* buf = smem + warp * relayout_buf_words(32);
-    const uint64_t tile0 = (uint64_t)blockIdx.x * PK;
-    const bool hasB = PK == 2 && tile0 + 1 < count;
     constexpr int M = 128;
+    const uint32_t fdesc = (MODE == kModeSortAny && !ascending) ? 0xFFFFFFFFu : 0u;
+    for (uint64_t tile0 = (uint64_t)blockIdx.x * PK; tile0 < count; tile0 += (uint64_t)gridDim.x * PK) {
+    const bool hasB = PK == 2 && tile0 + 1 < count;
+    if (threadIdx.x == 0) {
+        const uint64_t nt = tile0 + (uint64_t)gridDim.x * PK;
+        if (nt < count) {
+            const uint64_t nn = count - nt < (uint64_t)PK ? count - nt : (uint64_t)PK;
+            prefetch_l2(in + nt * (32 * M), (uint32_t)(nn * 32 * M * 4));
+        }
+    }
 
     uint32_t x[32];
     uint32_t bad = 0;
@@ -113,6 +129,8 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
         }
     }
 
+    if constexpr (MODE == kModeSortAny)
+        flip<0, 32>(x, fdesc);
     using V = VF<0xFFFFFFFFu, 0, 1, kWarp, 0, 32>;
     // levels 1..5: register-local, static
     row_sort<PK, V>(x, lane, (lane & 1) == 0);  // levels 1..5 (odd-even merge sort per row)
@@ -145,7 +163,7 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
             stages_down<PK, 0, 32>(x, half == 0 ? row_stages : 4);
         }
     }
-    flip<0, 32>(x, fcur);
+    flip<0, 32>(x, fcur ^ fdesc);
 
     // tile reductions of the per-warp flags
     __shared__ uint32_t flags_s[kTileWarps];
@@ -199,36 +217,46 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
             }
         }
     }
+    __syncthreads();  // flags_s is rewritten by the next tile
+    }  // tile loop
 }
 
 }  // namespace dmmdev
 
 namespace dmmhost {
 
+namespace {
+template <int PK, int MODE>
+dmm_status launch_tile(const GeneralArgs& a) {
+    auto kern = dmmdev::k_tile_sort<PK, MODE>;
+    const uint64_t units = (a.count + PK - 1) / PK;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, dmmdev::kTileWarps * 32, 0);
+    const uint64_t blocks = std::min<uint64_t>(units, uint64_t(sms) * std::max(per_sm, 1));
+    kern<<<unsigned(blocks), dmmdev::kTileWarps * 32, 0, a.stream>>>(a.in, a.out, a.count, a.domain, a.ascending,
+                                                                      a.stats, a.status);
+    return check_launch("k_tile_sort");
+}
+}  // namespace
+
 dmm_status launch_general_m128(int mode, bool pk2, bool ext, const GeneralArgs& a) {
     if (ext) {
         set_error("extension kernels are only built where the reference rejects the shape");
         return DMM_UNSUPPORTED_SHAPE;
     }
-    if (mode == dmmdev::kModeSortAny) {
-        set_error("sort_wide_any is built for m = 32, 64");
-        return DMM_UNSUPPORTED_SHAPE;
-    }
-    const int pk = (mode == dmmdev::kModePartition || pk2) ? 2 : 1;
-    const uint64_t blocks = (a.count + pk - 1) / pk;
-    if (blocks > 0x7FFFFFFFull)
+    if (a.probe) {
+        set_error("32 x 128 machines: no probe (w <= m has no PartitionProbe point)");
         return DMM_INVALID_ARGUMENT;
-    const dim3 grid{unsigned(blocks)}, block{unsigned(dmmdev::kTileWarps * 32)};
+    }
+    if (a.count == 0)
+        return DMM_OK;
+    if (mode == dmmdev::kModeSortAny)
+        return launch_tile<1, dmmdev::kModeSortAny>(a);
     if (mode == dmmdev::kModePartition)
-        dmmdev::k_tile_sort<2, dmmdev::kModePartition>
-            <<<grid, block, 0, a.stream>>>(a.in, a.out, a.count, a.domain, a.stats, a.status);
-    else if (pk == 2)
-        dmmdev::k_tile_sort<2, dmmdev::kModeIntegerSort>
-            <<<grid, block, 0, a.stream>>>(a.in, a.out, a.count, a.domain, a.stats, a.status);
-    else
-        dmmdev::k_tile_sort<1, dmmdev::kModeIntegerSort>
-            <<<grid, block, 0, a.stream>>>(a.in, a.out, a.count, a.domain, a.stats, a.status);
-    return check_launch("k_tile_sort");
+        return launch_tile<2, dmmdev::kModePartition>(a);
+    return pk2 ? launch_tile<2, dmmdev::kModeIntegerSort>(a) : launch_tile<1, dmmdev::kModeIntegerSort>(a);
 }
 
 }  // namespace dmmhost

@@ -35,7 +35,12 @@ def _torchrun(nproc, script, *args, env=None, timeout=600):
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), script, *args]
     e = dict(os.environ)
     e.update(env or {})
-    return subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT, env=e)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT, env=e)
+    if r.returncode != 0:  # keep the whole log (torchrun's tail hides the failing rank's trace)
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        with open(os.path.join(ROOT, "gpurun_out", f"torchrun_{os.path.basename(script)}_{_port()}.log"), "w") as f:
+            f.write(r.stdout + "\n" + r.stderr)
+    return r
 
 
 @pytest.mark.parametrize("world", [2, 3])

@@ -269,3 +269,34 @@ def test_cfg3_full_batch_multiset_check():
     bad[count - 1, 31, 127] = bad[count - 1, 31, 126]
     r = bench.verify_sort_full(g, bad, count)
     assert not (r["sum_sumsq"] and r["xor"])
+
+
+@pytest.mark.parametrize("asc", [True, False])
+def test_sort_wide_any_32x128(port, asc):
+    # detail::sort_wide_any at 32 x 128 (sort.hpp:321-330 -> shearsort_rect, merge rows): the
+    # CTA tile kernel in comparison mode, both directions, against the oracle and numpy
+    rng = np.random.default_rng(128 + asc)
+    g = rng.integers(0, 2 ** 32, size=(9, 32, 128), dtype=np.uint64).astype(np.uint32)
+    g[2] = rng.integers(0, 3, size=(32, 128), dtype=np.uint64).astype(np.uint32)
+    out = dmm.as_uint32(dmm.sort_wide_any(g, ascending=asc))
+    for k in range(9):
+        exp = np.sort(g[k].ravel())
+        assert (out[k].ravel() == (exp if asc else exp[::-1])).all(), k
+    s, exp = port.simple("sort_wide_any", g[0], int(asc))
+    assert s == 0 and (out[0] == exp).all()
+
+
+def test_partition_general_32x128_vs_oracle(port):
+    # partition mode of the 32 x 128 tile kernel (two instances per register) against the oracle
+    seeds = list(range(1, 38))  # odd count: the last CTA pairs an instance with nothing
+    grids = _oracle_batch(port, 1, 32, 128, seeds)
+    out, st = dmm.partition_general(grids)
+    out = dmm.as_uint32(out)
+    for k in range(len(seeds)):
+        ost, oout, orep = port.partition_general(grids[k])
+        assert ost == 0 and (out[k] == oout).all()
+        assert int(st.cleanup_retries[k]) == orep["cleanup_retries"]
+    bad = grids[:3].copy()
+    bad[1, 4, 4] = 40
+    with pytest.raises(dmm.InvalidInstance):
+        dmm.partition_general(bad)

@@ -142,3 +142,17 @@ def test_port_vs_reference_run_algorithm(port, ref):
     assert st == 0 and rep["correct"] and rep["conflicts"] == 0
     a = port.permute(g, 9)
     assert a[2]["iterations"] == rep["iterations"] and a[2]["fallback"] == rep["fallback"]
+
+
+@pytest.mark.parametrize("w,m", [(32, 128), (32, 32), (4, 16), (8, 64)])
+def test_oracle_sort_wide_any(port, w, m):
+    # detail::sort_wide_any (sort.hpp:321-330): the sorted multiset in either direction (its
+    # outcome is unique), and ShapeViolation unless w <= m and w | m (sort.hpp:291-292)
+    rng = np.random.default_rng(w * m)
+    g = rng.integers(0, 2 ** 32, size=(w, m), dtype=np.uint64)
+    for asc in (1, 0):
+        s, out = port.simple("sort_wide_any", g, asc)
+        exp = np.sort(g.ravel())
+        assert s == 0 and (out.ravel() == (exp if asc else exp[::-1])).all()
+    s, _ = port.simple("sort_wide_any", rng.integers(0, 9, size=(32, 48), dtype=np.uint64), 1)
+    assert s == 1  # DMM_SHAPE_VIOLATION
