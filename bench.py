@@ -560,7 +560,10 @@ def main():
         # step i's D2H overlaps step i+1's H2D (PCIe is full duplex)
         e2e_streams = [torch.cuda.Stream(), torch.cuda.Stream()]
         d_in = [torch.empty_like(g) for _ in range(2)]
-        h_outs = [h_out, torch.empty_like(h_in).pin_memory()]
+        # a rank receives the keys of its labels from every rank: up to the receive capacity
+        cap = peers[0].capacity if args.transport == "p2p" else p2p_capacity(keys_per_gpu, world)
+        h_outs = [torch.empty(cap, dtype=torch.int32).pin_memory() for _ in range(2)]
+        d2h_keys = []
 
         def gp_step(i):
             s = e2e_streams[i % 2]
@@ -571,6 +574,7 @@ def main():
                 else:
                     res, _ = global_partition(d_in[i % 2].view(-1))
                 h_outs[i % 2].view(-1)[: res.numel()].copy_(res, non_blocking=True)
+                d2h_keys.append(res.numel())
 
         for i in range(2):  # warm-up
             gp_step(i)
@@ -624,7 +628,9 @@ def main():
                          else "fallback 6650 GB/s"},
             "smem": smem_line(traffic, ms),
             "e2e": {"value": total_keys / (e2e_ms / 1e3), "unit": "keys/s",
-                    "h2d_bytes_per_step": keys_per_gpu * 4, "d2h_bytes_per_step": keys_per_gpu * 4},
+                    "h2d_bytes_per_step": keys_per_gpu * 4,
+                    "d2h_bytes_per_step": (keys_per_gpu * 4 if alg != "global_partition"
+                                           else int(4 * sum(d2h_keys[-e2e_steps:]) / e2e_steps))},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
             "correct": ok,

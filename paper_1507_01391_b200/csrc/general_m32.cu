@@ -10,10 +10,12 @@ dmm_status launch_general_m32(int mode, bool pk2, bool ext, const GeneralArgs& a
         set_error("extension kernels are only built where the reference rejects the shape");
         return DMM_UNSUPPORTED_SHAPE;
     }
-    // w = m: partition_leaf only (any starting layout); without a probe a persistent kernel
-    // runs it (DMM_PIPE: 2 = L2 prefetch of the next task (default), 1 = TMA into a per-warp
-    // shared-memory slot, 0 = one task per warp)
-    static const int pipe_mode = getenv("DMM_PIPE") ? atoi(getenv("DMM_PIPE")) : 2;
+    // w = m: partition_leaf only (any starting layout).  DMM_PIPE selects a persistent variant
+    // (2 = L2 prefetch of the next task, 1 = TMA into a per-warp shared-memory slot); both
+    // measured SLOWER than one task per warp (0, the default): 320 / 321 vs 351 G keys/s on
+    // cfg1 (profiles/r02/pipeline_ab.txt) -- fewer resident warps (1) or a longer register
+    // lifetime (2) cost more than the hidden load latency gains.
+    static const int pipe_mode = getenv("DMM_PIPE") ? atoi(getenv("DMM_PIPE")) : 0;
     const bool pipe = !a.probe && pipe_mode != 0;
     switch (mode) {
         case dmmdev::kModePartition:

@@ -18,6 +18,7 @@
 // ONE copy of the transpose and of the five single-stage bodies (runtime switch): the
 // straight-line version (64 KB of SASS) stalled on instruction fetch (ncu: no_inst 42 %).
 #include <algorithm>
+#include <cstdlib>
 
 #include "general_kernel.cuh"
 
@@ -230,11 +231,20 @@ template <int PK, int MODE>
 dmm_status launch_tile(const GeneralArgs& a) {
     auto kern = dmmdev::k_tile_sort<PK, MODE>;
     const uint64_t units = (a.count + PK - 1) / PK;
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, dmmdev::kTileWarps * 32, 0);
-    const uint64_t blocks = std::min<uint64_t>(units, uint64_t(sms) * std::max(per_sm, 1));
+    // one CTA per tile (pair): a persistent grid with L2 prefetch of the next tile measured
+    // slower (165 vs 184 G keys/s on cfg3, profiles/r02/pipeline_ab.txt); DMM_TILE_PERSIST=1
+    // selects it
+    static const bool persist = getenv("DMM_TILE_PERSIST") && getenv("DMM_TILE_PERSIST")[0] == '1';
+    uint64_t blocks = units;
+    if (persist) {
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, dmmdev::kTileWarps * 32, 0);
+        blocks = std::min<uint64_t>(units, uint64_t(sms) * std::max(per_sm, 1));
+    }
+    if (blocks > 0x7FFFFFFFull)
+        return DMM_INVALID_ARGUMENT;
     kern<<<unsigned(blocks), dmmdev::kTileWarps * 32, 0, a.stream>>>(a.in, a.out, a.count, a.domain, a.ascending,
                                                                       a.stats, a.status);
     return check_launch("k_tile_sort");
