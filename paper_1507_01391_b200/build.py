@@ -58,7 +58,7 @@ def build(verbose: bool = False, jobs: int = 0, defines: tuple = (), out: str = 
     paper_1507_01391_b200/_variants/) with its own object directory."""
     obj_dir, lib_path = OBJ, LIB
     if defines:
-        tag = "_".join(d.split("=")[0].lower() for d in defines)
+        tag = "_".join(d.replace("=", "_").lower() for d in defines)
         obj_dir = os.path.join(PKG, "_build_" + tag)
         lib_path = out or os.path.join(PKG, "_variants", f"libdmm_b200_{tag}.so")
         os.makedirs(os.path.dirname(lib_path), exist_ok=True)

@@ -59,8 +59,11 @@ __device__ __forceinline__ uint32_t synth_key(uint64_t k, int row, int c) {
 }
 
 // CTA shape: warps per CTA and the occupancy target handed to ptxas (register cap)
+#ifndef DMM_WPB
+#define DMM_WPB 8  // warps per CTA of the one-warp-machine kernels (A/B variants: -DDMM_WPB=2/4)
+#endif
 template <int M, int PK, int WM = kWarp>
-constexpr int warps_per_block() { return WM > kWarp ? WM / kWarp : (M >= 128 ? 4 : 8); }
+constexpr int warps_per_block() { return WM > kWarp ? WM / kWarp : (M >= 128 ? 4 : DMM_WPB); }
 template <int M, int PK>
 constexpr int min_blocks_per_sm() { return 1; }
 // shared-memory words per warp (WM <= 32) or per machine (WM > 32: one machine per CTA)

@@ -33,6 +33,7 @@
 //     with c = (k + r) mod 32: bank c, distinct across every warp.  The result leaves from
 //     the registers (chunk layout: row r, columns 32k .. 32k + 31, 16-byte stores).
 #include <algorithm>
+#include <cstdlib>
 
 #include "general_kernel.cuh"
 
@@ -138,6 +139,107 @@ __device__ __forceinline__ void count_row_sort(uint32_t (&x)[32], uint32_t* S, u
             : "+r"(jn)
             : "r"(sptr(nr + cur * 32)), "r"(cross));
         x[j] = (uint32_t)cur ^ dm;
+    }
+}
+
+// Four label machines per CTA (kModePartition / small-domain integer sorts): byte b of every
+// register belongs to machine b (labels < 32 fit a byte), so the warp transposes and the row
+// exchanges move four keys per word, four independent run walks give the emit four-fold ILP,
+// and the CTA barriers are shared by four machines.  Thread (k, r) counts machine b's label l
+// into byte b of its counter word cnt[l] (a thread holds at most 32 keys of a row: a byte
+// suffices); the row totals add the four bytes in 16-bit lanes (even / odd bytes), and warp b
+// (b < 4) builds machine b's run tables.  Same schedule, per machine, as count_row_sort.
+constexpr int kTab4 = 4 * 2 * 32 * 32;  // E and NX tables of the four machines
+template <class AfterCount>
+__device__ __forceinline__ void count_row_sort4(uint32_t (&x)[32], uint32_t* S, uint32_t* T, int k, int r, bool desc,
+                                                AfterCount&& after_count) {
+    uint32_t* cnt = S + k * kM + r;  // this thread's counters cnt[32 l]: bank r, byte b = machine b
+    __syncthreads();
+#pragma unroll
+    for (int l = 0; l < 32; ++l)
+        cnt[l * 32] = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            atomicAdd(cnt + ((x[j] >> (8 * b)) & 31u) * 32, 1u << (8 * b));
+    }
+    __syncthreads();
+    // label k's count in row r of each machine: the row's 32 threads' bytes, summed in 16-bit
+    // lanes (at most 1024 per machine)
+    uint32_t ev = 0, od = 0;
+    const uint32_t* col = S + k * 32 + r;
+#pragma unroll
+    for (int kk = 0; kk < 32; ++kk) {
+        const uint32_t w = col[kk * kM];
+        ev += w & 0x00FF00FFu;
+        od += (w >> 8) & 0x00FF00FFu;
+    }
+    T[(0 * 2) * 1024 + k * 32 + r] = ev & 0xFFFFu;
+    T[(1 * 2) * 1024 + k * 32 + r] = od & 0xFFFFu;
+    T[(2 * 2) * 1024 + k * 32 + r] = ev >> 16;
+    T[(3 * 2) * 1024 + k * 32 + r] = od >> 16;
+    __syncthreads();
+    after_count();
+    if (k < 4) {
+        // machine k's run ends E and next-non-empty links NX of row r, in the row's order
+        uint32_t* E = T + (k * 2) * 1024;
+        uint32_t* NX = E + 1024;
+        uint32_t t[32];
+#pragma unroll
+        for (int l = 0; l < 32; ++l)
+            t[l] = E[(desc ? 31 - l : l) * 32 + r];
+        uint32_t sum = 0;
+#pragma unroll
+        for (int l = 0; l < 32; ++l) {
+            sum += t[l];
+            t[l] = sum;
+            E[l * 32 + r] = sum;
+        }
+        uint32_t nxt = (32u << 16) | kM;
+#pragma unroll
+        for (int l = 31; l >= 0; --l) {
+            NX[l * 32 + r] = nxt;
+            const uint32_t start = l ? t[l - 1] : 0u;
+            if (t[l] > start)
+                nxt = ((uint32_t)l << 16) | t[l];
+        }
+    }
+    __syncthreads();
+    const uint32_t base = 32u * (uint32_t)k;
+    const uint32_t dm = desc ? 31u : 0u;
+    // two machines' walks at a time (register budget: 32 keys + two walk states)
+#pragma unroll
+    for (int b0 = 0; b0 < 4; b0 += 2) {
+        int cur[2];
+        uint32_t e[2], jn[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const uint32_t* er = T + ((b0 + q) * 2) * 1024 + r;
+            int c = 0;  // first run whose end exceeds base
+#pragma unroll
+            for (int s = 16; s >= 1; s >>= 1)
+                if (er[(c + s - 1) * 32] <= base)
+                    c += s;
+            cur[q] = c;
+            e[q] = er[c * 32];
+            jn[q] = er[1024 + c * 32];
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            uint32_t v = b0 == 0 ? 0u : x[j];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const uint32_t cross = base + j >= e[q] ? 1u : 0u;
+                cur[q] = cross ? (int)(jn[q] >> 16) : cur[q];
+                e[q] = cross ? (jn[q] & 0xFFFFu) : e[q];
+                asm("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.shared.u32 %0, [%1];\n}\n"
+                    : "+r"(jn[q])
+                    : "r"(sptr(T + ((b0 + q) * 2 + 1) * 1024 + r + cur[q] * 32)), "r"(cross));
+                v |= ((uint32_t)cur[q] ^ dm) << (8 * (b0 + q));
+            }
+            x[j] = v;
+        }
     }
 }
 
@@ -319,6 +421,135 @@ __global__ void __launch_bounds__(1024, 1)
     }
 }
 
+// The label machines, four per CTA (count_row_sort4): partition_short_wide, partition_general /
+// integer_sort_general with domain <= 32 and the partition's ShortWideHook probe.  Persistent
+// over groups of four machines; each CTA prefetches its next group into L2 (four 128 KB bulk
+// prefetches) at the start of the current one, and threads load / store their row chunks
+// (row r, columns 32k .. 32k + 31) with 16-byte global accesses.
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1)
+    k_short_wide32_labels(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count,
+                          uint64_t domain, int ascending, dmm_general_stats* __restrict__ stats,
+                          uint8_t* __restrict__ status, uint32_t* __restrict__ probe) {
+    extern __shared__ __align__(128) uint32_t smem[];
+    uint32_t* S = smem;
+    uint32_t* T = smem + kStage;
+    uint32_t* F = T + kTab4;  // four flag words: two per task parity
+    const int tid = threadIdx.x, k = tid >> 5, r = tid & 31;
+    const bool asc = ascending != 0;
+    const bool part = MODE == kModePartition || (MODE == kModeSortAny && domain < (1ull << 32));
+    uint32_t* slab = S + k * kSlab;
+    const uint32_t d = domain < 32 ? (uint32_t)domain : 32u;
+    if (tid < 4)
+        F[tid] = 0;
+    __syncthreads();
+    uint32_t parity = 0;
+    for (uint64_t m0 = (uint64_t)blockIdx.x * 4; m0 < count; m0 += (uint64_t)gridDim.x * 4, parity ^= 1) {
+        const uint64_t nx = m0 + (uint64_t)gridDim.x * 4;
+        if (tid < 4 && nx + tid < count)
+            prefetch_l2(in + (nx + tid) * kWords, kBytes);
+        uint32_t x[32];
+        uint32_t bad = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const uint64_t inst = m0 + b;
+            const uint4* q = reinterpret_cast<const uint4*>(in + inst * kWords + r * kM + 32 * k);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint4 t = inst < count ? __ldg(q + i) : make_uint4(0, 0, 0, 0);
+                const uint32_t v[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    bad |= v[e] >= d ? (1u << b) : 0u;
+                    const uint32_t c = min(v[e], 31u) << (8 * b);
+                    x[4 * i + e] = b == 0 ? c : (x[4 * i + e] | c);
+                }
+            }
+        }
+        uint32_t* Fb = F + 2 * parity;
+        {
+            const uint32_t wb = __reduce_or_sync(0xFFFFFFFFu, bad);
+            if (r == 0 && wb)
+                atomicOr(Fb, wb);
+        }
+        if (tid == 0)
+            F[2 * (parity ^ 1)] = F[2 * (parity ^ 1) + 1] = 0;  // the next group's flags (last read a group ago)
+        uint32_t* snaps = probe != nullptr ? probe + m0 * 3 * kWords : nullptr;
+        auto snap4 = [&](int stage, bool stride) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                if (m0 + b >= count)
+                    break;
+                uint32_t* dst = snaps + (uint64_t)b * 3 * kWords + (uint64_t)stage * kWords;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    dst[r * kM + (stride ? 32 * j + k : 32 * k + j)] = (x[j] >> (8 * b)) & 0xFFu;
+            }
+        };
+        auto nothing = []() {};
+
+        for (int pass = 0; pass < 2; ++pass) {
+            const bool desc_alt = ((r & 1) == 0) != asc;
+            count_row_sort4(x, S, T, k, r, desc_alt, nothing);  // chunk layout out
+            __syncthreads();
+            warp_transpose(x, slab, r);  // to_column_major
+            if (pass == 0 && snaps)
+                snap4(0, true);  // after_first_convert
+            count_row_sort4(x, S, T, k, r, !asc, nothing);
+            chunk_to_stride(x, S, k, r, k);
+            __syncthreads();
+            warp_transpose(x, slab, r);  // to_row_major: chunk layout out
+            if (pass == 0 && snaps)
+                snap4(1, false);  // after_first_pass
+        }
+        count_row_sort4(x, S, T, k, r, !asc, nothing);
+        if (snaps)
+            snap4(2, false);  // done
+        uint32_t mism = 0;
+        if (part) {
+            uint32_t diff = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                diff |= x[j] ^ ((uint32_t)r * 0x01010101u);
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                mism |= ((diff >> (8 * b)) & 0xFFu) ? (1u << b) : 0u;
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const uint64_t inst = m0 + b;
+            if (inst >= count)
+                break;
+            uint4* q = reinterpret_cast<uint4*>(out + inst * kWords + r * kM + 32 * k);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                q[i] = make_uint4((x[4 * i] >> (8 * b)) & 0xFFu, (x[4 * i + 1] >> (8 * b)) & 0xFFu,
+                                  (x[4 * i + 2] >> (8 * b)) & 0xFFu, (x[4 * i + 3] >> (8 * b)) & 0xFFu);
+        }
+        {
+            const uint32_t wm = __reduce_or_sync(0xFFFFFFFFu, mism);
+            if (r == 0 && wm)
+                atomicOr(Fb + 1, wm);
+        }
+        __syncthreads();
+        if (tid < 4 && m0 + tid < count) {
+            const uint64_t inst = m0 + tid;
+            const bool bd = (Fb[0] >> tid) & 1u, inv = bd || ((Fb[1] >> tid) & 1u);
+            uint8_t st = DMM_OK;
+            if (part && inv)
+                st = DMM_INVALID_INSTANCE;
+            else if (bd)
+                st = DMM_KEY_OUT_OF_RANGE;
+            if (status)
+                status[inst] = st;
+            if (stats) {
+                stats[inst].cleanup_retries = 0;  // w <= m: partition_leaf only
+                stats[inst].sorted = 1;
+            }
+        }
+    }
+}
+
 }  // namespace sw32
 }  // namespace dmmdev
 
@@ -341,6 +572,23 @@ dmm_status launch_sw32(const GeneralArgs& a) {
                                                                        a.stats, a.status, a.probe);
     return check_launch("k_short_wide32");
 }
+template <int MODE>
+dmm_status launch_sw32_labels(const GeneralArgs& a) {
+    auto kern = dmmdev::sw32::k_short_wide32_labels<MODE>;
+    constexpr size_t smem = size_t(dmmdev::sw32::kStage + dmmdev::sw32::kTab4 + 4) * 4;
+    static std::atomic<uint64_t> configured{0};
+    if (dmm_status e = configure_kernel(kern, smem, configured); e != DMM_OK)
+        return e;
+    if (a.count == 0)
+        return DMM_OK;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t grid = std::min<uint64_t>((a.count + 3) / 4, uint64_t(sms));
+    kern<<<unsigned(grid), 1024, smem, a.stream>>>(a.in, a.out, a.count, a.domain, a.ascending, a.stats, a.status,
+                                                   a.probe);
+    return check_launch("k_short_wide32_labels");
+}
 }  // namespace
 
 // 32 x 1024 machines: every entry point's leaf is the short-wide skeleton (w^2 <= m)
@@ -353,7 +601,16 @@ dmm_status launch_general_m1024(int mode, bool /*pk2*/, bool ext, const GeneralA
         set_error("32 x 1024 machines capture the three ShortWideHook stages only");
         return DMM_INVALID_ARGUMENT;
     }
+    // label machines (domain <= 32): four per CTA; DMM_SW32_SINGLE=1 runs them one per CTA
+    static const bool single = getenv("DMM_SW32_SINGLE") && getenv("DMM_SW32_SINGLE")[0] == '1';
     const bool count = a.domain <= 32;
+    if (count && !single) {
+        switch (mode) {
+            case dmmdev::kModePartition: return launch_sw32_labels<dmmdev::kModePartition>(a);
+            case dmmdev::kModeIntegerSort: return launch_sw32_labels<dmmdev::kModeIntegerSort>(a);
+            default: return launch_sw32_labels<dmmdev::kModeSortAny>(a);
+        }
+    }
     switch (mode) {
         case dmmdev::kModePartition:
             return launch_sw32<true, dmmdev::kModePartition>(a);
