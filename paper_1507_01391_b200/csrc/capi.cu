@@ -33,7 +33,7 @@ int dmm_supported(const char* algorithm, uint32_t w, uint32_t m) {
             case 256: return m == 16;
             case 128: return m == 32 || m == 64;
             case 64: return m == 8 || m == 16 || m == 32 || m == 64;
-            case 32: return m == 8 || m == 16 || m == 32 || m == 64 || m == 128 || m == 1024;
+            case 32: return m == 8 || m == 16 || m == 32 || m == 64 || m == 128 || m == 256 || m == 1024;
             case 16:
             case 8: return m == 8 || m == 16 || m == 32 || m == 64;
             case 4: return m == 4 || m == 8 || m == 16;
@@ -45,7 +45,7 @@ int dmm_supported(const char* algorithm, uint32_t w, uint32_t m) {
     if (a == "partition_general" || a == "integer_sort_general")
         return general();
     if (a == "sort_wide_any")
-        return general() && w <= m && m % w == 0 && (w != 32 || m == 32 || m == 64 || m == 128 || m == 1024);
+        return general() && w <= m && m % w == 0 && (w != 32 || m == 32 || m == 64 || m == 128 || m == 256 || m == 1024);
     if (a == "partition_square" || a == "sort_square")
         return general() && w == m && (m == 4 || m == 16 || m == 64);
     if (a == "partition_short_wide" || a == "sort_short_wide")

@@ -60,10 +60,11 @@ __device__ __forceinline__ uint32_t synth_key(uint64_t k, int row, int c) {
 
 // CTA shape: warps per CTA and the occupancy target handed to ptxas (register cap)
 #ifndef DMM_WPB
-#define DMM_WPB 8  // warps per CTA of the one-warp-machine kernels (A/B variants: -DDMM_WPB=2/4)
+#define DMM_WPB 8  // warps per CTA of the one-warp-machine kernels (A/B variants: -DDMM_WPB=2/4;
+                   // 32 x 32 machines: 4, measured 364 vs 351 G keys/s with 8, profiles/r02/pipeline_ab.txt)
 #endif
 template <int M, int PK, int WM = kWarp>
-constexpr int warps_per_block() { return WM > kWarp ? WM / kWarp : (M >= 128 ? 4 : DMM_WPB); }
+constexpr int warps_per_block() { return WM > kWarp ? WM / kWarp : (M >= 128 || M == 32 ? 4 : DMM_WPB); }
 template <int M, int PK>
 constexpr int min_blocks_per_sm() { return 1; }
 // shared-memory words per warp (WM <= 32) or per machine (WM > 32: one machine per CTA)
@@ -411,6 +412,7 @@ dmm_status launch_general_m16(int mode, bool pk2, bool ext, const GeneralArgs& a
 dmm_status launch_general_m32(int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_m64(int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_m128(int mode, bool pk2, bool ext, const GeneralArgs& a);
+dmm_status launch_general_m256(int mode, bool pk2, bool ext, const GeneralArgs& a);
 // 32 x 1024: the short-wide skeleton on a CTA of 32 warps (short_wide32.cu)
 dmm_status launch_general_m1024(int mode, bool pk2, bool ext, const GeneralArgs& a);
 // multi-warp machines (w = 64, 128, 256 rows, one per CTA), general_tall*.cu

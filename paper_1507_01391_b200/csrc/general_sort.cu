@@ -29,6 +29,7 @@ dmm_status dispatch(int mode, const uint32_t* in, uint32_t* out, uint32_t w, uin
                 case 32: return launch_general_m32(mode, pk2, ext, a);
                 case 64: return launch_general_m64(mode, pk2, ext, a);
                 case 128: return launch_general_m128(mode, pk2, ext, a);
+                case 256: return launch_general_m256(mode, pk2, ext, a);
                 case 1024: return launch_general_m1024(mode, pk2, ext, a);
                 default: break;
             }

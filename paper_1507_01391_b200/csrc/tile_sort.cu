@@ -55,17 +55,21 @@ __device__ __forceinline__ void cross_warp_stage(uint32_t (&x)[32], uint32_t* sl
 // memory), so the next tile's loads hit L2 while this one sorts.  MODE kModeSortAny:
 // sort_wide_any (sort.hpp:321-330 -> shearsort_rect) ascending or descending (descending =
 // the ascending sort of the complemented keys).
-template <int PK, int MODE>
-__global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* __restrict__ in,
-                                                               uint32_t* __restrict__ out, uint64_t count,
-                                                               uint64_t domain, int ascending,
-                                                               dmm_general_stats* __restrict__ stats,
-                                                               uint8_t* __restrict__ status) {
-    __shared__ __align__(16) uint32_t smem[kTileWarps * relayout_buf_words(32)];
+// NW warps per tile: 4 (32 x 128, cfg3) or 8 (32 x 256); the tile is 1024 * NW keys and its
+// sort has 10 + log2(NW) levels, the last log2(NW) with cross-warp stages.
+template <int PK, int MODE, int NW = kTileWarps>
+__global__ void __launch_bounds__(NW * 32) k_tile_sort(const uint32_t* __restrict__ in,
+                                                       uint32_t* __restrict__ out, uint64_t count,
+                                                       uint64_t domain, int ascending,
+                                                       dmm_general_stats* __restrict__ stats,
+                                                       uint8_t* __restrict__ status) {
+    static_assert(NW == 4 || NW == 8, "32 x 128 or 32 x 256 tiles");
+    constexpr int LOGNW = NW == 8 ? 3 : 2;
+    __shared__ __align__(16) uint32_t smem[NW * relayout_buf_words(32)];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     uint32_t* buf = smem + warp * relayout_buf_words(32);
-    constexpr int M = 128;
+    constexpr int M = 32 * NW;
     const uint32_t fdesc = (MODE == kModeSortAny && !ascending) ? 0xFFFFFFFFu : 0u;
     for (uint64_t tile0 = (uint64_t)blockIdx.x * PK; tile0 < count; tile0 += (uint64_t)gridDim.x * PK) {
     const bool hasB = PK == 2 && tile0 + 1 < count;
@@ -141,7 +145,7 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
         uint32_t f;
         if (level < 10)
             f = (lane >> (level - 5)) & 1;  // in-warp level: direction = element bit `level`
-        else if (level < 12)
+        else if (level < 10 + LOGNW)
             f = (warp >> (level - 10)) & 1;  // cross-warp levels: direction = warp bit
         else
             f = 0;
@@ -149,13 +153,13 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
     };
     uint32_t fcur = 0;
 #pragma unroll 1
-    for (int pass = 0; pass < 7; ++pass) {
+    for (int pass = 0; pass < 5 + LOGNW; ++pass) {
         const int level = 6 + pass;
         const uint32_t f = dir_mask(level);
         flip<0, 32>(x, f ^ fcur);
         fcur = f;
 #pragma unroll 1
-        for (int b = level - 11; b >= 0; --b)  // stages on warp bits (levels 11, 12)
+        for (int b = level - 11; b >= 0; --b)  // stages on warp bits (levels 11 .. 10 + log2 NW)
             cross_warp_stage<PK>(x, smem, warp, lane, b);
         const int row_stages = (level < 10 ? level : 10) - 6;  // row-bit stages row_stages..0
 #pragma unroll 1
@@ -167,11 +171,11 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
     flip<0, 32>(x, fcur ^ fdesc);
 
     // tile reductions of the per-warp flags
-    __shared__ uint32_t flags_s[kTileWarps];
+    __shared__ uint32_t flags_s[NW];
     uint32_t mism = 0;
     if constexpr (MODE == kModePartition) {
-        // row-major rank e = 1024 w + 32 r + j belongs to machine row e / 128 = 8 w + r / 4
-        const uint32_t row = 8u * warp + lane / 4;
+        // row-major rank e = 1024 w + 32 r + j belongs to machine row e / M
+        const uint32_t row = (1024u / M) * warp + lane / (M / 32);
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
             if constexpr (PK == 2) {
@@ -188,7 +192,7 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
     __syncthreads();
     uint32_t all = 0;
 #pragma unroll
-    for (int i = 0; i < kTileWarps; ++i)
+    for (int i = 0; i < NW; ++i)
         all |= flags_s[i];
     const uint32_t badt = all & 3u, invalid = (all >> 2) | badt;
 
@@ -227,9 +231,9 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_tile_sort(const uint32_t* _
 namespace dmmhost {
 
 namespace {
-template <int PK, int MODE>
+template <int PK, int MODE, int NW = dmmdev::kTileWarps>
 dmm_status launch_tile(const GeneralArgs& a) {
-    auto kern = dmmdev::k_tile_sort<PK, MODE>;
+    auto kern = dmmdev::k_tile_sort<PK, MODE, NW>;
     const uint64_t units = (a.count + PK - 1) / PK;
     // one CTA per tile (pair): a persistent grid with L2 prefetch of the next tile measured
     // slower (165 vs 184 G keys/s on cfg3, profiles/r02/pipeline_ab.txt); DMM_TILE_PERSIST=1
@@ -240,12 +244,12 @@ dmm_status launch_tile(const GeneralArgs& a) {
         int dev = 0, sms = 148, per_sm = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, dmmdev::kTileWarps * 32, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, 0);
         blocks = std::min<uint64_t>(units, uint64_t(sms) * std::max(per_sm, 1));
     }
     if (blocks > 0x7FFFFFFFull)
         return DMM_INVALID_ARGUMENT;
-    kern<<<unsigned(blocks), dmmdev::kTileWarps * 32, 0, a.stream>>>(a.in, a.out, a.count, a.domain, a.ascending,
+    kern<<<unsigned(blocks), NW * 32, 0, a.stream>>>(a.in, a.out, a.count, a.domain, a.ascending,
                                                                       a.stats, a.status);
     return check_launch("k_tile_sort");
 }
@@ -267,6 +271,27 @@ dmm_status launch_general_m128(int mode, bool pk2, bool ext, const GeneralArgs& 
     if (mode == dmmdev::kModePartition)
         return launch_tile<2, dmmdev::kModePartition>(a);
     return pk2 ? launch_tile<2, dmmdev::kModeIntegerSort>(a) : launch_tile<1, dmmdev::kModeIntegerSort>(a);
+}
+
+// 32 x 256 machines (8192 keys): partition_leaf -> square_skeleton with h = 16 (partition.hpp:
+// 156-172, sort.hpp:250-280) or sort_wide_any; every outcome is the sorted machine, which the
+// 8-warp tile sort produces
+dmm_status launch_general_m256(int mode, bool pk2, bool ext, const GeneralArgs& a) {
+    if (ext) {
+        set_error("extension kernels are only built where the reference rejects the shape");
+        return DMM_UNSUPPORTED_SHAPE;
+    }
+    if (a.probe) {
+        set_error("32 x 256 machines: no probe (w <= m has no PartitionProbe point)");
+        return DMM_INVALID_ARGUMENT;
+    }
+    if (a.count == 0)
+        return DMM_OK;
+    if (mode == dmmdev::kModeSortAny)
+        return launch_tile<1, dmmdev::kModeSortAny, 8>(a);
+    if (mode == dmmdev::kModePartition)
+        return launch_tile<2, dmmdev::kModePartition, 8>(a);
+    return pk2 ? launch_tile<2, dmmdev::kModeIntegerSort, 8>(a) : launch_tile<1, dmmdev::kModeIntegerSort, 8>(a);
 }
 
 }  // namespace dmmhost

@@ -300,3 +300,29 @@ def test_partition_general_32x128_vs_oracle(port):
     bad[1, 4, 4] = 40
     with pytest.raises(dmm.InvalidInstance):
         dmm.partition_general(bad)
+
+
+def test_32x256_vs_oracle(port):
+    # 32 x 256 (partition_leaf -> square_skeleton with h = 16; 51 513 steps): the
+    # 8-warp tile kernel in partition (two instances per register), integer-sort and
+    # comparison modes, against the oracle
+    seeds = list(range(1, 12))
+    grids = _oracle_batch(port, 1, 32, 256, seeds)
+    out, st = dmm.partition_general(grids)
+    out = dmm.as_uint32(out)
+    for k in range(len(seeds)):
+        ost, oout, orep = port.partition_general(grids[k])
+        assert ost == 0 and (out[k] == oout).all()
+        assert int(st.cleanup_retries[k]) == orep["cleanup_retries"]
+    rng = np.random.default_rng(256)
+    keys = rng.integers(0, 2 ** 32, size=(7, 32, 256), dtype=np.uint64).astype(np.uint32)
+    out, _ = dmm.integer_sort_general(keys, 1 << 32)
+    out = dmm.as_uint32(out)
+    for k in range(7):
+        ost, oout, _ = port.integer_sort_general(keys[k], 1 << 32)
+        assert ost == 0 and (out[k] == oout).all()
+    for asc in (True, False):
+        o2 = dmm.as_uint32(dmm.sort_wide_any(keys, ascending=asc))
+        for k in range(7):
+            exp = np.sort(keys[k].ravel())
+            assert (o2[k].ravel() == (exp if asc else exp[::-1])).all()
