@@ -424,8 +424,8 @@ __global__ void __launch_bounds__(1024, 1)
 // The label machines, four per CTA (count_row_sort4): partition_short_wide, partition_general /
 // integer_sort_general with domain <= 32 and the partition's ShortWideHook probe.  Persistent
 // over groups of four machines; each CTA prefetches its next group into L2 (four 128 KB bulk
-// prefetches) at the start of the current one, and threads load / store their row chunks
-// (row r, columns 32k .. 32k + 31) with 16-byte global accesses.
+// prefetches) at the start of the current one; machines move between HBM / L2 and the
+// shared staging copy by TMA bulk copies, one at a time (the staging copy is 128 KB).
 template <int MODE>
 __global__ void __launch_bounds__(1024, 1)
     k_short_wide32_labels(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count,
@@ -435,36 +435,48 @@ __global__ void __launch_bounds__(1024, 1)
     uint32_t* S = smem;
     uint32_t* T = smem + kStage;
     uint32_t* F = T + kTab4;  // four flag words: two per task parity
+    uint64_t* bar = reinterpret_cast<uint64_t*>(F + 4);
     const int tid = threadIdx.x, k = tid >> 5, r = tid & 31;
+    const int c = (k + r) & 31;  // rotated stride column: bank c on the row-major staging copy
     const bool asc = ascending != 0;
     const bool part = MODE == kModePartition || (MODE == kModeSortAny && domain < (1ull << 32));
     uint32_t* slab = S + k * kSlab;
     const uint32_t d = domain < 32 ? (uint32_t)domain : 32u;
     if (tid < 4)
         F[tid] = 0;
+    if (tid == 0)
+        mbar_init(bar);
     __syncthreads();
-    uint32_t parity = 0;
+    uint32_t parity = 0, bpar = 0;
     for (uint64_t m0 = (uint64_t)blockIdx.x * 4; m0 < count; m0 += (uint64_t)gridDim.x * 4, parity ^= 1) {
         const uint64_t nx = m0 + (uint64_t)gridDim.x * 4;
         if (tid < 4 && nx + tid < count)
             prefetch_l2(in + (nx + tid) * kWords, kBytes);
+        // ingest: machine b streams into S by one TMA bulk copy (from L2: prefetched a group
+        // ago), every thread takes its row's words (row r, columns 32j + c: bank c) into byte b
         uint32_t x[32];
         uint32_t bad = 0;
-#pragma unroll
+#pragma unroll 1
         for (int b = 0; b < 4; ++b) {
             const uint64_t inst = m0 + b;
-            const uint4* q = reinterpret_cast<const uint4*>(in + inst * kWords + r * kM + 32 * k);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const uint4 t = inst < count ? __ldg(q + i) : make_uint4(0, 0, 0, 0);
-                const uint32_t v[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    bad |= v[e] >= d ? (1u << b) : 0u;
-                    const uint32_t c = min(v[e], 31u) << (8 * b);
-                    x[4 * i + e] = b == 0 ? c : (x[4 * i + e] | c);
+            if (inst < count) {
+                if (tid == 0) {
+                    bulk_wait_read();  // the previous group's last store has left S
+                    fence_async_smem();
+                    tma_load(S, in + inst * kWords, kBytes, bar);
                 }
+                mbar_wait(bar, bpar);
+                bpar ^= 1;
             }
+            const uint32_t* src = S + r * kM + c;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t v = inst < count ? src[32 * j] : 0u;
+                bad |= v >= d ? (1u << b) : 0u;
+                const uint32_t cv = min(v, 31u) << (8 * b);
+                x[j] = b == 0 ? cv : (x[j] | cv);
+            }
+            __syncthreads();  // S is read
         }
         uint32_t* Fb = F + 2 * parity;
         {
@@ -515,16 +527,25 @@ __global__ void __launch_bounds__(1024, 1)
             for (int b = 0; b < 4; ++b)
                 mism |= ((diff >> (8 * b)) & 0xFFu) ? (1u << b) : 0u;
         }
-#pragma unroll
+        // egress: the rotated stride layout (row r, columns 32j + c) writes the row-major staging
+        // copy conflict-free; machine b leaves S by one TMA bulk copy
+        chunk_to_stride(x, S, k, r, c);
+#pragma unroll 1
         for (int b = 0; b < 4; ++b) {
             const uint64_t inst = m0 + b;
             if (inst >= count)
                 break;
-            uint4* q = reinterpret_cast<uint4*>(out + inst * kWords + r * kM + 32 * k);
+            if (tid == 0)
+                bulk_wait_read();  // machine b - 1 has left S
+            __syncthreads();
+            uint32_t* dst = S + r * kM + c;
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-                q[i] = make_uint4((x[4 * i] >> (8 * b)) & 0xFFu, (x[4 * i + 1] >> (8 * b)) & 0xFFu,
-                                  (x[4 * i + 2] >> (8 * b)) & 0xFFu, (x[4 * i + 3] >> (8 * b)) & 0xFFu);
+            for (int j = 0; j < 32; ++j)
+                dst[32 * j] = (x[j] >> (8 * b)) & 0xFFu;
+            fence_async_smem();
+            __syncthreads();
+            if (tid == 0)
+                tma_store(out + inst * kWords, S, kBytes);
         }
         {
             const uint32_t wm = __reduce_or_sync(0xFFFFFFFFu, mism);
@@ -548,6 +569,8 @@ __global__ void __launch_bounds__(1024, 1)
             }
         }
     }
+    if (tid == 0)
+        bulk_wait_all();
 }
 
 }  // namespace sw32
@@ -575,7 +598,7 @@ dmm_status launch_sw32(const GeneralArgs& a) {
 template <int MODE>
 dmm_status launch_sw32_labels(const GeneralArgs& a) {
     auto kern = dmmdev::sw32::k_short_wide32_labels<MODE>;
-    constexpr size_t smem = size_t(dmmdev::sw32::kStage + dmmdev::sw32::kTab4 + 4) * 4;
+    constexpr size_t smem = size_t(dmmdev::sw32::kStage + dmmdev::sw32::kTab4 + 8) * 4;
     static std::atomic<uint64_t> configured{0};
     if (dmm_status e = configure_kernel(kern, smem, configured); e != DMM_OK)
         return e;
