@@ -150,6 +150,7 @@ __device__ __forceinline__ void count_row_sort(uint32_t (&x)[32], uint32_t* S, u
 // suffices); the row totals add the four bytes in 16-bit lanes (even / odd bytes), and warp b
 // (b < 4) builds machine b's run tables.  Same schedule, per machine, as count_row_sort.
 constexpr int kTab4 = 4 * 2 * 32 * 32;  // E and NX tables of the four machines
+constexpr int kSplit = 16;              // bulk copies per machine load / store (8 KB each)
 template <class AfterCount>
 __device__ __forceinline__ void count_row_sort4(uint32_t (&x)[32], uint32_t* S, uint32_t* T, int k, int r, bool desc,
                                                 AfterCount&& after_count) {
@@ -460,10 +461,12 @@ __global__ void __launch_bounds__(1024, 1)
         for (int b = 0; b < 4; ++b) {
             const uint64_t inst = m0 + b;
             if (inst < count) {
-                if (tid == 0) {
-                    bulk_wait_read();  // the previous group's last store has left S
+                if (k == 0) {
+                    if (r < kSplit)
+                        bulk_wait_read();  // the previous group's last stores have left S
+                    __syncwarp();
                     fence_async_smem();
-                    tma_load(S, in + inst * kWords, kBytes, bar);
+                    tma_load_split(S, in + inst * kWords, kBytes, bar, r, kSplit);
                 }
                 mbar_wait(bar, bpar);
                 bpar ^= 1;
@@ -535,8 +538,8 @@ __global__ void __launch_bounds__(1024, 1)
             const uint64_t inst = m0 + b;
             if (inst >= count)
                 break;
-            if (tid == 0)
-                bulk_wait_read();  // machine b - 1 has left S
+            if (k == 0 && r < kSplit)
+                bulk_wait_read();  // machine b - 1 has left S (each lane waits for its own copies)
             __syncthreads();
             uint32_t* dst = S + r * kM + c;
 #pragma unroll
@@ -544,8 +547,8 @@ __global__ void __launch_bounds__(1024, 1)
                 dst[32 * j] = (x[j] >> (8 * b)) & 0xFFu;
             fence_async_smem();
             __syncthreads();
-            if (tid == 0)
-                tma_store(out + inst * kWords, S, kBytes);
+            if (k == 0 && r < kSplit)  // kSplit bulk stores of one group, issued by kSplit lanes
+                tma_store(out + inst * kWords + r * (kWords / kSplit), S + r * (kWords / kSplit), kBytes / kSplit);
         }
         {
             const uint32_t wm = __reduce_or_sync(0xFFFFFFFFu, mism);
@@ -569,7 +572,7 @@ __global__ void __launch_bounds__(1024, 1)
             }
         }
     }
-    if (tid == 0)
+    if (k == 0 && r < kSplit)
         bulk_wait_all();
 }
 

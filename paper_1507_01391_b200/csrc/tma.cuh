@@ -19,6 +19,19 @@ __device__ __forceinline__ void tma_load(uint32_t* dst, const uint32_t* src, uin
                  ::"r"(sptr(dst)), "l"(src), "r"(bytes), "r"(sptr(bar))
                  : "memory");
 }
+// the same load split into `parts` bulk copies issued by lanes 0 .. parts-1 of the calling warp
+// (several copies in flight instead of one long one); the whole warp calls it
+__device__ __forceinline__ void tma_load_split(uint32_t* dst, const uint32_t* src, uint32_t bytes, uint64_t* bar,
+                                               int lane, int parts) {
+    if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sptr(bar)), "r"(bytes) : "memory");
+    __syncwarp();
+    const uint32_t part = bytes / parts;
+    if (lane < parts)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(sptr(dst + lane * (part / 4))), "l"(src + lane * (part / 4)), "r"(part), "r"(sptr(bar))
+                     : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n .reg .pred p;\n"
