@@ -232,15 +232,24 @@ def smem_line(traffic, ms):
             "source": traffic.get("source")}
 
 
-def measured_traffic(cfg_name: str):
+def measured_traffic(cfg_name: str, count: int = 0):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the config's dominant kernel,
     from the committed ncu --set full capture (profiles/traffic.json, written by
-    profiles/ncu_summarize.py --traffic), or None."""
+    profiles/ncu_summarize.py --traffic), or None.  A capture of fewer instances than this
+    run's `count` (its "instances" field) is scaled linearly to it."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f).get(cfg_name)
     except (OSError, ValueError):
         return None
+    if t and count and t.get("instances") and t["instances"] != count:
+        t = dict(t)
+        f = count / t["instances"]
+        for key in ("bytes_per_launch", "read_bytes", "write_bytes", "smem_wavefronts",
+                    "smem_excessive_wavefronts", "smem_wavefront_bytes_per_launch", "ncu_duration_us"):
+            if key in t:
+                t[key] = t[key] * f
+        t["scaled_from_instances"] = t["instances"]
     return t
 
 
@@ -613,7 +622,7 @@ def main():
         total_keys = keys_per_gpu * world
         value = total_keys / (ms_max / 1e3)
         bytes_per_launch = keys_per_gpu * 8  # algorithmic: one u32 read + one u32 write per key
-        traffic = measured_traffic(args.config)
+        traffic = measured_traffic(args.config, count)
         achieved = bytes_per_launch / (ms / 1e3) / 1e9
         line = {
             "metric": "keys/s", "value": value, "unit": "keys/s", "n_gpus": world, "steps": args.steps,

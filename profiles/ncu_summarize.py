@@ -110,6 +110,10 @@ def traffic(args):
         out = {}
     for a in args:
         cfg, rep = a.split("=", 1)
+        instances = None  # cfg=report@N: the capture ran N instances (bench.py scales to its count)
+        if "@" in rep:
+            rep, n = rep.rsplit("@", 1)
+            instances = int(n)
         m = raw_metrics(rep)
         rd = to_bytes(*m["dram__bytes_read.sum"])
         wr = to_bytes(*m["dram__bytes_write.sum"])
@@ -131,6 +135,8 @@ def traffic(args):
                                                .replace(",", "")),
                     "warp_instructions": float(m["smsp__inst_executed.sum"][0].replace(",", "")),
                     "source": os.path.join(src_dir or os.path.dirname(rep), os.path.basename(rep))}
+        if instances:
+            out[cfg]["instances"] = instances
         print(cfg, out[cfg])
     with open(path, "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)
