@@ -304,6 +304,31 @@ def verify_sort_full(g, out, count: int, tiles_exact: int = 64) -> dict:
             "ok": ok_sum and ok_xor and ok_sorted and ok_exact}
 
 
+SECONDARY = ["cfg1", "cfg1sw", "cfg2", "cfg2b", "cfg3sw", "cfg4", "cfg4s", "cfg5"]
+
+
+def run_secondaries(args) -> dict:
+    """The default run also measures every other config once (device-resident throughput,
+    20-step-style timing with fewer steps, its own correctness check, no e2e / CPU leg), so the
+    driver's single default invocation carries evidence for all BASELINE configs.  Each runs in
+    its own process (fresh device memory)."""
+    res = {}
+    for c in SECONDARY:
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", c, "--steps", "10", "--warmup", "3",
+               "--no-cpu-baseline", "--no-e2e", "--no-secondary"]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+            line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+            res[c] = {"workload": line["config"]["workload"], "value": line["value"], "unit": line["unit"],
+                      "ms_per_step": line["ms_per_step"], "steps": line["steps"],
+                      "roofline_frac": line["roofline"]["frac"], "correct": line["correct"],
+                      "sm_mhz": line["clocks"].get("sm_mhz"), "reasons": line["clocks"].get("reasons"),
+                      "gpu_launches": line["gpu_launches"]}
+        except Exception as e:  # pragma: no cover
+            res[c] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+    return res
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -340,6 +365,9 @@ def main():
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end (pinned host) leg")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="default run only: skip the device-resident lines of the other configs")
     ap.add_argument("--count", type=int, default=0, help="instances per GPU (default: the config's)")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="pipeline chunks of the end-to-end leg")
     ap.add_argument("--no-graph", action="store_true", help="time the eager launch loop instead of graph replay")
@@ -525,98 +553,108 @@ def main():
         full_check = verify_sort_full(g, out, count)
         ok = full_check["ok"]
 
-    # ---- end to end through the public API (pinned host in/out) -------------------------
-    # chunks cycle over 3 streams: H2D of chunk i+1 || kernel of chunk i || D2H of chunk i-1
-    from paper_1507_01391_b200.pipeline import run_pipelined
-    h_in = g.cpu().pin_memory()
-    h_out = torch.empty_like(h_in).pin_memory()
+    e2e_ms = None
+    if not args.no_e2e:
+        # ---- end to end through the public API (pinned host in/out) -------------------------
+        # chunks cycle over 3 streams: H2D of chunk i+1 || kernel of chunk i || D2H of chunk i-1
+        from paper_1507_01391_b200.pipeline import run_pipelined
+        h_in = g.cpu().pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
 
-    perm_slot_bufs = {}
+        perm_slot_bufs = {}
 
-    def chunk_fn(din, dout, s, lo):
-        if alg == "partition_general":
-            dmm.partition_general(din, flags=flags, out=dout, stream=s, check=False)
-        elif alg == "partition_short_wide":
-            dmm.partition_short_wide(din, out=dout, stream=s, check=False)
-        elif alg == "sort_short_wide":
-            dmm.sort_short_wide(din, out=dout, stream=s)
-        elif alg == "integer_sort_general":
-            dmm.integer_sort_general(din, 1 << 32, out=dout, stream=s, check=False)
-        elif alg == "permute":
-            bufs = perm_slot_bufs.setdefault((s.cuda_stream, din.shape[0]), {})
-            if "seeds" not in bufs:
-                bufs["seeds"] = torch.arange(1 + rank * count + lo, 1 + rank * count + lo + din.shape[0],
-                                             dtype=torch.int64, device="cuda")
-            dmm.permute_into(din, dout, None, bufs, stream=s)
+        def chunk_fn(din, dout, s, lo):
+            if alg == "partition_general":
+                dmm.partition_general(din, flags=flags, out=dout, stream=s, check=False)
+            elif alg == "partition_short_wide":
+                dmm.partition_short_wide(din, out=dout, stream=s, check=False)
+            elif alg == "sort_short_wide":
+                dmm.sort_short_wide(din, out=dout, stream=s)
+            elif alg == "integer_sort_general":
+                dmm.integer_sort_general(din, 1 << 32, out=dout, stream=s, check=False)
+            elif alg == "permute":
+                bufs = perm_slot_bufs.setdefault((s.cuda_stream, din.shape[0]), {})
+                if "seeds" not in bufs:
+                    bufs["seeds"] = torch.arange(1 + rank * count + lo, 1 + rank * count + lo + din.shape[0],
+                                                 dtype=torch.int64, device="cuda")
+                dmm.permute_into(din, dout, None, bufs, stream=s)
+            else:
+                from paper_1507_01391_b200.distributed import global_partition
+                res, _ = global_partition(din.view(-1))
+                dout.view(-1).copy_(res)
+
+        ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2e_steps = max(3, args.steps // 4)
+        if alg != "global_partition":
+            slots = run_pipelined(chunk_fn, h_in, h_out, chunks=args.e2e_chunks, nstreams=args.e2e_streams)  # warm-up
+            torch.cuda.synchronize()
+            barrier()
+            ee0.record(stream)
+            for _ in range(e2e_steps):
+                run_pipelined(chunk_fn, h_in, h_out, chunks=args.e2e_chunks, slots=slots)
+            ee1.record(stream)
         else:
-            from paper_1507_01391_b200.distributed import global_partition
-            res, _ = global_partition(din.view(-1))
-            dout.view(-1).copy_(res)
+            # the global partition is bucket-major over the whole batch, so a step is not chunked;
+            # consecutive steps are double-buffered instead (two streams, two host result buffers):
+            # step i's D2H overlaps step i+1's H2D (PCIe is full duplex)
+            e2e_streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+            d_in = [torch.empty_like(g) for _ in range(2)]
+            # a rank receives the keys of its labels from every rank: up to the receive capacity
+            cap = peers[0].capacity if args.transport == "p2p" else p2p_capacity(keys_per_gpu, world)
+            h_outs = [torch.empty(cap, dtype=torch.int32).pin_memory() for _ in range(2)]
+            d2h_keys = []
 
-    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(3, args.steps // 4)
-    if alg != "global_partition":
-        slots = run_pipelined(chunk_fn, h_in, h_out, chunks=args.e2e_chunks, nstreams=args.e2e_streams)  # warm-up
+            def gp_step(i):
+                s = e2e_streams[i % 2]
+                with torch.cuda.stream(s):
+                    d_in[i % 2].copy_(h_in, non_blocking=True)
+                    if args.transport == "p2p":
+                        res, _ = global_partition_p2p(d_in[i % 2].view(-1), peers[i % 2])
+                    else:
+                        res, _ = global_partition(d_in[i % 2].view(-1))
+                    h_outs[i % 2].view(-1)[: res.numel()].copy_(res, non_blocking=True)
+                    d2h_keys.append(res.numel())
+
+            for i in range(2):  # warm-up
+                gp_step(i)
+            torch.cuda.synchronize()
+            barrier()
+            ee0.record(stream)
+            for s in e2e_streams:
+                s.wait_stream(stream)
+            for i in range(e2e_steps):
+                gp_step(i)
+            for s in e2e_streams:
+                stream.wait_stream(s)
+            ee1.record(stream)
         torch.cuda.synchronize()
-        barrier()
-        ee0.record(stream)
-        for _ in range(e2e_steps):
-            run_pipelined(chunk_fn, h_in, h_out, chunks=args.e2e_chunks, slots=slots)
-        ee1.record(stream)
-    else:
-        # the global partition is bucket-major over the whole batch, so a step is not chunked;
-        # consecutive steps are double-buffered instead (two streams, two host result buffers):
-        # step i's D2H overlaps step i+1's H2D (PCIe is full duplex)
-        e2e_streams = [torch.cuda.Stream(), torch.cuda.Stream()]
-        d_in = [torch.empty_like(g) for _ in range(2)]
-        # a rank receives the keys of its labels from every rank: up to the receive capacity
-        cap = peers[0].capacity if args.transport == "p2p" else p2p_capacity(keys_per_gpu, world)
-        h_outs = [torch.empty(cap, dtype=torch.int32).pin_memory() for _ in range(2)]
-        d2h_keys = []
-
-        def gp_step(i):
-            s = e2e_streams[i % 2]
-            with torch.cuda.stream(s):
-                d_in[i % 2].copy_(h_in, non_blocking=True)
-                if args.transport == "p2p":
-                    res, _ = global_partition_p2p(d_in[i % 2].view(-1), peers[i % 2])
-                else:
-                    res, _ = global_partition(d_in[i % 2].view(-1))
-                h_outs[i % 2].view(-1)[: res.numel()].copy_(res, non_blocking=True)
-                d2h_keys.append(res.numel())
-
-        for i in range(2):  # warm-up
-            gp_step(i)
-        torch.cuda.synchronize()
-        barrier()
-        ee0.record(stream)
-        for s in e2e_streams:
-            s.wait_stream(stream)
-        for i in range(e2e_steps):
-            gp_step(i)
-        for s in e2e_streams:
-            stream.wait_stream(s)
-        ee1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = ee0.elapsed_time(ee1) / e2e_steps
-    t = all_reduce(torch.tensor([e2e_ms], device="cuda"), dist.ReduceOp.MAX)
-    e2e_ms = float(t.item())
-    if alg in ("partition_general", "partition_short_wide"):
-        rows = torch.arange(w, dtype=torch.int32).view(1, w, 1)
-        ok = ok and bool((h_out == rows).all())
-    elif alg == "global_partition":
-        # the last end-to-end result in host memory: this rank's labels only, bucket-major
-        got = h_outs[(e2e_steps - 1) % 2].view(-1)[: res.numel()]
-        lab = (got.to(torch.int64) & 0xFFFFFFFF) >> 29
-        ok = ok and bool(((lab >= lo) & (lab < hi)).all())
-        if world == 1:
-            ok = ok and bool((lab[1:] >= lab[:-1]).all())
+        e2e_ms = ee0.elapsed_time(ee1) / e2e_steps
+        t = all_reduce(torch.tensor([e2e_ms], device="cuda"), dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+        if alg in ("partition_general", "partition_short_wide"):
+            rows = torch.arange(w, dtype=torch.int32).view(1, w, 1)
+            ok = ok and bool((h_out == rows).all())
+        elif alg == "global_partition":
+            # the last end-to-end result in host memory: this rank's labels only, bucket-major
+            got = h_outs[(e2e_steps - 1) % 2].view(-1)[: res.numel()]
+            lab = (got.to(torch.int64) & 0xFFFFFFFF) >> 29
+            ok = ok and bool(((lab >= lo) & (lab < hi)).all())
+            if world == 1:
+                ok = ok and bool((lab[1:] >= lab[:-1]).all())
 
     # every rank's verdict (its own instances / received keys), and the seed range each rank
     # generated its instances from (disjoint shards)
     ok = bool(all_reduce(torch.tensor([int(ok)], device="cuda"), dist.ReduceOp.MIN).item())
     seed_ranges = [[1 + r * count, (r + 1) * count] for r in range(world)] if alg != "global_partition" else \
         [[r * keys_per_gpu, (r + 1) * keys_per_gpu] for r in range(world)]
+    secondary = None
+    if rank == 0 and world == 1 and not args.no_secondary and args.config == "cfg3" and not args.count:
+        import gc
+        g = out = h_in = h_out = slots = None  # noqa: F841  (release the batch before the children run)
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        secondary = run_secondaries(args)
     if rank == 0:
         peaks, peak_kind = _peaks()
         total_keys = keys_per_gpu * world
@@ -636,7 +674,7 @@ def main():
                          "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
                          else "fallback 6650 GB/s"},
             "smem": smem_line(traffic, ms),
-            "e2e": {"value": total_keys / (e2e_ms / 1e3), "unit": "keys/s",
+            "e2e": None if e2e_ms is None else {"value": total_keys / (e2e_ms / 1e3), "unit": "keys/s",
                     "h2d_bytes_per_step": keys_per_gpu * 4,
                     "d2h_bytes_per_step": (keys_per_gpu * 4 if alg != "global_partition"
                                            else int(4 * sum(d2h_keys[-e2e_steps:]) / e2e_steps))},
@@ -646,6 +684,8 @@ def main():
         }
         if full_check is not None:
             line["full_size_check"] = full_check
+        if secondary is not None:
+            line["secondary"] = secondary
         line["config"]["shards"] = {"backend": backend if world > 1 else None,
                                     ("seed_ranges" if alg != "global_partition" else "key_index_ranges"): seed_ranges}
         if not args.no_cpu_baseline:
