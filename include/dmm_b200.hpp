@@ -445,7 +445,7 @@ inline PermuteReport permute(Machine& mach, Rng& rng, const PermuteParams& param
 /// The dispatcher the reference's CLI and acceptance harness use, over the B200 kernels: the
 /// same instance checks, views, verification and report fields.  The GPU has no DMM step
 /// meter: report.steps / work are the reference's counts where modelled (dmm_modelled_steps,
-/// dmm_leaf_steps, dmm_general_steps; the permutation 0); conflicts counts the model's violations (0: every
+/// dmm_leaf_steps, dmm_general_steps, dmm_permute_steps); conflicts counts the model's violations (0: every
 /// kernel relayout is checked conflict-free at compile time); record_trace throws
 /// TraceIncomplete.
 inline RunOutcome run_algorithm(Algorithm alg, const Instance& in, const RunOptions& opt = {}) {
@@ -534,6 +534,19 @@ inline RunOutcome run_algorithm(Algorithm alg, const Instance& in, const RunOpti
                          : dmm_general_steps(dg.as<uint32_t>(), in.w, in.m, 1, domain, ds.as<uint64_t>(), nullptr,
                                              nullptr);
         if (ms == DMM_OK) {
+            std::vector<uint64_t> st(1);
+            to_host(st, ds);
+            out.report.steps = st[0];
+        }
+    } else if (alg == Algorithm::permute) {
+        // the permutation kernel's phase replay + the finish sort's meter
+        std::vector<uint32_t> g(in.grid.begin(), in.grid.end());
+        const uint64_t seed = out.report.seed;
+        DeviceBuffer dg(sizeof(uint32_t) * g.size()), dsd(sizeof(uint64_t)), ds(sizeof(uint64_t));
+        to_device(dg, g);
+        cuda_check(cudaMemcpy(dsd.ptr, &seed, sizeof(seed), cudaMemcpyHostToDevice), "H2D");
+        if (dmm_permute_steps(dg.as<uint32_t>(), in.w, in.m, 1, dsd.as<uint64_t>(), opt.alpha, 64,
+                              ds.as<uint64_t>(), nullptr) == DMM_OK) {
             std::vector<uint64_t> st(1);
             to_host(st, ds);
             out.report.steps = st[0];

@@ -182,6 +182,15 @@ dmm_status dmm_permute_from_state(const uint32_t* in, uint32_t* out, uint32_t w,
 dmm_status dmm_permute(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
                        const uint64_t* seeds, uint32_t alpha, uint32_t iter_cap, dmm_permute_report* reports,
                        uint64_t* history, uint32_t* shifts, uint8_t* status, void* workspace, void* stream);
+/* The permutation's modelled DMM step count, Machine::steps() after permute (what
+ * run_algorithm reports, instance.hpp:357): steps[k] (device, count entries) for instance k run
+ * with seeds[k] (device) -- the kernel replays every phase's data-dependent cost (shuffle, hash
+ * broadcast, rescan / communication / synchronisation per iteration, packing rounds, the
+ * three-phase delivery) and the finish's integer_sort_general is metered by
+ * dmm_general_steps.  0 where not modelled (a packed sort that exhausted its cleanup
+ * retries, the last-resort tall sort).  Off the hot path: allocates, synchronises. */
+dmm_status dmm_permute_steps(const uint32_t* in, uint32_t w, uint32_t m, uint64_t count, const uint64_t* seeds,
+                             uint32_t alpha, uint32_t iter_cap, uint64_t* steps, void* stream);
 
 /* ---- cfg5: local step of the global w-way partition across GPUs --------------- */
 /* Stable partition of n keys by label = (key >> shift) & (nbuckets-1), bucket-major into

@@ -37,6 +37,7 @@ SIGNATURES = {
     "dmm_partition_general_probe": (_int, [_vp, _vp, _u32, _u32, _u64, _u32, _vp, _vp, _vp, _u32, _vp]),
     "dmm_integer_sort_general_probe": (_int, [_vp, _vp, _u32, _u32, _u64, _u64, _u32, _vp, _vp, _vp, _u32, _vp]),
     "dmm_short_wide_probe": (_int, [_vp, _vp, _u32, _u32, _u64, _int, _int, _vp, _vp, _vp]),
+    "dmm_permute_steps": (_int, [_vp, _u32, _u32, _u64, _vp, _u32, _u32, _vp, _vp]),
     "dmm_partition_square": (_int, [_vp, _vp, _u32, _u32, _u64, _vp, _vp]),
     "dmm_partition_short_wide": (_int, [_vp, _vp, _u32, _u32, _u64, _vp, _vp]),
     "dmm_sort_short_wide": (_int, [_vp, _vp, _u32, _u32, _u64, _int, _vp]),

@@ -18,6 +18,9 @@
 //   * finish / fallback run the general-sort warp schedule (dmm_algos.cuh) on the packed
 //     32 x m' or full 32 x m view, then the three-phase delivery (each phase step writes
 //     distinct destination rows).
+#include <algorithm>
+#include <vector>
+
 #include "general_kernel.cuh"
 #include "dmm_rng.cuh"
 
@@ -30,7 +33,14 @@ struct PermArgs {
     uint32_t t;             // matching rounds ceil(log2 w)^2
     uint32_t bundle;        // ceil(2m / t)
     uint32_t width_ok;      // bit b: width 2^b passes general_sort_shape_ok && cleanup_headroom (host)
+    // step meter (dmm_permute_steps; NULL on the hot path): per instance kMeterWords words --
+    // [0,1] the steps of every phase but the finish's sort (u64), [2] the delivery's steps,
+    // [3] the finish sort's width (0: nothing sorted), [4] 1 if unmodelled (last-resort sort);
+    // sort_in: the finish sort's input matrix, w x width words per instance (w x m capacity)
+    uint32_t* meter;
+    uint32_t* sort_in;
 };
+constexpr int kMeterWords = 8;
 
 constexpr int kRngWords = 312;
 // warps (machines) per CTA: the kernel only synchronises warps, so small CTAs let the
@@ -213,7 +223,7 @@ __device__ __forceinline__ uint32_t hash_eval(uint64_t key, uint32_t m, uint32_t
 // region (row i in column i: outs[j*R + i]).
 template <int M, int R>
 __device__ __forceinline__ void three_phase_delivery(const uint32_t* q, int wp, uint32_t* outs, const Mach<R>& mc,
-                                                     uint32_t empty) {
+                                                     uint32_t empty, uint32_t* deliv_steps = nullptr) {
     const int row = mc.row;
     int cnt = 0;
     for (int c = 0; c < wp; ++c)
@@ -232,6 +242,18 @@ __device__ __forceinline__ void three_phase_delivery(const uint32_t* q, int wp, 
     // middle labels: destination rows owned by this packed row alone, one per step
     const int nmid = l0 - f;
     const int max_mid = (int)mc.max_all((uint32_t)nmid);
+    if (deliv_steps) {
+        // the reference's send() costs a read and a write step per non-empty batch: every
+        // middle step, and every slot j some row's first (last) group sends at
+        uint64_t jf = 0, jl = 0;
+        for (int c = 0; c < f; ++c)
+            jf |= 1ull << (q[c * R + row] % M);
+        for (int c = l0; c < cnt; ++c)
+            jl |= 1ull << (q[c * R + row] % M);
+        const uint32_t nf = __popcll(((uint64_t)mc.or_all((uint32_t)(jf >> 32)) << 32) | mc.or_all((uint32_t)jf));
+        const uint32_t nl = __popcll(((uint64_t)mc.or_all((uint32_t)(jl >> 32)) << 32) | mc.or_all((uint32_t)jl));
+        *deliv_steps = 2u * ((uint32_t)max_mid + nf + nl);
+    }
     for (int k = 0; k < max_mid; ++k) {
         if (k < nmid) {
             const uint32_t label = q[(f + k) * R + row];
@@ -268,8 +290,16 @@ __device__ __forceinline__ void three_phase_delivery(const uint32_t* q, int wp, 
 // Returns false on PostconditionFailed (strict): the caller falls back.
 template <int WP, int M, int R>
 __device__ __forceinline__ bool finish_packed(uint32_t (&y)[WP], uint32_t* buf, uint32_t* q, uint32_t* outs,
-                                              const Mach<R>& mc, uint32_t empty, uint32_t& retries) {
+                                              const Mach<R>& mc, uint32_t empty, uint32_t& retries,
+                                              uint32_t* meter = nullptr, uint32_t* sort_in = nullptr) {
     using V = VF<0xFFFFFFFFu, 0, 1, R, 0, WP, R, R>;
+    if (meter) {  // the finish sort's input, for the host-side meter of integer_sort_general
+#pragma unroll
+        for (int c = 0; c < WP; ++c)
+            sort_in[(uint64_t)mc.row * WP + c] = y[c];
+        if (mc.row == 0)
+            meter[3] = WP;
+    }
     GenResult res{{0u, 0u}, 0u};
     balance_divide_sort<1, V, false, 0x80000000u>(y, buf, mc.row, res);  // packed labels <= n < 2^31
     if constexpr (R == kWarp)
@@ -284,7 +314,10 @@ __device__ __forceinline__ bool finish_packed(uint32_t (&y)[WP], uint32_t* buf, 
     for (int c = 0; c < WP; ++c)
         q[c * R + mc.row] = y[c];
     mc.sync();
-    three_phase_delivery<M, R>(q, WP, outs, mc, empty);
+    uint32_t ds = 0;
+    three_phase_delivery<M, R>(q, WP, outs, mc, empty, meter ? &ds : nullptr);
+    if (meter && mc.row == 0)
+        meter[2] = ds;
     return true;
 }
 
@@ -309,7 +342,7 @@ __host__ __device__ constexpr int perm_machines_per_cta() { return R > kWarp ? 1
 template <int WP, int M, int R>
 __device__ __forceinline__ bool finish_width(uint32_t width, const uint32_t* pk, uint32_t* stage, uint32_t* B,
                                              uint32_t* outs, const Mach<R>& mc, uint32_t empty, uint32_t& retries,
-                                             bool& handled) {
+                                             bool& handled, uint32_t* meter, uint32_t* sort_in) {
     if constexpr (WP >= 2 && 2 * WP <= M && general_shape_ok_c(R, WP, false)) {
         if (width == (uint32_t)WP) {
             handled = true;
@@ -317,7 +350,7 @@ __device__ __forceinline__ bool finish_width(uint32_t width, const uint32_t* pk,
 #pragma unroll
             for (int c = 0; c < WP; ++c)
                 y[c] = pk[c * R + mc.row];
-            return finish_packed<WP, M, R>(y, stage, B, outs, mc, empty, retries);
+            return finish_packed<WP, M, R>(y, stage, B, outs, mc, empty, retries, meter, sort_in);
         }
     }
     return false;
@@ -354,6 +387,13 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
     if (k >= count)
         return;
 
+    uint32_t* meter = a.meter ? a.meter + k * kMeterWords : nullptr;
+    uint32_t* sort_in = a.meter ? a.sort_in + k * (uint64_t)W * M : nullptr;
+    uint64_t pre = 0;  // metered steps outside the finish's sort (machine-uniform)
+    constexpr uint32_t kLogW = (uint32_t)ilog2_ceil_c(W);
+    if (meter && row < kMeterWords)
+        meter[row] = 0;
+
     uint32_t x[M];
     load_row<M>(in + (k * W + row) * M, x);
     uint32_t badkey = 0;
@@ -389,6 +429,11 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
             x[c] = B[c * R + row];
         using Blk = VF<0xFFFFFFFFu, 0, 1, M, 0, M, R, R>;  // every aligned m x m block of rows
         transpose_square<Blk>(x, stage, row);
+        if (meter) {
+            // rows rotating by s != 0 read and write all m cells (gcd cycles); the m x m block
+            // transposes run in lockstep: 2 (m - 1) steps (permute.hpp:118-140)
+            pre += (mc.any(sh != 0) ? 2u * M : 0u) + 2u * (M - 1);
+        }
     }
 
     // ---- iterations permute.hpp:570-577 ---------------------------------------------------
@@ -488,6 +533,17 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
             x[c] = B[c * R + row];
         // synchronize permute.hpp:278-285
         leftover = mc.add_all(row_left);
+        if (meter) {
+            // draw_and_broadcast_hash: min(m, w) writes + doubling to w (permute.hpp:147-166);
+            // rescan_and_bucket: 5 m + 6 (live labels) accesses on the busiest row (:174-216);
+            // communication: 3 steps per colour step, empty ones included (:225-274);
+            // synchronize: one write, tree sum 2 log w, broadcast 1 + 2 log w (:278-285)
+            constexpr uint32_t h0 = M < W ? M : W;
+            uint32_t dbl = 0;
+            for (uint32_t have = h0; have < W; have *= 2)
+                ++dbl;
+            pre += h0 + 2u * dbl + 5u * M + 6u * mc.max_all(run) + 3u * a.alpha * M + 2u + 4u * kLogW;
+        }
         if (row == 0 && hist && iterations < DMM_PERMUTE_MAX_HIST)
             hist[k * DMM_PERMUTE_MAX_HIST + iterations] = leftover;
         ++iterations;
@@ -506,6 +562,15 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
             width <<= 1;
         if (2 * width <= M) {
             // compaction into the packed rows (own column)
+            if (meter) {
+                // compaction: m reads, the live writes, the pad to width, two counter writes;
+                // then t rounds of 5 + 2 bundle steps, empty batches included (:327-423)
+                uint32_t live = 0;
+#pragma unroll
+                for (int c = 0; c < M; ++c)
+                    live += x[c] != empty ? 1u : 0u;
+                pre += M + max(mc.max_all(live), width) + 2u + (uint64_t)a.t * (5u + 2u * a.bundle);
+            }
             uint32_t load = 0;
             mc.sync();
 #pragma unroll
@@ -551,6 +616,8 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
                 load = load - give + (got ? give_in : 0u);
             }
             const bool overflow = mc.any(load > width);
+            if (meter && !overflow)
+                pre += mc.max_all(width > load ? width - load : 0u);  // the final pad (:431-434)
             if (!overflow) {
                 mc.sync();
                 for (uint32_t c = load; c < width; ++c)
@@ -559,12 +626,16 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
                 used_packing = true;
                 packed_width = width;
                 bool ok = false, handled = false;
-                ok = finish_width<2, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled) || ok;
-                ok = finish_width<4, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled) || ok;
-                ok = finish_width<8, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled) || ok;
-                ok = finish_width<16, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled) || ok;
-                ok = finish_width<32, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled) || ok;
+                ok = finish_width<2, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled, meter, sort_in) || ok;
+                ok = finish_width<4, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled, meter, sort_in) || ok;
+                ok = finish_width<8, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled, meter, sort_in) || ok;
+                ok = finish_width<16, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled, meter, sort_in) || ok;
+                ok = finish_width<32, M, R>(width, pk, stage, B, outs, mc, empty, cleanup_retries, handled, meter, sort_in) || ok;
                 delivered = ok;
+                // a packed sort that ran out of cleanup retries: the reference recovers its
+                // clock past the failed attempt's stamps -- not modelled
+                if (meter && handled && !ok && row == 0)
+                    meter[4] = 1;
             }
         }
     }
@@ -586,8 +657,11 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
             for (int c = 0; c < M; ++c)
                 y[c] = B[c * R + row];
         }
+        pre += meter ? 2u * M : 0u;  // in-place compaction: m reads + m writes per row (:602-614)
         uint32_t r2 = 0;
-        if (!finish_packed<M, M, R>(y, stage, B, outs, mc, empty, r2) && M < W) {
+        if (!finish_packed<M, M, R>(y, stage, B, outs, mc, empty, r2, meter, sort_in) && M < W) {
+            if (meter && row == 0)
+                meter[4] = 1;  // the last-resort tall sort: not modelled
             // last resort: comparison tall sort of the working window left by the failed
             // attempt (permute.hpp:618-625) -- y, the same multiset in the attempt's arrangement
             using V = VF<0xFFFFFFFFu, 0, 1, R, 0, M, R, R>;
@@ -616,6 +690,10 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
     wrong = mc.or_all(wrong);
     store_row<M>(out + (k * W + row) * M, v);
     if (row == 0) {
+        if (meter) {
+            meter[0] = (uint32_t)pre;
+            meter[1] = (uint32_t)(pre >> 32);
+        }
         if (reps) {
             dmm_permute_report r;
             r.iterations = iterations;
@@ -679,7 +757,8 @@ using namespace dmmhost;
 
 static dmm_status permute_impl(const uint32_t* in, uint32_t* out, uint32_t w, uint32_t m, uint64_t count,
                        const uint64_t* seeds, const uint64_t* states, uint32_t alpha, uint32_t iter_cap, dmm_permute_report* reports,
-                       uint64_t* history, uint32_t* shifts, uint8_t* status, void* workspace, void* stream) {
+                       uint64_t* history, uint32_t* shifts, uint8_t* status, void* workspace, void* stream,
+                       uint32_t* meter = nullptr, uint32_t* sort_in = nullptr) {
     reset_launches();
     (void)workspace;
     if (m < 2 || w % m != 0)  // permute.hpp:547-548
@@ -695,6 +774,8 @@ static dmm_status permute_impl(const uint32_t* in, uint32_t* out, uint32_t w, ui
         return DMM_INVALID_ARGUMENT;
     }
     dmmdev::PermArgs a;
+    a.meter = meter;
+    a.sort_in = sort_in;
     a.alpha = alpha;
     a.iter_cap = iter_cap;
     a.threshold = permute_threshold(w, m);
@@ -754,6 +835,89 @@ dmm_status dmm_permute_from_state(const uint32_t* in, uint32_t* out, uint32_t w,
                                   void* stream) {
     return permute_impl(in, out, w, m, count, nullptr, rng_states, alpha, iter_cap, reports, history, shifts, status,
                         nullptr, stream);
+}
+
+// The permutation's modelled step count (RunReport.steps after run_algorithm(permute),
+// instance.hpp:357): the permutation kernel replays every phase's data-dependent cost
+// (PermArgs::meter) and hands over the matrix its finish sorted; that sort is metered by
+// dmm_general_steps (integer_sort_general with domain n + 1, the finish's call permute.hpp:
+// 536-541).  Off the hot path: allocates its buffers, synchronises the stream.
+dmm_status dmm_permute_steps(const uint32_t* in, uint32_t w, uint32_t m, uint64_t count, const uint64_t* seeds,
+                             uint32_t alpha, uint32_t iter_cap, uint64_t* steps, void* stream) {
+    if (count == 0)
+        return DMM_OK;
+    if (!in || !seeds || !steps)
+        return DMM_INVALID_ARGUMENT;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint64_t n = uint64_t(w) * m;
+    uint32_t *dout = nullptr, *dmeter = nullptr, *dsort = nullptr;
+    auto release = [&]() {
+        cudaFree(dout);
+        cudaFree(dmeter);
+        cudaFree(dsort);
+    };
+    if (cudaMalloc(reinterpret_cast<void**>(&dout), count * n * 4) != cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void**>(&dmeter), count * dmmdev::kMeterWords * 4) != cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void**>(&dsort), count * n * 4) != cudaSuccess) {
+        release();
+        return check_launch("cudaMalloc (permute meter)");
+    }
+    dmm_status e = permute_impl(in, dout, w, m, count, seeds, nullptr, alpha, iter_cap, nullptr, nullptr, nullptr,
+                                nullptr, nullptr, stream, dmeter, dsort);
+    std::vector<uint32_t> hm(count * dmmdev::kMeterWords);
+    if (e == DMM_OK && cudaMemcpyAsync(hm.data(), dmeter, hm.size() * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        e = check_launch("meter D2H");
+    if (e == DMM_OK && cudaStreamSynchronize(st) != cudaSuccess)
+        e = check_launch("permute meter");
+    std::vector<uint64_t> total(count, 0);
+    // the finish sorts, grouped by width: each group's matrices gathered and metered in one call
+    std::vector<uint32_t> widths;
+    for (uint64_t k = 0; k < count && e == DMM_OK; ++k) {
+        const uint32_t* r = hm.data() + k * dmmdev::kMeterWords;
+        total[k] = (uint64_t(r[1]) << 32 | r[0]) + r[2];
+        if (r[3] && std::find(widths.begin(), widths.end(), r[3]) == widths.end())
+            widths.push_back(r[3]);
+    }
+    for (uint32_t wd : widths) {
+        if (e != DMM_OK)
+            break;
+        std::vector<uint64_t> idx;
+        for (uint64_t k = 0; k < count; ++k)
+            if (hm[k * dmmdev::kMeterWords + 3] == wd)
+                idx.push_back(k);
+        uint32_t* g = nullptr;
+        uint64_t* gs = nullptr;
+        if (cudaMalloc(reinterpret_cast<void**>(&g), idx.size() * w * wd * 4) != cudaSuccess ||
+            cudaMalloc(reinterpret_cast<void**>(&gs), idx.size() * 8) != cudaSuccess) {
+            cudaFree(g);
+            e = check_launch("cudaMalloc (permute meter group)");
+            break;
+        }
+        for (uint64_t i = 0; i < idx.size() && e == DMM_OK; ++i)
+            if (cudaMemcpyAsync(g + i * w * wd, dsort + idx[i] * n, uint64_t(w) * wd * 4, cudaMemcpyDeviceToDevice,
+                                st) != cudaSuccess)
+                e = check_launch("meter gather");
+        if (e == DMM_OK)
+            e = dmm_general_steps(g, w, wd, idx.size(), n + 1, gs, nullptr, stream);
+        std::vector<uint64_t> hs(idx.size());
+        if (e == DMM_OK && cudaMemcpyAsync(hs.data(), gs, hs.size() * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+            e = check_launch("meter D2H");
+        if (e == DMM_OK && cudaStreamSynchronize(st) != cudaSuccess)
+            e = check_launch("permute meter sort");
+        for (uint64_t i = 0; i < idx.size() && e == DMM_OK; ++i)
+            total[idx[i]] += hs[i];
+        cudaFree(g);
+        cudaFree(gs);
+    }
+    for (uint64_t k = 0; k < count; ++k)
+        if (hm[k * dmmdev::kMeterWords + 4])
+            total[k] = 0;  // not modelled (a failed packed sort's clock recovery / the tall sort)
+    if (e == DMM_OK && cudaMemcpyAsync(steps, total.data(), count * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        e = check_launch("steps H2D");
+    if (e == DMM_OK && cudaStreamSynchronize(st) != cudaSuccess)
+        e = check_launch("permute meter");
+    release();
+    return e;
 }
 
 }  // extern "C"

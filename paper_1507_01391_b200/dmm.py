@@ -428,6 +428,18 @@ def permute(grid, seeds, alpha: int = 4, iter_cap: int = 64, *, out=None, stream
     return (res[0] if single else res), rep
 
 
+def permute_steps(grid, seeds, alpha: int = 4, iter_cap: int = 64, stream=None) -> torch.Tensor:
+    """Machine::steps() after permute(Machine&, Rng&) for each instance (what run_algorithm reports,
+    instance.hpp:357): int64 [count] (0 where not modelled).  Off the hot path (dmm_permute_steps)."""
+    t, _ = _as_batch(grid)
+    count, w, m = t.shape
+    sd = torch.as_tensor(np.asarray(seeds, dtype=np.uint64).astype(np.int64), device=t.device)
+    steps = torch.zeros(count, dtype=torch.int64, device=t.device)
+    _check(lib().dmm_permute_steps(t.data_ptr(), w, m, count, sd.data_ptr(), alpha, iter_cap, steps.data_ptr(),
+                                   _stream(stream)), "permute_steps")
+    return steps
+
+
 def permute_into(src: torch.Tensor, dst: torch.Tensor, seeds, bufs: dict, alpha: int = 4, iter_cap: int = 64,
                  stream=None):
     """Allocation-free permute over device tensors (bench / pipelines): reports, history,

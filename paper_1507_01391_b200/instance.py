@@ -339,6 +339,9 @@ def run_algorithms(alg: str, instances: list[Instance], *, strict: bool = True, 
         steps = general_steps(grid, w if alg == "partition_general" else w * m)[0].cpu().tolist()
     elif alg in ("sort_short_wide", "sort_square", "sort_tall") and sort_metered(alg, w, m):
         steps = sort_steps(alg, grid).cpu().tolist()
+    elif alg == "permute":
+        # the kernel's phase replay + the finish sort's meter (dmm_permute_steps)
+        steps = dmm.permute_steps(grid, seeds, alpha=alpha).cpu().tolist()
     res = o.cpu().numpy().astype(np.uint64)
     outs = []
     for k in range(count):

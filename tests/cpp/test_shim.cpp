@@ -328,6 +328,7 @@ static void run_algorithm_cases() {
             CHECK(ra.report.cleanup_retries == rb.report.cleanup_retries);
             CHECK(ra.report.iterations == rb.report.iterations && ra.report.fallback == rb.report.fallback);
             if (dmm_modelled_steps(algorithm_name(c.a), c.w, c.m) || c.a == Algorithm::sort_short_wide ||
+                c.a == Algorithm::permute ||
                 c.a == Algorithm::sort_square || c.a == Algorithm::sort_tall ||
                 c.a == Algorithm::partition_general || c.a == Algorithm::integer_sort_general)
                 // modelled / replayed meters (w > m: dmm_general_steps)

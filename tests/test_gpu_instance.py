@@ -47,7 +47,7 @@ def test_run_algorithm_matches_reference(ref, alg, w, m):
         assert (rep.iterations, rep.fallback, rep.cleanup_retries) == \
             (rr["iterations"], rr["fallback"], rr["cleanup_retries"])
         assert rep.conflicts == rr["conflicts"] == 0
-        metered = (I.modelled_steps(alg, w, m) or I.sort_metered(alg, w, m)
+        metered = (I.modelled_steps(alg, w, m) or I.sort_metered(alg, w, m) or alg == "permute"
                    or (alg in ("partition_general", "integer_sort_general")
                        and (I.leaf_metered(w, m) or I.general_metered(w, m))))
         if metered:  # the reference's meter, reproduced exactly
@@ -124,3 +124,21 @@ def test_sort_steps_match_reference(ref, alg, w, m):
     got = I.sort_steps(alg, torch.from_numpy(insts.view(np.int32)).cuda()).cpu().tolist()
     exp = [ref.run_algorithm(REF_ALG[alg], insts[k].astype(np.uint64), k + 1)[2]["steps"] for k in range(len(insts))]
     assert got == exp
+
+
+@pytest.mark.parametrize("w,m,seeds", [(32, 32, range(1, 7)), (32, 16, range(1, 7)), (32, 2, range(1, 5)),
+                                       (32, 4, range(1, 5)), (64, 8, range(1, 5)), (64, 16, range(1, 5)),
+                                       (128, 64, range(1, 4))])
+def test_permute_steps_match_reference(ref, w, m, seeds):
+    # Machine::steps() after permute (instance.hpp:357) -- the phases the kernel replays plus the
+    # finish's integer sort -- equal to the reference instance by instance, packing (32 x 32:
+    # SURVEY A.3 31646, 31640, ...) and fallback (32 x 16 seeds 1, 3, 5, 6) paths alike
+    seeds = list(seeds)
+    grids = np.stack([ref.gen_instance(2, w, m, s) for s in seeds]).astype(np.uint32)
+    got = dmm.permute_steps(grids, seeds).cpu().tolist()
+    for k, s in enumerate(seeds):
+        st, _, rr = ref.run_algorithm(REF_ALG["permute"], grids[k].astype(np.uint64), s)
+        assert st == 0
+        assert got[k] == rr["steps"], (w, m, s, got[k], rr["steps"])
+    if (w, m) == (32, 32):
+        assert got[:6] == [31646, 31640, 31644, 31652, 31648, 31640]  # SURVEY A.3 known answers
