@@ -9,7 +9,7 @@ from .dmm import (  # noqa: F401
     DivisibilityViolation, Error, GeneralStats, InvalidInstance, KeyOutOfRange, NotBijective, NotSquare, OutOfBounds,
     OverlappingViews, PackingOverflow, PermuteReports, PostconditionFailed, ShapeViolation, UnsupportedShape,
     as_uint32, gen_instances, gen_keys, multisplit, multisplit_count, multisplit_scatter_to, integer_sort_general, lib, partition_general, partition_short_wide,
-    partition_square, permute, permute_into, short_wide_probe, sort_rows, sort_short_wide, sort_square, sort_tall, sort_wide_any, supported,
+    partition_square, permute, permute_into, permute_steps, short_wide_probe, sort_rows, sort_short_wide, sort_square, sort_tall, sort_wide_any, supported,
     to_column_major, to_row_major, transpose_square, version)
 from . import instance  # noqa: F401,E402  (instance.hpp mirror: text format, run_algorithm)
 from .instance import (  # noqa: F401,E402
