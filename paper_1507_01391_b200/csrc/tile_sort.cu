@@ -226,6 +226,20 @@ __global__ void __launch_bounds__(NW * 32) k_tile_sort(const uint32_t* __restric
     }  // tile loop
 }
 
+// one ascending stage on register bit j (pairs (p, p ^ 2^j)) of the lane's 64 registers, j at
+// run time: six bodies in all, so the merge levels' code stays small (instruction cache)
+template <int PK>
+__device__ __forceinline__ void stage64(uint32_t (&x)[64], int j) {
+    switch (j) {
+        case 0: reg_stage<PK, 0, 64, 0>(x); break;
+        case 1: reg_stage<PK, 0, 64, 1>(x); break;
+        case 2: reg_stage<PK, 0, 64, 2>(x); break;
+        case 3: reg_stage<PK, 0, 64, 3>(x); break;
+        case 4: reg_stage<PK, 0, 64, 4>(x); break;
+        default: reg_stage<PK, 0, 64, 5>(x); break;
+    }
+}
+
 // 32 x 128 tiles on TWO warps of 64 keys per lane (element e = 2048 w + 64 l + r): levels 1-6
 // sort the lane's 64 registers, levels 7-12 are passes of {flip; the cross-warp stage (level
 // 12); transpose the two 32 x 32 register blocks; stages on the lane bits (transposed register
@@ -320,11 +334,16 @@ __global__ void __launch_bounds__(64) k_tile_sort64(const uint32_t* __restrict__
             __syncthreads();
         }
         // lane bits level-1 .. 6 (transposed register bits level-7 .. 0), then bit 5
-        transpose_blocks<V>(x, buf, lane);
-        stages_down<PK, 0, R>(x, (level < 11 ? level : 11) - 7);
-        reg_stage<PK, 0, R, 5>(x);
-        transpose_blocks<V>(x, buf, lane);
-        stages_down<PK, 0, R>(x, 4);
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+            transpose_blocks<V>(x, buf, lane);
+            // half 0: lane bits (transposed register bits level-7 .. 0), then bit 5;
+            // half 1: register bits 4 .. 0
+            const int top = half == 0 ? (level < 11 ? level : 11) - 7 : 4;
+#pragma unroll 1
+            for (int j = top; j >= -(1 - half); --j)
+                stage64<PK>(x, j < 0 ? 5 : j);
+        }
     }
     flip<0, R>(x, fcur ^ fdesc);
 
