@@ -226,26 +226,17 @@ __global__ void __launch_bounds__(NW * 32) k_tile_sort(const uint32_t* __restric
     }  // tile loop
 }
 
-// one ascending stage on register bit j (pairs (p, p ^ 2^j)) of the lane's 64 registers, j at
-// run time: six bodies in all, so the merge levels' code stays small (instruction cache)
-template <int PK>
-__device__ __forceinline__ void stage64(uint32_t (&x)[64], int j) {
-    switch (j) {
-        case 0: reg_stage<PK, 0, 64, 0>(x); break;
-        case 1: reg_stage<PK, 0, 64, 1>(x); break;
-        case 2: reg_stage<PK, 0, 64, 2>(x); break;
-        case 3: reg_stage<PK, 0, 64, 3>(x); break;
-        case 4: reg_stage<PK, 0, 64, 4>(x); break;
-        default: reg_stage<PK, 0, 64, 5>(x); break;
-    }
-}
-
 // 32 x 128 tiles on TWO warps of 64 keys per lane (element e = 2048 w + 64 l + r): levels 1-6
 // sort the lane's 64 registers, levels 7-12 are passes of {flip; the cross-warp stage (level
 // 12); transpose the two 32 x 32 register blocks; stages on the lane bits (transposed register
 // bits) and on register bit 5; transpose back; stages on register bits 4..0}.  12 transposes
 // and one cross-warp stage per tile instead of 14 and three: 0.81 shared wavefronts per key
-// instead of 1.06.  Selected with DMM_TILE64=1 (A/B against the 4-warp kernel).
+// instead of 1.06.  Selected with DMM_TILE64=1 (A/B against the 4-warp kernel): measured
+// SLOWER, 170 vs 181 G keys/s on cfg3 -- 0.84 wavefronts and 128 instructions per key (-24 %,
+// -12 %), but 94 registers leave 20 warps per SM and the 64-register networks' straight-line
+// code misses the instruction cache (no_inst 28 % of stalls); a run-time stage loop that fixes
+// the misses costs 31 % more instructions in register moves (156 G keys/s).
+// (profiles/r02/pipeline_ab.txt)
 template <int PK, int MODE>
 __global__ void __launch_bounds__(64) k_tile_sort64(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                                                     uint64_t count, uint64_t domain, int ascending,
@@ -334,16 +325,12 @@ __global__ void __launch_bounds__(64) k_tile_sort64(const uint32_t* __restrict__
             __syncthreads();
         }
         // lane bits level-1 .. 6 (transposed register bits level-7 .. 0), then bit 5
-#pragma unroll 1
-        for (int half = 0; half < 2; ++half) {
-            transpose_blocks<V>(x, buf, lane);
-            // half 0: lane bits (transposed register bits level-7 .. 0), then bit 5;
-            // half 1: register bits 4 .. 0
-            const int top = half == 0 ? (level < 11 ? level : 11) - 7 : 4;
-#pragma unroll 1
-            for (int j = top; j >= -(1 - half); --j)
-                stage64<PK>(x, j < 0 ? 5 : j);
-        }
+        // lane bits level-1 .. 6 (transposed register bits level-7 .. 0), then bit 5
+        transpose_blocks<V>(x, buf, lane);
+        stages_down<PK, 0, R>(x, (level < 11 ? level : 11) - 7);
+        reg_stage<PK, 0, R, 5>(x);
+        transpose_blocks<V>(x, buf, lane);
+        stages_down<PK, 0, R>(x, 4);
     }
     flip<0, R>(x, fcur ^ fdesc);
 
