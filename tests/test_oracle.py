@@ -116,7 +116,8 @@ def test_reference_rejections_and_extension(port):
     assert port.partition_general(bad, FLAG_EXT_PARTIAL_GROUPS)[0] == 2
 
 
-@pytest.mark.parametrize("shape", [(32, 32), (32, 16), (32, 64), (64, 16), (16, 16), (64, 64)])
+@pytest.mark.parametrize("shape", [(32, 32), (32, 16), (32, 64), (64, 16), (16, 16), (64, 64), (32, 128), (32, 256),
+                                   (32, 1024)])
 def test_port_vs_reference_partition(port, ref, shape):
     w, m = shape
     for s in range(10, 16):
@@ -156,3 +157,18 @@ def test_oracle_sort_wide_any(port, w, m):
         assert s == 0 and (out.ravel() == (exp if asc else exp[::-1])).all()
     s, _ = port.simple("sort_wide_any", rng.integers(0, 9, size=(32, 48), dtype=np.uint64), 1)
     assert s == 1  # DMM_SHAPE_VIOLATION
+
+
+def test_port_vs_reference_short_wide_32x1024(port, ref):
+    # the w = 32 short-wide machine (n = 32 w^2): the restatement's partition_short_wide and
+    # sort_short_wide against the reference's run_algorithm on the same instances
+    for s in (1, 2):
+        g = ref.gen_instance(1, 32, 1024, s)
+        st, rout, rep = ref.run_algorithm(3, g, s)  # partition_short_wide
+        assert st == 0 and rep["correct"] and rep["steps"] == 76 * 1024
+        ps, pout = port.simple("partition_short_wide", g)
+        assert ps == 0 and (pout == rout).all()
+        k = (ref.gen_instance(0, 32, 1024, s) >> np.uint64(32)).astype(np.uint64)
+        st, rout, rep = ref.run_algorithm(0, k, s)  # sort_short_wide
+        ps, pout = port.simple("sort_short_wide", k, 1)
+        assert st == 0 and ps == 0 and (pout == rout).all()
