@@ -55,23 +55,37 @@ constexpr int kPermWarps = DMM_PERM_WARPS;
 #endif
 
 // Collective primitives of one machine of R rows: one warp (R = 32: shuffles and warp
-// votes) or one CTA of R / 32 warps (R > 32: a machine barrier and an exchange array `xch`
-// of R words + a reduction scratch `red` of R / 32 words in shared memory).
+// votes) or one CTA of R / 32 warps (R > 32: shared-memory exchange slots and CTA barriers).
+// FAST (R > 32 machines whose colour-count area H holds them): every exchange / reduction is
+// ONE barrier -- two alternating slot sets, so a slot is rewritten only two collectives later,
+// after the intervening collective's barrier; otherwise the single-slot form (three barriers).
+// Slots overlay the start of H, dead wherever a collective runs (see k_permute).
 template <int R>
+constexpr int mach_slot_words() { return 6 * R + 2 * (R / 32); }
+template <int R, bool FAST = (R >= 128)>
 struct Mach {
-    uint32_t* xch;
+    uint32_t* xch;  // FAST: 2 x (3 R) exchange words, then 2 x (R / 32) reduction words
     uint32_t* red;
     int row;
+    mutable uint32_t par = 0;  // FAST: the slot set of the next collective
     __device__ __forceinline__ void sync() const {
         if constexpr (R == kWarp)
             __syncwarp();
         else
             __syncthreads();
     }
+    __device__ __forceinline__ uint32_t* slot() const { return xch + par * (3 * R); }
+    __device__ __forceinline__ uint32_t* rslot() const { return xch + 6 * R + par * (R / 32); }
     // value of v held by row src (every row calls)
     __device__ __forceinline__ uint32_t shfl(uint32_t v, int src) const {
         if constexpr (R == kWarp) {
             return __shfl_sync(0xFFFFFFFFu, v, src);
+        } else if constexpr (FAST) {
+            uint32_t* x = slot();
+            x[row] = v;
+            __syncthreads();
+            par ^= 1u;
+            return x[src];
         } else {
             __syncthreads();
             xch[row] = v;
@@ -81,21 +95,59 @@ struct Mach {
             return r;
         }
     }
+    // three values of row src at once (one barrier when FAST)
+    __device__ __forceinline__ void shfl3(uint32_t& a, uint32_t& b, uint32_t& c, int src) const {
+        if constexpr (R == kWarp || !FAST) {
+            a = shfl(a, src);
+            b = shfl(b, src);
+            c = shfl(c, src);
+        } else {
+            uint32_t* x = slot();
+            x[row] = a;
+            x[R + row] = b;
+            x[2 * R + row] = c;
+            __syncthreads();
+            par ^= 1u;
+            a = x[src];
+            b = x[R + src];
+            c = x[2 * R + src];
+        }
+    }
+    // FAST reductions: warp reduce, one word per warp, one barrier, every row combines
+    template <class Op>
+    __device__ __forceinline__ uint32_t reduce_fast(uint32_t v, Op op) const {
+        uint32_t* r = rslot();
+        if ((row & 31) == 0)
+            r[row >> 5] = v;
+        __syncthreads();
+        par ^= 1u;
+        uint32_t acc = r[0];
+#pragma unroll
+        for (int w = 1; w < R / 32; ++w)
+            acc = op(acc, r[w]);
+        return acc;
+    }
     __device__ __forceinline__ uint32_t or_all(uint32_t v) const {
         if constexpr (R == kWarp)
             return __reduce_or_sync(0xFFFFFFFFu, v);
+        else if constexpr (FAST)
+            return reduce_fast(__reduce_or_sync(0xFFFFFFFFu, v), [](uint32_t a, uint32_t b) { return a | b; });
         else
             return group_or<R, R>(v, row, red);
     }
     __device__ __forceinline__ uint32_t max_all(uint32_t v) const {
         if constexpr (R == kWarp)
             return __reduce_max_sync(0xFFFFFFFFu, v);
+        else if constexpr (FAST)
+            return reduce_fast(__reduce_max_sync(0xFFFFFFFFu, v), [](uint32_t a, uint32_t b) { return max(a, b); });
         else
             return group_max<R, R>(v, row, red);
     }
     __device__ __forceinline__ uint32_t add_all(uint32_t v) const {
         if constexpr (R == kWarp) {
             return __reduce_add_sync(0xFFFFFFFFu, v);
+        } else if constexpr (FAST) {
+            return reduce_fast(__reduce_add_sync(0xFFFFFFFFu, v), [](uint32_t a, uint32_t b) { return a + b; });
         } else {
             v = __reduce_add_sync(0xFFFFFFFFu, v);
             __syncthreads();
@@ -259,7 +311,6 @@ __device__ __forceinline__ void three_phase_delivery(const uint32_t* q, int wp, 
             const uint32_t label = q[(f + k) * R + row];
             outs[(label % M) * R + label / M] = label;
         }
-        mc.sync();
     }
     // first group, then last group: at step j every row sends its label with slot j
     int pf = 0, pl = l0;
@@ -271,7 +322,6 @@ __device__ __forceinline__ void three_phase_delivery(const uint32_t* q, int wp, 
                 ++pf;
             }
         }
-        mc.sync();
     }
     for (int j = 0; j < M; ++j) {
         if (pl < cnt) {
@@ -281,8 +331,10 @@ __device__ __forceinline__ void three_phase_delivery(const uint32_t* q, int wp, 
                 ++pl;
             }
         }
-        mc.sync();
     }
+    // the steps only write the output region (each destination cell once) and read the row's
+    // own column: no step needs a barrier of its own; one ends the delivery
+    mc.sync();
 }
 
 // finish (permute.hpp:536-541) on a packed R x WP view held in registers y[0..WP):
@@ -382,6 +434,7 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
     // R > 32: the machine's exchange / reduction scratch overlays the start of the colour
     // counts H: every use (input check, leftover sum, packing rounds, finish reductions,
     // delivery) falls where H is dead (and CTA barriers separate them from its uses)
+    static_assert(R < 128 || perm_h_words<M, R>() >= mach_slot_words<R>(), "FAST slots overlay H");
     const Mach<R> mc{stage, stage + R, row};
     const uint64_t k = (uint64_t)blockIdx.x * perm_machines_per_cta<R>() + mach;
     if (k >= count)
@@ -531,7 +584,9 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
 #pragma unroll
         for (int c = 0; c < M; ++c)
             x[c] = B[c * R + row];
-        // synchronize permute.hpp:278-285
+        // synchronize permute.hpp:278-285 (the barrier: H, which the exchange slots overlay, is
+        // still read by rows in their communication loop)
+        mc.sync();
         leftover = mc.add_all(row_left);
         if (meter) {
             // draw_and_broadcast_hash: min(m, w) writes + doubling to w (permute.hpp:147-166);
@@ -587,23 +642,22 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
                 const uint32_t shift = 1u + (uint32_t)(rng.word(drawn) % W);  // rng_below(W), W a power of two
                 ++drawn;
                 const int partner = (row + (int)shift) % W, src = (row - (int)shift + W) % W;
-                const uint32_t p_load = mc.shfl(cell_load, partner);
-                const bool p_recv = mc.shfl(recv ? 1u : 0u, partner) != 0;
+                // the partner's (load | received) and cursor cells, one exchange
+                uint32_t p_load = cell_load, p_recv_u = recv ? 1u : 0u, p_cursor = cell_cursor;
+                mc.shfl3(p_load, p_recv_u, p_cursor, partner);
+                const bool p_recv = p_recv_u != 0;
                 const bool sender = load > theta && !p_recv && p_load <= theta;
                 const uint32_t give = sender ? min(a.bundle, load) : 0u;
-                const uint32_t p_cursor = mc.shfl(cell_cursor, partner);
-                const uint32_t maxgive = mc.max_all(give);
-                for (uint32_t kk = 0; kk < maxgive; ++kk) {
-                    uint32_t moved = 0;
-                    if (kk < give)
-                        moved = pk[(load - 1 - kk) * R + row];
-                    mc.sync();
-                    if (kk < give && p_cursor + kk < M)
-                        pk[(p_cursor + kk) * R + partner] = moved;  // distinct partner columns
-                    mc.sync();
-                }
-                const bool got = mc.shfl(sender ? 1u : 0u, src) != 0;
-                const uint32_t give_in = mc.shfl(give, src);
+                // bundle moves into the partner's column: a sender's partner is never a sender
+                // (its load is <= theta), so no row reads a cell another row writes here -- the
+                // reference's lockstep steps need no barrier of their own (one after the loop)
+                for (uint32_t kk = 0; kk < give; ++kk)
+                    if (p_cursor + kk < M)
+                        pk[(p_cursor + kk) * R + partner] = pk[(load - 1 - kk) * R + row];
+                mc.sync();
+                uint32_t got_u = sender ? 1u : 0u, give_in = give, unused = 0;
+                mc.shfl3(got_u, give_in, unused, src);
+                const bool got = got_u != 0;
                 if (sender) {
                     cell_load = load - give;  // the own-load write lands last (permute.hpp:415-419)
                     recv = false;
