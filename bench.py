@@ -554,11 +554,17 @@ def main():
         ok = full_check["ok"]
 
     e2e_ms = None
+    e2e_count = count
     if not args.no_e2e:
         # ---- end to end through the public API (pinned host in/out) -------------------------
         # chunks cycle over 3 streams: H2D of chunk i+1 || kernel of chunk i || D2H of chunk i-1
         from paper_1507_01391_b200.pipeline import run_pipelined
-        h_in = g.cpu().pin_memory()
+        # pinned host memory: the whole batch at one GPU; with N ranks on one host each rank's
+        # end-to-end batch is capped at 16 GiB / N of input (host memory stays 32 GiB in all)
+        e2e_count = count
+        if world > 1 and alg != "global_partition":
+            e2e_count = max(1, min(count, (16 << 30) // (w * m * 4) // world))
+        h_in = g[:e2e_count].cpu().pin_memory()
         h_out = torch.empty_like(h_in).pin_memory()
 
         perm_slot_bufs = {}
@@ -647,6 +653,7 @@ def main():
     ok = bool(all_reduce(torch.tensor([int(ok)], device="cuda"), dist.ReduceOp.MIN).item())
     seed_ranges = [[1 + r * count, (r + 1) * count] for r in range(world)] if alg != "global_partition" else \
         [[r * keys_per_gpu, (r + 1) * keys_per_gpu] for r in range(world)]
+    e2e_keys = e2e_count * w * m
     secondary = None
     if rank == 0 and world == 1 and not args.no_secondary and args.config == "cfg3" and not args.count:
         import gc
@@ -674,10 +681,11 @@ def main():
                          "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
                          else "fallback 6650 GB/s"},
             "smem": smem_line(traffic, ms),
-            "e2e": None if e2e_ms is None else {"value": total_keys / (e2e_ms / 1e3), "unit": "keys/s",
-                    "h2d_bytes_per_step": keys_per_gpu * 4,
-                    "d2h_bytes_per_step": (keys_per_gpu * 4 if alg != "global_partition"
-                                           else int(4 * sum(d2h_keys[-e2e_steps:]) / e2e_steps))},
+            "e2e": None if e2e_ms is None else {"value": e2e_keys * world / (e2e_ms / 1e3), "unit": "keys/s",
+                    "h2d_bytes_per_step": e2e_keys * 4,
+                    "d2h_bytes_per_step": (e2e_keys * 4 if alg != "global_partition"
+                                           else int(4 * sum(d2h_keys[-e2e_steps:]) / e2e_steps)),
+                    "instances_per_gpu": e2e_count},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
             "correct": ok,
@@ -688,7 +696,7 @@ def main():
             line["secondary"] = secondary
         line["config"]["shards"] = {"backend": backend if world > 1 else None,
                                     ("seed_ranges" if alg != "global_partition" else "key_index_ranges"): seed_ranges}
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # rank 0 at N = 1 only
             try:
                 line["cpu_baseline"] = cpu_baseline(args.config)
             except Exception as e:  # pragma: no cover
