@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(NW * 32) k_tile_sort(const uint32_t* __restric
                                                        uint32_t* __restrict__ out, uint64_t count,
                                                        uint64_t domain, int ascending,
                                                        dmm_general_stats* __restrict__ stats,
-                                                       uint8_t* __restrict__ status) {
+                                                       uint8_t* __restrict__ status, uint64_t pf_dist) {
     static_assert(NW == 4 || NW == 8, "32 x 128 or 32 x 256 tiles");
     constexpr int LOGNW = NW == 8 ? 3 : 2;
     __shared__ __align__(16) uint32_t smem[NW * relayout_buf_words(32)];
@@ -73,8 +73,10 @@ __global__ void __launch_bounds__(NW * 32) k_tile_sort(const uint32_t* __restric
     const uint32_t fdesc = (MODE == kModeSortAny && !ascending) ? 0xFFFFFFFFu : 0u;
     for (uint64_t tile0 = (uint64_t)blockIdx.x * PK; tile0 < count; tile0 += (uint64_t)gridDim.x * PK) {
     const bool hasB = PK == 2 && tile0 + 1 < count;
-    if (threadIdx.x == 0) {
-        const uint64_t nt = tile0 + (uint64_t)gridDim.x * PK;
+    if (threadIdx.x == 0 && pf_dist) {
+        // the tile (pair) pf_dist ahead -- the next task of this slot: the persistent stride,
+        // or (one CTA per tile) the tile a CTA that starts when this one ends will take
+        const uint64_t nt = tile0 + pf_dist;
         if (nt < count) {
             const uint64_t nn = count - nt < (uint64_t)PK ? count - nt : (uint64_t)PK;
             prefetch_l2(in + nt * (32 * M), (uint32_t)(nn * 32 * M * 4));
@@ -397,18 +399,22 @@ dmm_status launch_tile(const GeneralArgs& a) {
     // slower (165 vs 184 G keys/s on cfg3, profiles/r02/pipeline_ab.txt); DMM_TILE_PERSIST=1
     // selects it
     static const bool persist = getenv("DMM_TILE_PERSIST") && getenv("DMM_TILE_PERSIST")[0] == '1';
+    // DMM_TILE_PF=1: each CTA prefetches into L2 the tile a CTA starting after it will take
+    // (SMs x resident CTAs ahead)
+    static const bool pf = getenv("DMM_TILE_PF") && getenv("DMM_TILE_PF")[0] == '1';
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, 0);
+    const uint64_t resident = uint64_t(sms) * std::max(per_sm, 1);
     uint64_t blocks = units;
-    if (persist) {
-        int dev = 0, sms = 148, per_sm = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, 0);
-        blocks = std::min<uint64_t>(units, uint64_t(sms) * std::max(per_sm, 1));
-    }
+    if (persist)
+        blocks = std::min<uint64_t>(units, resident);
     if (blocks > 0x7FFFFFFFull)
         return DMM_INVALID_ARGUMENT;
+    const uint64_t pf_dist = persist ? blocks * PK : pf ? resident * PK : 0;
     kern<<<unsigned(blocks), NW * 32, 0, a.stream>>>(a.in, a.out, a.count, a.domain, a.ascending,
-                                                                      a.stats, a.status);
+                                                                      a.stats, a.status, pf_dist);
     return check_launch("k_tile_sort");
 }
 template <int PK, int MODE>
