@@ -150,6 +150,11 @@ __device__ __forceinline__ void count_row_sort(uint32_t (&x)[32], uint32_t* S, u
 // suffices); the row totals add the four bytes in 16-bit lanes (even / odd bytes), and warp b
 // (b < 4) builds machine b's run tables.  Same schedule, per machine, as count_row_sort.
 constexpr int kTab4 = 4 * 2 * 32 * 32;  // E and NX tables of the four machines
+#ifndef DMM_SW32_EVICT_FIRST
+#define DMM_SW32_EVICT_FIRST 1
+#endif
+constexpr bool kStoreEvictFirst = DMM_SW32_EVICT_FIRST;  // results leave L2 first (the next group's
+                                                          // inputs were prefetched there)
 constexpr int kSplit = 4;               // bulk copies per machine load / store (32 KB each; 1 vs 16: no
                                         // measurable difference, 183 vs 181 G keys/s)
 template <class AfterCount>
@@ -548,8 +553,13 @@ __global__ void __launch_bounds__(1024, 1)
                 dst[32 * j] = (x[j] >> (8 * b)) & 0xFFu;
             fence_async_smem();
             __syncthreads();
-            if (k == 0 && r < kSplit)  // kSplit bulk stores of one group, issued by kSplit lanes
-                tma_store(out + inst * kWords + r * (kWords / kSplit), S + r * (kWords / kSplit), kBytes / kSplit);
+            if (k == 0 && r < kSplit) {  // kSplit bulk stores of one group, issued by kSplit lanes
+                if (kStoreEvictFirst)
+                    tma_store_evict_first(out + inst * kWords + r * (kWords / kSplit), S + r * (kWords / kSplit),
+                                          kBytes / kSplit);
+                else
+                    tma_store(out + inst * kWords + r * (kWords / kSplit), S + r * (kWords / kSplit), kBytes / kSplit);
+            }
         }
         {
             const uint32_t wm = __reduce_or_sync(0xFFFFFFFFu, mism);

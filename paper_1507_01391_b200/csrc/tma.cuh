@@ -51,6 +51,16 @@ __device__ __forceinline__ void tma_store(uint32_t* dst, const uint32_t* src, ui
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+// the same store with an L2 evict-first policy: the result streams out without displacing the
+// inputs prefetched into L2 for the next machines
+__device__ __forceinline__ void tma_store_evict_first(uint32_t* dst, const uint32_t* src, uint32_t bytes) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+                 "r"(sptr(src)), "r"(bytes), "l"(pol)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
