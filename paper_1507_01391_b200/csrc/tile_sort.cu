@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(NW * 32) k_tile_sort(const uint32_t* __restric
                                                        uint32_t* __restrict__ out, uint64_t count,
                                                        uint64_t domain, int ascending,
                                                        dmm_general_stats* __restrict__ stats,
-                                                       uint8_t* __restrict__ status, uint64_t pf_dist) {
+                                                       uint8_t* __restrict__ status, uint64_t pf_dist, int shfl6) {
     static_assert(NW == 4 || NW == 8, "32 x 128 or 32 x 256 tiles");
     constexpr int LOGNW = NW == 8 ? 3 : 2;
     __shared__ __align__(16) uint32_t smem[NW * relayout_buf_words(32)];
@@ -164,6 +164,22 @@ __global__ void __launch_bounds__(NW * 32) k_tile_sort(const uint32_t* __restric
         for (int b = level - 11; b >= 0; --b)  // stages on warp bits (levels 11 .. 10 + log2 NW)
             cross_warp_stage<PK>(x, smem, warp, lane, b);
         const int row_stages = (level < 10 ? level : 10) - 6;  // row-bit stages row_stages..0
+        if (level == 6 && shfl6) {
+            // level 6's one lane-bit stage (element bit 5 = lane bit 0) as a shuffle exchange with
+            // the neighbour lane (the lower lane keeps the minimum) instead of two transposes:
+            // one SHFL and one select-min/max per register against 80 shared instructions
+            const bool upper = lane & 1;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x[j], 1);
+                if constexpr (PK == 2)
+                    x[j] = upper ? __vmaxu2(x[j], y) : __vminu2(x[j], y);
+                else
+                    x[j] = upper ? max(x[j], y) : min(x[j], y);
+            }
+            stages_down<PK, 0, 32>(x, 4);
+            continue;
+        }
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
             transpose_blocks<V>(x, buf, lane);
@@ -413,8 +429,10 @@ dmm_status launch_tile(const GeneralArgs& a) {
     if (blocks > 0x7FFFFFFFull)
         return DMM_INVALID_ARGUMENT;
     const uint64_t pf_dist = persist ? blocks * PK : pf ? resident * PK : 0;
+    // DMM_TILE_SHFL6=0: level 6 through two transposes instead of one shuffle stage
+    static const bool shfl6 = !(getenv("DMM_TILE_SHFL6") && getenv("DMM_TILE_SHFL6")[0] == '0');
     kern<<<unsigned(blocks), NW * 32, 0, a.stream>>>(a.in, a.out, a.count, a.domain, a.ascending,
-                                                                      a.stats, a.status, pf_dist);
+                                                                      a.stats, a.status, pf_dist, shfl6 ? 1 : 0);
     return check_launch("k_tile_sort");
 }
 template <int PK, int MODE>
