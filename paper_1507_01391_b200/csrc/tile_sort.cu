@@ -164,18 +164,23 @@ __global__ void __launch_bounds__(NW * 32) k_tile_sort(const uint32_t* __restric
         for (int b = level - 11; b >= 0; --b)  // stages on warp bits (levels 11 .. 10 + log2 NW)
             cross_warp_stage<PK>(x, smem, warp, lane, b);
         const int row_stages = (level < 10 ? level : 10) - 6;  // row-bit stages row_stages..0
-        if (level == 6 && shfl6) {
-            // level 6's one lane-bit stage (element bit 5 = lane bit 0) as a shuffle exchange with
-            // the neighbour lane (the lower lane keeps the minimum) instead of two transposes:
-            // one SHFL and one select-min/max per register against 80 shared instructions
-            const bool upper = lane & 1;
+        if (level - 5 <= shfl6) {
+            // the level's lane-bit stages (element bits level-1 .. 5 = lane bits level-6 .. 0) as
+            // shuffle exchanges with the partner lane (the lower lane keeps the minimum) instead of
+            // two transposes: per stage one SHFL and a min / max per register, against 80 shared
+            // instructions per transpose pair (levels 6 and 7: fewer shared wavefronts, same
+            // issue)
+#pragma unroll 1
+            for (int b = level - 6; b >= 0; --b) {
+                const bool upper = (lane >> b) & 1;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x[j], 1);
-                if constexpr (PK == 2)
-                    x[j] = upper ? __vmaxu2(x[j], y) : __vminu2(x[j], y);
-                else
-                    x[j] = upper ? max(x[j], y) : min(x[j], y);
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x[j], 1 << b);
+                    if constexpr (PK == 2)
+                        x[j] = upper ? __vmaxu2(x[j], y) : __vminu2(x[j], y);
+                    else
+                        x[j] = upper ? max(x[j], y) : min(x[j], y);
+                }
             }
             stages_down<PK, 0, 32>(x, 4);
             continue;
@@ -429,10 +434,11 @@ dmm_status launch_tile(const GeneralArgs& a) {
     if (blocks > 0x7FFFFFFFull)
         return DMM_INVALID_ARGUMENT;
     const uint64_t pf_dist = persist ? blocks * PK : pf ? resident * PK : 0;
-    // DMM_TILE_SHFL6=0: level 6 through two transposes instead of one shuffle stage
-    static const bool shfl6 = !(getenv("DMM_TILE_SHFL6") && getenv("DMM_TILE_SHFL6")[0] == '0');
+    // DMM_TILE_SHFL=L: levels 6 .. 5 + L run their lane-bit stages as shuffle exchanges
+    // (0: every level through transposes)
+    static const int shfl = getenv("DMM_TILE_SHFL") ? atoi(getenv("DMM_TILE_SHFL")) : 1;
     kern<<<unsigned(blocks), NW * 32, 0, a.stream>>>(a.in, a.out, a.count, a.domain, a.ascending,
-                                                                      a.stats, a.status, pf_dist, shfl6 ? 1 : 0);
+                                                                      a.stats, a.status, pf_dist, shfl);
     return check_launch("k_tile_sort");
 }
 template <int PK, int MODE>
