@@ -16,6 +16,10 @@
 
 #include "dmm_device.cuh"
 
+#ifndef DMM_BLOCK_SHFL_LEVELS
+#define DMM_BLOCK_SHFL_LEVELS 1  // 32 x 32 block sorts: merge levels whose row-bit stages run as shuffles
+#endif
+constexpr int kBlockShflLevels = DMM_BLOCK_SHFL_LEVELS;
 #ifndef DMM_COMPACT_WARP_BLOCKS
 #define DMM_COMPACT_WARP_BLOCKS 1  // one-warp 32 x 32 block sorts use the looped form too (+3 % cfg1)
 #endif
@@ -322,6 +326,27 @@ __device__ __forceinline__ void sort_block_compact(uint32_t (&x)[M], uint32_t* b
         const uint32_t f = (level < 2 * L && ((V::local(lane) >> (level - L)) & 1)) ? 0xFFFFFFFFu : 0u;
         flip<V::C0, V::MV>(x, f ^ fcur);
         fcur = f;
+        // views whose local rows are the warp's lanes in order (unit stride, aligned, full)
+        constexpr bool kLaneRows = V::ST == 1 && V::WV == 32 && V::WRAP % 32 == 0 && V::LO % 32 == 0 &&
+                                   (V::ROWS > kWarp || V::MASK == 0xFFFFFFFFu);
+        if (kLaneRows && level - L <= kBlockShflLevels) {
+            // the level's row-bit stages as shuffle exchanges with the partner lane (local row
+            // bits = lane bits), no transposes (fewer shared wavefronts)
+#pragma unroll 1
+            for (int b = level - L - 1; b >= 0; --b) {
+                const bool upper = (lane >> b) & 1;
+#pragma unroll
+                for (int c = V::C0; c < V::C0 + V::MV; ++c) {
+                    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x[c], 1 << b);
+                    if constexpr (PK == 2)
+                        x[c] = upper ? __vmaxu2(x[c], y) : __vminu2(x[c], y);
+                    else
+                        x[c] = upper ? max(x[c], y) : min(x[c], y);
+                }
+            }
+            stages_down<PK, V::C0, V::MV>(x, L - 1);
+            continue;
+        }
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
             transpose_blocks<V>(x, buf, lane);

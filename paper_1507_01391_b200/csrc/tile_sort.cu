@@ -436,7 +436,7 @@ dmm_status launch_tile(const GeneralArgs& a) {
     const uint64_t pf_dist = persist ? blocks * PK : pf ? resident * PK : 0;
     // DMM_TILE_SHFL=L: levels 6 .. 5 + L run their lane-bit stages as shuffle exchanges
     // (0: every level through transposes)
-    static const int shfl = getenv("DMM_TILE_SHFL") ? atoi(getenv("DMM_TILE_SHFL")) : 1;
+    static const int shfl = getenv("DMM_TILE_SHFL") ? atoi(getenv("DMM_TILE_SHFL")) : 2;
     kern<<<unsigned(blocks), NW * 32, 0, a.stream>>>(a.in, a.out, a.count, a.domain, a.ascending,
                                                                       a.stats, a.status, pf_dist, shfl);
     return check_launch("k_tile_sort");
