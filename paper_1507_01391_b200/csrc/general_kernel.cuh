@@ -413,6 +413,10 @@ dmm_status launch_general_m32(int mode, bool pk2, bool ext, const GeneralArgs& a
 dmm_status launch_general_m64(int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_m128(int mode, bool pk2, bool ext, const GeneralArgs& a);
 dmm_status launch_general_m256(int mode, bool pk2, bool ext, const GeneralArgs& a);
+// leaf-only partitions / small-domain integer sorts of 32 x {32, 64, 128, 256} views as one
+// per-bank counting pass (partition_count.cu); the launchers below try it first
+bool partition_count_applies(uint32_t m, int mode, const GeneralArgs& a);
+dmm_status launch_partition_count(uint32_t m, int mode, const GeneralArgs& a);
 // 32 x 1024: the short-wide skeleton on a CTA of 32 warps (short_wide32.cu)
 dmm_status launch_general_m1024(int mode, bool pk2, bool ext, const GeneralArgs& a);
 // multi-warp machines (w = 64, 128, 256 rows, one per CTA), general_tall*.cu

@@ -10,6 +10,8 @@ dmm_status launch_general_m32(int mode, bool pk2, bool ext, const GeneralArgs& a
         set_error("extension kernels are only built where the reference rejects the shape");
         return DMM_UNSUPPORTED_SHAPE;
     }
+    if (partition_count_applies(32, mode, a))
+        return launch_partition_count(32, mode, a);
     // w = m: partition_leaf only (any starting layout).  DMM_PIPE selects a persistent variant
     // (2 = L2 prefetch of the next task, 1 = TMA into a per-warp shared-memory slot); both
     // measured SLOWER than one task per warp (0, the default): 320 / 321 vs 351 G keys/s on

@@ -8,6 +8,8 @@ dmm_status launch_general_m64(int mode, bool pk2, bool ext, const GeneralArgs& a
         set_error("extension kernels are only built where the reference rejects the shape");
         return DMM_UNSUPPORTED_SHAPE;
     }
+    if (partition_count_applies(64, mode, a))
+        return launch_partition_count(64, mode, a);
     switch (mode) {
         case dmmdev::kModePartition:
             return pk2 ? launch_general<64, 2, false, dmmdev::kModePartition>(a) : launch_general<64, 1, false, dmmdev::kModePartition>(a);

@@ -463,6 +463,8 @@ dmm_status launch_general_m128(int mode, bool pk2, bool ext, const GeneralArgs& 
     }
     if (a.count == 0)
         return DMM_OK;
+    if (partition_count_applies(128, mode, a))
+        return launch_partition_count(128, mode, a);
     static const bool t64 = getenv("DMM_TILE64") && getenv("DMM_TILE64")[0] == '1';
     if (t64) {
         if (mode == dmmdev::kModeSortAny)
@@ -492,6 +494,8 @@ dmm_status launch_general_m256(int mode, bool pk2, bool ext, const GeneralArgs& 
     }
     if (a.count == 0)
         return DMM_OK;
+    if (partition_count_applies(256, mode, a))
+        return launch_partition_count(256, mode, a);
     if (mode == dmmdev::kModeSortAny)
         return launch_tile<1, dmmdev::kModeSortAny, 8>(a);
     if (mode == dmmdev::kModePartition)
