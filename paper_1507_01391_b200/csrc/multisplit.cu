@@ -16,6 +16,8 @@
 // (dmm_multisplit_count + dmm_multisplit_scatter_to: k_ms_scatter<LB, true> stores each key
 // straight into its owner's receive buffer, peer memory over NVLink) or an NCCL all-to-all
 // after dmm_multisplit (paper_1507_01391_b200/distributed.py).
+#include <cstdlib>
+
 #include "capi_common.h"
 
 namespace dmmdev {
@@ -216,9 +218,12 @@ __device__ __forceinline__ void scatter_tile(const uint32_t* __restrict__ keys, 
     const uint32_t lt = (1u << lane) - 1u;  // lanes below this one
     const uint32_t lane_nb = lane < NB ? 0xFFFFFFFFu : 0u;  // lanes that carry a bucket total
     uint32_t sl[LB > 0 ? LB : 1];                            // this lane's bucket bits as masks
+    uint32_t lbit[LB > 0 ? LB : 1];                          // the key bit of label bit i
 #pragma unroll
-    for (int i = 0; i < LB; ++i)
+    for (int i = 0; i < LB; ++i) {
         sl[i] = ((lane >> i) & 1) ? 0xFFFFFFFFu : 0u;
+        lbit[i] = 1u << (shift + i);
+    }
     uint32_t k[kG];
     bool valid[kG];
     auto load_group = [&](int r, uint32_t (&kk)[kG], bool (&vv)[kG]) {
@@ -239,21 +244,22 @@ __device__ __forceinline__ void scatter_tile(const uint32_t* __restrict__ keys, 
 #pragma unroll
         for (int j = 0; j < kG; ++j) {
             const uint32_t b = (k[j] >> shift) & (NB - 1);
-            uint32_t mo = FULL ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, valid[j]);
-            uint32_t ml = mo & lane_nb;
+            // mk: the lanes whose key carries label (lane mod NB) -- LB ballots of the label bits,
+            // each folded in by one LOP3 against this lane's own bucket bits.  Every lane's mk is
+            // a row total of its bucket, and the key's own bucket mates are lane b's mk (one
+            // shuffle), so the per-key work is the same for any NB.
+            uint32_t mk = FULL ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, valid[j]);
 #pragma unroll
             for (int i = 0; i < LB; ++i) {
-                // si: all ones iff label bit i is set; x & ~(bi ^ si) keeps the lanes that agree
-                const uint32_t si = uint32_t(int32_t(k[j] << (31 - int(shift) - i)) >> 31);
-                const uint32_t bi = __ballot_sync(0xFFFFFFFFu, si != 0u);
-                mo &= ~(bi ^ si);
-                ml &= ~(bi ^ sl[i]);
+                const uint32_t bi = __ballot_sync(0xFFFFFFFFu, (k[j] & lbit[i]) != 0u);
+                mk &= ~(bi ^ sl[i]);
             }
+            const uint32_t mo = __shfl_sync(0xFFFFFFFFu, mk, (int)b);
             uint32_t* d = reinterpret_cast<uint32_t*>(
                 __shfl_sync(0xFFFFFFFFu, reinterpret_cast<unsigned long long>(cur), (int)b));
             if (valid[j])
                 d[__popc(mo & lt)] = k[j];
-            cur += __popc(ml);
+            cur += __popc(mk & lane_nb);
         }
         if (r + kG < kMsRows * 4) {
 #pragma unroll
@@ -268,8 +274,8 @@ __device__ __forceinline__ void scatter_tile(const uint32_t* __restrict__ keys, 
 // REMOTE: bucket b goes to its own destination array dst[b] (a peer GPU's receive buffer over
 // NVLink, or any device pointer) starting at dst_base[b] -- the all-to-all fused into the
 // scatter: keys leave the SM straight for the owner's memory, no staging copy, no NCCL pass.
-template <int LB, bool REMOTE = false>
-__global__ void __launch_bounds__(256) k_ms_scatter(const uint32_t* __restrict__ keys, uint64_t n, uint32_t shift,
+template <int LB, bool REMOTE = false, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_ms_scatter(const uint32_t* __restrict__ keys, uint64_t n, uint32_t shift,
                                                     const uint64_t* __restrict__ offsets, uint64_t ntiles,
                                                     uint32_t* __restrict__ out, uint32_t* const* __restrict__ dst = nullptr,
                                                     const uint64_t* __restrict__ dst_base = nullptr) {
@@ -316,9 +322,17 @@ dmm_status run_multisplit(const uint32_t* keys, uint64_t n, uint32_t shift, uint
     const uint64_t grid = (ntiles + warps_per_block - 1) / warps_per_block;
     if (grid > 0x7FFFFFFFull || nblocks > 0x7FFFFFFFull)
         return DMM_INVALID_ARGUMENT;  // grid x limit
+    // DMM_MS_MINB=B (A/B, 8 buckets): ask ptxas for B resident 8-warp CTAs per SM on the scatter
+    static const int ms_minb = getenv("DMM_MS_MINB") ? atoi(getenv("DMM_MS_MINB")) : 0;
     if (phase == 2) {
-        dmmdev::k_ms_scatter<LB, true><<<unsigned(grid), warps_per_block * 32, 0, s>>>(keys, n, shift, offsets,
-                                                                                      ntiles, nullptr, dst, dst_base);
+        auto kern = dmmdev::k_ms_scatter<LB, true>;
+        if constexpr (LB == 3) {
+            if (ms_minb == 3)
+                kern = dmmdev::k_ms_scatter<LB, true, 3>;
+            else if (ms_minb == 4)
+                kern = dmmdev::k_ms_scatter<LB, true, 4>;
+        }
+        kern<<<unsigned(grid), warps_per_block * 32, 0, s>>>(keys, n, shift, offsets, ntiles, nullptr, dst, dst_base);
         return check_launch("k_ms_scatter (remote)");
     }
     dmmdev::k_ms_count<LB><<<unsigned(grid), warps_per_block * 32, 0, s>>>(keys, n, shift, tile_counts, ntiles);

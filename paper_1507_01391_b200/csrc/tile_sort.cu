@@ -57,8 +57,8 @@ __device__ __forceinline__ void cross_warp_stage(uint32_t (&x)[32], uint32_t* sl
 // the ascending sort of the complemented keys).
 // NW warps per tile: 4 (32 x 128, cfg3) or 8 (32 x 256); the tile is 1024 * NW keys and its
 // sort has 10 + log2(NW) levels, the last log2(NW) with cross-warp stages.
-template <int PK, int MODE, int NW = kTileWarps>
-__global__ void __launch_bounds__(NW * 32) k_tile_sort(const uint32_t* __restrict__ in,
+template <int PK, int MODE, int NW = kTileWarps, int MINB = 1>
+__global__ void __launch_bounds__(NW * 32, MINB) k_tile_sort(const uint32_t* __restrict__ in,
                                                        uint32_t* __restrict__ out, uint64_t count,
                                                        uint64_t domain, int ascending,
                                                        dmm_general_stats* __restrict__ stats,
@@ -415,6 +415,17 @@ namespace {
 template <int PK, int MODE, int NW = dmmdev::kTileWarps>
 dmm_status launch_tile(const GeneralArgs& a) {
     auto kern = dmmdev::k_tile_sort<PK, MODE, NW>;
+    // DMM_TILE_MINB=B: ask ptxas for B resident CTAs per SM on the cfg3 kernel (register cap
+    // 65536 / (128 B)).  Default 10 (48 registers, 40 warps per SM): 178.9 vs 175.2 G keys/s for
+    // ptxas's own choice (0: 85 registers, 24 warps per SM); 12 spills (171.0)
+    // (profiles/r02/pipeline_ab.txt)
+    if constexpr (PK == 1 && MODE == dmmdev::kModeIntegerSort && NW == 4) {
+        static const int minb = getenv("DMM_TILE_MINB") ? atoi(getenv("DMM_TILE_MINB")) : 10;
+        if (minb == 10)
+            kern = dmmdev::k_tile_sort<PK, MODE, NW, 10>;
+        else if (minb == 12)
+            kern = dmmdev::k_tile_sort<PK, MODE, NW, 12>;
+    }
     const uint64_t units = (a.count + PK - 1) / PK;
     // one CTA per tile (pair): a persistent grid with L2 prefetch of the next tile measured
     // slower (165 vs 184 G keys/s on cfg3, profiles/r02/pipeline_ab.txt); DMM_TILE_PERSIST=1
@@ -423,6 +434,13 @@ dmm_status launch_tile(const GeneralArgs& a) {
     // DMM_TILE_PF=1: each CTA prefetches into L2 the tile a CTA starting after it will take
     // (SMs x resident CTAs ahead)
     static const bool pf = getenv("DMM_TILE_PF") && getenv("DMM_TILE_PF")[0] == '1';
+    // DMM_TILE_CARVE=1 (A/B): ask for the full shared-memory carveout (the driver's default
+    // split leaves more L1)
+    static const bool carve = getenv("DMM_TILE_CARVE") && getenv("DMM_TILE_CARVE")[0] == '1';
+    static std::atomic<uint64_t> configured{0};
+    if (carve)
+        if (dmm_status e = configure_kernel(kern, 0, configured); e != DMM_OK)
+            return e;
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
