@@ -19,6 +19,7 @@
 //     32 x m' or full 32 x m view, then the three-phase delivery (each phase step writes
 //     distinct destination rows).
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "general_kernel.cuh"
@@ -270,9 +271,29 @@ __device__ __forceinline__ uint32_t hash_eval(uint64_t key, uint32_t m, uint32_t
     return (uint32_t)(splitmix64(key ^ ((uint64_t)i * 0x9e3779b97f4a7c15ULL)) % m);
 }
 
+// Where the output region lives.  32-row machines: shared memory with row i in column i
+// (outs[j*R + i]): a colour step's destinations are distinct rows, i.e. distinct banks -- the
+// paper's conflict-free delivery.  Taller machines (R > 32 rows on 32 physical banks: distinct
+// rows can share a bank, the only shared accesses with excess wavefronts in r02) deliver
+// straight into the instance's global output instead (label L is cell L of the row-major
+// result), which also returns M x R words of shared memory per machine to occupancy.
+// DMM_PERM_GOUT: 0 = always shared, 1 = R > 32 global (default), 2 = always global (A/B).
+#ifndef DMM_PERM_GOUT
+#define DMM_PERM_GOUT 1
+#endif
+template <int R>
+__host__ __device__ constexpr bool perm_gout() { return DMM_PERM_GOUT == 2 || (DMM_PERM_GOUT == 1 && R > kWarp); }
+template <int M, int R>
+__device__ __forceinline__ void deliver(uint32_t* outs, uint32_t label) {
+    if constexpr (perm_gout<R>())
+        outs[label] = label;  // cell (label / M, label % M) of the instance's row-major output
+    else
+        outs[(label % M) * R + label / M] = label;
+}
+
 // Three-phase delivery (permute.hpp:452-529) of one row's lexicographically sorted packed
 // row (own bank of q: q[c*R + row], c < WP; empty labels at the tail) into the output
-// region (row i in column i: outs[j*R + i]).
+// region (deliver()).
 template <int M, int R>
 __device__ __forceinline__ void three_phase_delivery(const uint32_t* q, int wp, uint32_t* outs, const Mach<R>& mc,
                                                      uint32_t empty, uint32_t* deliv_steps = nullptr) {
@@ -309,7 +330,7 @@ __device__ __forceinline__ void three_phase_delivery(const uint32_t* q, int wp, 
     for (int k = 0; k < max_mid; ++k) {
         if (k < nmid) {
             const uint32_t label = q[(f + k) * R + row];
-            outs[(label % M) * R + label / M] = label;
+            deliver<M, R>(outs, label);
         }
     }
     // first group, then last group: at step j every row sends its label with slot j
@@ -318,7 +339,7 @@ __device__ __forceinline__ void three_phase_delivery(const uint32_t* q, int wp, 
         if (pf < f) {
             const uint32_t label = q[pf * R + row];
             if (label % M == (uint32_t)j) {
-                outs[(label % M) * R + label / M] = label;
+                deliver<M, R>(outs, label);
                 ++pf;
             }
         }
@@ -327,7 +348,7 @@ __device__ __forceinline__ void three_phase_delivery(const uint32_t* q, int wp, 
         if (pl < cnt) {
             const uint32_t label = q[pl * R + row];
             if (label % M == (uint32_t)j) {
-                outs[(label % M) * R + label / M] = label;
+                deliver<M, R>(outs, label);
                 ++pl;
             }
         }
@@ -385,7 +406,7 @@ __host__ __device__ constexpr int perm_stage_words() {
 }
 template <int M, int R>
 __host__ __device__ constexpr int perm_machine_words() {  // u32 words of smem per machine
-    return 2 * kRngWords + M * R + perm_stage_words<M, R>();
+    return 2 * kRngWords + (perm_gout<R>() ? 0 : M * R) + perm_stage_words<M, R>();
 }
 template <int R>
 __host__ __device__ constexpr int perm_machines_per_cta() { return R > kWarp ? 1 : kPermWarps; }
@@ -422,8 +443,11 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
     const int mach = kMulti ? 0 : (int)(threadIdx.x >> 5);
     uint32_t* wbase = reinterpret_cast<uint32_t*>(smem64) + mach * perm_machine_words<M, R>();
     MachRng<R> rng{wbase, wbase + kRngWords, 0};
-    uint32_t* outs = wbase + 2 * kRngWords;     // output region, row i in column i: outs[j*R + i]
-    uint32_t* stage = outs + M * R;             // relayout buffer / own-bank rows A,B,H
+    constexpr bool kGOut = perm_gout<R>();
+    const uint64_t k = (uint64_t)blockIdx.x * perm_machines_per_cta<R>() + mach;
+    // output region: shared, row i in column i (outs[j*R + i]), or the instance's global output
+    uint32_t* outs = kGOut ? out + k * (uint64_t)n : wbase + 2 * kRngWords;
+    uint32_t* stage = wbase + 2 * kRngWords + (kGOut ? 0 : M * R);  // relayout buffer / own-bank rows A,B,H
     uint32_t* B = stage + perm_h_words<M, R>();  // colour-sorted (compacted) row
     uint32_t* pk = B;                            // packed rows (own column), capacity m: aliases B,
                                                  // which is dead from packing until the finish
@@ -436,7 +460,6 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
     // delivery) falls where H is dead (and CTA barriers separate them from its uses)
     static_assert(R < 128 || perm_h_words<M, R>() >= mach_slot_words<R>(), "FAST slots overlay H");
     const Mach<R> mc{stage, stage + R, row};
-    const uint64_t k = (uint64_t)blockIdx.x * perm_machines_per_cta<R>() + mach;
     if (k >= count)
         return;
 
@@ -453,9 +476,20 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
 #pragma unroll
     for (int c = 0; c < M; ++c) {
         badkey |= x[c] >= n ? 1u : 0u;
-        outs[c * R + row] = 0xFFFFFFFFu;  // sentinel: undelivered
+        if constexpr (!kGOut)
+            outs[c * R + row] = 0xFFFFFFFFu;  // sentinel: undelivered
     }
     badkey = mc.or_all(badkey);
+    if constexpr (kGOut) {
+        // sentinel: undelivered.  After the machine barrier of or_all every row is in registers
+        // (in == out allowed), and the first delivery follows several more barriers
+        static_assert(!kGOut || M % 4 == 0, "global output rows move as 16-byte vectors");
+        uint32_t sent[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+            sent[c] = 0xFFFFFFFFu;
+        store_row<M>(outs + (uint64_t)row * M, sent);
+    }
     if (states)
         rng.load(states + k * (kRngWords + 1), mc);
     else
@@ -577,7 +611,7 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
             const uint32_t take = min(end - start, a.alpha);
             for (uint32_t p = 0; p < take; ++p) {
                 const uint32_t label = B[(start + p) * R + row];
-                outs[(label % M) * R + label / M] = label;
+                deliver<M, R>(outs, label);
                 B[(start + p) * R + row] = empty;
             }
         }
@@ -734,15 +768,34 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
     mc.sync();
     // output region (row i in column i) -> global row-major; verify the bijection
     uint32_t v[M];
-    uint32_t wrong = badkey;
+    uint32_t wrong = badkey, undelivered = 0;
+    if constexpr (kGOut) {
+        // the deliveries of every row of this CTA are visible after the barrier (coherent
+        // loads: the cells were written in this kernel)
+        const uint4* q4 = reinterpret_cast<const uint4*>(outs + (uint64_t)row * M);
+#pragma unroll
+        for (int i = 0; i < M / 4; ++i) {
+            const uint4 t = q4[i];
+            v[4 * i] = t.x;
+            v[4 * i + 1] = t.y;
+            v[4 * i + 2] = t.z;
+            v[4 * i + 3] = t.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < M; ++j)
+            v[j] = outs[j * R + row];
+    }
 #pragma unroll
     for (int j = 0; j < M; ++j) {
-        const uint32_t o = outs[j * R + row];
+        const uint32_t o = v[j];
         wrong |= o != (uint32_t)row * M + j ? 1u : 0u;
+        undelivered |= o == 0xFFFFFFFFu ? 1u : 0u;
         v[j] = o == 0xFFFFFFFFu ? 0u : o;  // undelivered cells keep the machine's zero
     }
     wrong = mc.or_all(wrong);
-    store_row<M>(out + (k * W + row) * M, v);
+    if (!kGOut || undelivered)
+        store_row<M>(out + (k * W + row) * M, v);
     if (row == 0) {
         if (meter) {
             meter[0] = (uint32_t)pre;
@@ -783,7 +836,9 @@ dmm_status launch_permute(const uint32_t* in, uint32_t* out, uint64_t count, con
                           uint32_t* shifts, uint8_t* status, cudaStream_t s) {
     constexpr int kMach = dmmdev::perm_machines_per_cta<R>();
     auto kern = dmmdev::k_permute<M, R>;
-    const size_t smem = size_t(kMach) * dmmdev::perm_machine_words<M, R>() * sizeof(uint32_t);
+    // DMM_PERM_PAD_KB (occupancy sensitivity A/B): extra dynamic shared memory per CTA
+    static const size_t pad = getenv("DMM_PERM_PAD_KB") ? size_t(atoi(getenv("DMM_PERM_PAD_KB"))) * 1024 : 0;
+    const size_t smem = size_t(kMach) * dmmdev::perm_machine_words<M, R>() * sizeof(uint32_t) + pad;
     static std::atomic<uint64_t> configured{0};  // devices configured, per instantiation
     if (dmm_status e = configure_kernel(kern, smem, configured); e != DMM_OK)
         return e;
