@@ -54,6 +54,11 @@ constexpr int kPermWarps = DMM_PERM_WARPS;
 #ifndef DMM_PERM_TALL_MINB
 #define DMM_PERM_TALL_MINB 3
 #endif
+// CTAs per SM asked of ptxas for 32-row machines (4 per CTA): 4 = 128 registers, no spills
+// (ptxas's own choice: 168, 3 CTAs per SM); cfg4s 37.1 vs 36.4 G keys/s
+#ifndef DMM_PERM_MINB32
+#define DMM_PERM_MINB32 4
+#endif
 
 // Collective primitives of one machine of R rows: one warp (R = 32: shuffles and warp
 // votes) or one CTA of R / 32 warps (R > 32: shared-memory exchange slots and CTA barriers).
@@ -430,7 +435,7 @@ __device__ __forceinline__ bool finish_width(uint32_t width, const uint32_t* pk,
 }
 
 template <int M, int R>
-__global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DMM_PERM_TALL_MINB : 1)) k_permute(
+__global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DMM_PERM_TALL_MINB : R == kWarp ? DMM_PERM_MINB32 : 1)) k_permute(
     const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count, const uint64_t* __restrict__ seeds,
     const uint64_t* __restrict__ states, PermArgs a, dmm_permute_report* __restrict__ reps, uint64_t* __restrict__ hist,
     uint32_t* __restrict__ shifts_out, uint8_t* __restrict__ status) {
@@ -483,7 +488,6 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
     if constexpr (kGOut) {
         // sentinel: undelivered.  After the machine barrier of or_all every row is in registers
         // (in == out allowed), and the first delivery follows several more barriers
-        static_assert(!kGOut || M % 4 == 0, "global output rows move as 16-byte vectors");
         uint32_t sent[M];
 #pragma unroll
         for (int c = 0; c < M; ++c)
@@ -772,14 +776,20 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
     if constexpr (kGOut) {
         // the deliveries of every row of this CTA are visible after the barrier (coherent
         // loads: the cells were written in this kernel)
-        const uint4* q4 = reinterpret_cast<const uint4*>(outs + (uint64_t)row * M);
+        if constexpr (M % 4 == 0) {
+            const uint4* q4 = reinterpret_cast<const uint4*>(outs + (uint64_t)row * M);
 #pragma unroll
-        for (int i = 0; i < M / 4; ++i) {
-            const uint4 t = q4[i];
-            v[4 * i] = t.x;
-            v[4 * i + 1] = t.y;
-            v[4 * i + 2] = t.z;
-            v[4 * i + 3] = t.w;
+            for (int i = 0; i < M / 4; ++i) {
+                const uint4 t = q4[i];
+                v[4 * i] = t.x;
+                v[4 * i + 1] = t.y;
+                v[4 * i + 2] = t.z;
+                v[4 * i + 3] = t.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < M; ++j)
+                v[j] = outs[(uint64_t)row * M + j];
         }
     } else {
 #pragma unroll

@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(1024, 1)
 // over groups of four machines; each CTA prefetches its next group into L2 (four 128 KB bulk
 // prefetches) at the start of the current one; machines move between HBM / L2 and the
 // shared staging copy by TMA bulk copies, one at a time (the staging copy is 128 KB).
-template <int MODE>
+template <int MODE, bool DIRECT = false>
 __global__ void __launch_bounds__(1024, 1)
     k_short_wide32_labels(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count,
                           uint64_t domain, int ascending, dmm_general_stats* __restrict__ stats,
@@ -459,10 +459,33 @@ __global__ void __launch_bounds__(1024, 1)
         const uint64_t nx = m0 + (uint64_t)gridDim.x * 4;
         if (tid < 4 && nx + tid < count)
             prefetch_l2(in + (nx + tid) * kWords, kBytes);
-        // ingest: machine b streams into S by one TMA bulk copy (from L2: prefetched a group
-        // ago), every thread takes its row's words (row r, columns 32j + c: bank c) into byte b
         uint32_t x[32];
         uint32_t bad = 0;
+        if constexpr (DIRECT) {
+            // ingest: the first row sort's outcome does not depend on the order inside a row, so
+            // thread (k, r) takes row r's positions 32k .. 32k+31 straight from global memory
+            // (8 x 16-byte loads; a warp reads 32 full 128-byte segments, from L2: prefetched a
+            // group ago) -- no staging copy, no CTA barrier; byte b = machine b
+#pragma unroll 1
+            for (int b = 0; b < 4; ++b) {
+                const uint64_t inst = m0 + b;
+                const uint4* q = reinterpret_cast<const uint4*>(in + inst * kWords + r * kM + 32 * k);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const uint4 t = inst < count ? __ldg(q + i) : make_uint4(0, 0, 0, 0);
+                    const uint32_t v4[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint32_t v = v4[e];
+                        bad |= v >= d ? (1u << b) : 0u;
+                        const uint32_t cv = min(v, 31u) << (8 * b);
+                        x[4 * i + e] = b == 0 ? cv : (x[4 * i + e] | cv);
+                    }
+                }
+            }
+        } else {
+        // ingest: machine b streams into S by one TMA bulk copy (from L2: prefetched a group
+        // ago), every thread takes its row's words (row r, columns 32j + c: bank c) into byte b
 #pragma unroll 1
         for (int b = 0; b < 4; ++b) {
             const uint64_t inst = m0 + b;
@@ -486,6 +509,7 @@ __global__ void __launch_bounds__(1024, 1)
                 x[j] = b == 0 ? cv : (x[j] | cv);
             }
             __syncthreads();  // S is read
+        }
         }
         uint32_t* Fb = F + 2 * parity;
         {
@@ -536,6 +560,21 @@ __global__ void __launch_bounds__(1024, 1)
             for (int b = 0; b < 4; ++b)
                 mism |= ((diff >> (8 * b)) & 0xFFu) ? (1u << b) : 0u;
         }
+        if constexpr (DIRECT) {
+            // egress: the last row sort leaves the chunk layout (row r, positions 32k + j): each
+            // machine's bytes leave by 8 x 16-byte stores per thread (32 full segments per warp)
+#pragma unroll 1
+            for (int b = 0; b < 4; ++b) {
+                const uint64_t inst = m0 + b;
+                if (inst >= count)
+                    break;
+                uint4* q = reinterpret_cast<uint4*>(out + inst * kWords + r * kM + 32 * k);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    q[i] = make_uint4((x[4 * i] >> (8 * b)) & 0xFFu, (x[4 * i + 1] >> (8 * b)) & 0xFFu,
+                                      (x[4 * i + 2] >> (8 * b)) & 0xFFu, (x[4 * i + 3] >> (8 * b)) & 0xFFu);
+            }
+        } else {
         // egress: the rotated stride layout (row r, columns 32j + c) writes the row-major staging
         // copy conflict-free; machine b leaves S by one TMA bulk copy
         chunk_to_stride(x, S, k, r, c);
@@ -561,6 +600,7 @@ __global__ void __launch_bounds__(1024, 1)
                     tma_store(out + inst * kWords + r * (kWords / kSplit), S + r * (kWords / kSplit), kBytes / kSplit);
             }
         }
+        }
         {
             const uint32_t wm = __reduce_or_sync(0xFFFFFFFFu, mism);
             if (r == 0 && wm)
@@ -583,7 +623,7 @@ __global__ void __launch_bounds__(1024, 1)
             }
         }
     }
-    if (k == 0 && r < kSplit)
+    if (!DIRECT && k == 0 && r < kSplit)
         bulk_wait_all();
 }
 
@@ -611,7 +651,12 @@ dmm_status launch_sw32(const GeneralArgs& a) {
 }
 template <int MODE>
 dmm_status launch_sw32_labels(const GeneralArgs& a) {
-    auto kern = dmmdev::sw32::k_short_wide32_labels<MODE>;
+    // ingest / egress through the TMA staging copy (default) or, DMM_SW32_DIRECT=1, by direct
+    // 16-byte loads / stores in the chunk layout: measured 125 vs 181 G keys/s on cfg1sw -- a
+    // warp's 16-byte accesses to 32 rows 4 KB apart cost 32 L1/L2 requests per instruction,
+    // where the bulk copy streams each machine as 4 x 32 KB (profiles/r02/pipeline_ab.txt)
+    static const bool direct = getenv("DMM_SW32_DIRECT") && getenv("DMM_SW32_DIRECT")[0] == '1';
+    auto kern = direct ? dmmdev::sw32::k_short_wide32_labels<MODE, true> : dmmdev::sw32::k_short_wide32_labels<MODE, false>;
     constexpr size_t smem = size_t(dmmdev::sw32::kStage + dmmdev::sw32::kTab4 + 8) * 4;
     static std::atomic<uint64_t> configured{0};
     if (dmm_status e = configure_kernel(kern, smem, configured); e != DMM_OK)
