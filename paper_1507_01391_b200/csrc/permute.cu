@@ -44,6 +44,7 @@ struct PermArgs {
 constexpr int kMeterWords = 8;
 
 constexpr int kRngWords = 312;
+
 // warps (machines) per CTA: the kernel only synchronises warps, so small CTAs let the
 // per-warp shared-memory footprint, not the CTA granularity, set the occupancy
 #ifndef DMM_PERM_WARPS
@@ -290,6 +291,9 @@ template <int R>
 __host__ __device__ constexpr bool perm_gout() { return DMM_PERM_GOUT == 2 || (DMM_PERM_GOUT == 1 && R > kWarp); }
 template <int M, int R>
 __device__ __forceinline__ void deliver(uint32_t* outs, uint32_t label) {
+    // a label outside [0, n) (an input the status byte rejects as InvalidInstance) has no cell
+    if (label >= (uint32_t)(R * M))
+        return;
     if constexpr (perm_gout<R>())
         outs[label] = label;  // cell (label / M, label % M) of the instance's row-major output
     else

@@ -76,6 +76,24 @@ def test_permute_rejects_non_bijection(port):
         dmm.permute(g[None], [5])
 
 
+@pytest.mark.parametrize("w,m", [(32, 32), (64, 16), (128, 64)])
+def test_permute_rejects_out_of_range_labels(port, w, m):
+    # a label >= n has no output cell: the instance is InvalidInstance, nothing is written outside
+    # its own output (tall machines deliver into global memory), its neighbours are exact
+    seeds = [1, 2, 3]
+    grids = np.stack([port.gen_instance(2, w, m, s) for s in seeds]).astype(np.uint32)
+    bad = grids.copy()
+    bad[1, 0, 0] = w * m + 5
+    bad[2, w - 1, m - 1] = 0xFFFFFFFF  # the batch's last instance: past the end of the buffer
+    out, reps = dmm.permute(bad, seeds, check=False)
+    out = dmm.as_uint32(out)
+    assert reps.status.tolist() == [0, dmm.InvalidInstance.status, dmm.InvalidInstance.status]
+    ident = np.arange(w * m, dtype=np.uint32).reshape(w, m)
+    assert (out[0] == ident).all()
+    with pytest.raises(dmm.InvalidInstance):
+        dmm.permute(bad, seeds)
+
+
 @pytest.mark.parametrize("w,m,n_inst", [(64, 8, 12), (64, 16, 12), (128, 64, 6)])
 def test_permute_tall_vs_oracle(port, w, m, n_inst):
     # machines taller than a warp (one per CTA); 128 x 64 is n = 8192, the BASELINE's n,
