@@ -65,8 +65,12 @@ __device__ __forceinline__ uint32_t synth_key(uint64_t k, int row, int c) {
 #endif
 template <int M, int PK, int WM = kWarp>
 constexpr int warps_per_block() { return WM > kWarp ? WM / kWarp : (M >= 128 || M == 32 ? 4 : DMM_WPB); }
+// DMM_GEN_MINB (A/B): CTAs per SM asked of ptxas for the 32 x 8 / 32 x 16 general sorts
+#ifndef DMM_GEN_MINB
+#define DMM_GEN_MINB 1
+#endif
 template <int M, int PK>
-constexpr int min_blocks_per_sm() { return 1; }
+constexpr int min_blocks_per_sm() { return (M == 8 || M == 16) ? DMM_GEN_MINB : 1; }
 // shared-memory words per warp (WM <= 32) or per machine (WM > 32: one machine per CTA)
 template <int M, int WM>
 constexpr int staging_words() { return relayout_buf_words(M) * (WM > kWarp ? WM / kWarp : 1); }

@@ -35,6 +35,12 @@ __device__ __forceinline__ void cx_mix16(uint32_t& a, uint32_t& b) {
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h) : "r"(l), "r"(c_neg), "r"(s));
     a = l; b = h;
 }
+// max(a, b) = a ^ b ^ min(a, b): one LOP3 on the ALU pipe (is it full rate?)
+__device__ __forceinline__ void cx_lop(uint32_t& a, uint32_t& b) {
+    uint32_t l = min(a, b), h;
+    asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(h) : "r"(a), "r"(b), "r"(l));
+    a = l; b = h;
+}
 // MODE: 0 u32, 1 u16x2, 2 h2, 3 f64, 4 u32+f64 interleaved, 5 u16x2+h2 interleaved, 6 u16x2+h2+f64? (u32 semantic n/a)
 template <int MODE>
 __device__ __forceinline__ void cx(uint32_t& a, uint32_t& b, int i) {
@@ -49,6 +55,10 @@ __device__ __forceinline__ void cx(uint32_t& a, uint32_t& b, int i) {
     if (MODE == 8) { if (i % 3 == 0) cx_u32(a, b); else cx_mix(a, b); }
     if (MODE == 9) { if (i % 3 == 0) cx_u16(a, b); else cx_mix16(a, b); }
     if (MODE == 10) { if (i % 2 == 0) cx_u32(a, b); else cx_mix(a, b); }
+    if (MODE == 11) cx_lop(a, b);
+    if (MODE == 12) { if (i % 2 == 0) cx_lop(a, b); else cx_mix(a, b); }
+    if (MODE == 13) { if (i % 3 == 0) cx_lop(a, b); else cx_mix(a, b); }
+    if (MODE == 14) { if (i % 4 == 0) cx_u32(a, b); else if (i % 4 == 1) cx_lop(a, b); else cx_mix(a, b); }
 }
 
 template <int MODE>
@@ -74,6 +84,7 @@ __global__ void check(const uint32_t* a, const uint32_t* b, uint32_t* bad, int n
     uint32_t x = a[i], y = b[i];
     { uint32_t p = x, q = y, r = x, s = y; cx_u32(p, q); cx_f64(r, s); if (p != r || q != s) atomicAdd(bad, 1u); }
     { uint32_t p = x, q = y, r = x, s = y; cx_u32(p, q); cx_mix(r, s); if (p != r || q != s) atomicAdd(bad + 2, 1u); }
+    { uint32_t p = x, q = y, r = x, s = y; cx_u32(p, q); cx_lop(r, s); if (p != r || q != s) atomicAdd(bad + 4, 1u); }
     { uint32_t p = x, q = y, r = x, s = y; cx_u16(p, q); cx_mix16(r, s); if (p != r || q != s) atomicAdd(bad + 3, 1u); }
     { uint32_t p = x & 0x7BFF7BFFu, q = y & 0x7BFF7BFFu, r = p, s = q; cx_u16(p, q); cx_h2(r, s);
       if (p != r || q != s) atomicAdd(bad + 1, 1u); }
@@ -107,8 +118,12 @@ int main() {
     run<8>("u32: 1 pure : 2 IMAD-max", out);
     run<10>("u32: 1 pure : 1 IMAD-max", out);
     run<9>("U16x2: 1 pure : 2 IMAD-max", out);
+    run<11>("u32 min + LOP3 max", out);
+    run<12>("u32: 1 LOP3-max : 1 IMAD-max", out);
+    run<13>("u32: 1 LOP3-max : 2 IMAD-max", out);
+    run<14>("u32: 1 pure:1 LOP3:2 IMAD", out);
     const int n = 1 << 24;
-    uint32_t *a, *b, *bad; cudaMallocManaged(&a, n * 4); cudaMallocManaged(&b, n * 4); cudaMallocManaged(&bad, 16);
+    uint32_t *a, *b, *bad; cudaMallocManaged(&a, n * 4); cudaMallocManaged(&b, n * 4); cudaMallocManaged(&bad, 32);
     uint64_t st = 88172645463325252ull;
     for (int i = 0; i < n; ++i) {
         st ^= st << 13; st ^= st >> 7; st ^= st << 17;
@@ -116,9 +131,9 @@ int main() {
         if (i < 65536) { a[i] = i; b[i] = (i * 40503u) & 0xFFFF; }
         if (i >= 65536 && i < 131072) { a[i] = 0xFFFFFFFFu - (i & 0xFF); b[i] = i; }
     }
-    bad[0] = bad[1] = bad[2] = bad[3] = 0;
+    bad[0] = bad[1] = bad[2] = bad[3] = bad[4] = 0;
     check<<<n / 256, 256>>>(a, b, bad, n);
     cudaDeviceSynchronize();
-    printf("mismatches over %d pairs: DMNMX vs u32 %u, HMNMX2 vs U16x2 (< 0x7C00) %u, IMAD-max u32 %u, IMAD-max u16x2 %u\n", n, bad[0], bad[1], bad[2], bad[3]);
+    printf("mismatches over %d pairs: DMNMX vs u32 %u, HMNMX2 vs U16x2 (< 0x7C00) %u, IMAD-max u32 %u, IMAD-max u16x2 %u, LOP3-max u32 %u\n", n, bad[0], bad[1], bad[2], bad[3], bad[4]);
     return 0;
 }
