@@ -12,7 +12,9 @@
 //     counting sort (rescan_and_bucket), and runs alpha passes of m colour steps: in step
 //     (p, k) every row sends its p-th label of colour k to its destination cell.  The
 //     output region is laid out with row i in bank i, and the colouring guarantees the
-//     destinations of one step are distinct rows: 0 bank conflicts by the paper's argument;
+//     destinations of one step are distinct rows: 0 bank conflicts by the paper's argument
+//     (machines taller than 32 rows, whose distinct rows can share one of the 32 banks,
+//     deliver into the instance's global output instead: see deliver());
 //   * pack_leftovers' t shifted matching rounds use shuffles for the counter reads and
 //     one conflict-free step per bundle word (partners are distinct per round);
 //   * finish / fallback run the general-sort warp schedule (dmm_algos.cuh) on the packed
