@@ -209,7 +209,10 @@ __global__ void k_ms_scan_add(uint64_t* __restrict__ out, uint64_t total, const 
 // ballots); the row's per-bucket totals are the same masks for bucket = lane.  Lane b < NB
 // holds bucket b's next output address (`cur`), so a key needs one 64-bit shuffle.  FULL: the
 // whole tile is in range (no per-key bounds).
-constexpr int kG = 16;  // rows per group (4: 223, 8: 255, 16: 295, 32: 276 G keys/s on cfg5)
+#ifndef DMM_MS_G
+#define DMM_MS_G 16
+#endif
+constexpr int kG = DMM_MS_G;  // rows per group (r01 ranking: 4: 223, 8: 255, 16: 295, 32: 276 G keys/s on cfg5)
 
 template <int LB, bool FULL>
 __device__ __forceinline__ void scatter_tile(const uint32_t* __restrict__ keys, uint64_t n, uint32_t shift,
