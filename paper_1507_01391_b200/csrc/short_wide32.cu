@@ -303,6 +303,64 @@ __device__ __forceinline__ void bitonic_row_sort(uint32_t (&x)[32], uint32_t* S,
     flip<0, 32>(x, fr);
 }
 
+// The row sort that follows to_column_major needs only the merge levels.  The conversion
+// leaves new row b's chunk j (positions 32j .. 32j+31) = the sorted old row j's positions
+// 32k + b, k = 0..31, in the stride layout (thread (k, b), register j holds position 32j + k)
+// -- exactly the layout bitonic_level<6> reaches after its first exchange -- and the
+// alternating row sort before it sorted old rows 2i and 2i+1 in opposite directions, so every
+// 64-position block is already a bitonic sequence (also after the complement of a descending
+// sort).  Levels 1..5 and level 6's first exchange are skipped; the outcome is the sorted row.
+// DMM_SW32_FULLROWS=1 runs the full row sort there instead (A/B).
+#ifndef DMM_SW32_FULLROWS
+#define DMM_SW32_FULLROWS 0
+#endif
+__device__ __forceinline__ void merge_runs_row_sort(uint32_t (&x)[32], uint32_t* S, int k, int r, bool desc) {
+    const uint32_t fr = desc ? 0xFFFFFFFFu : 0u;
+    flip<0, 32>(x, fr);
+    // level 6 from its stride half: position bit 5 = register bit 0, direction = bit 6 = register bit 1
+    reg_stages<1, 0, 32, 0, 1>(x);
+    stride_to_chunk(x, S, k, r);
+    const uint32_t f = ((k >> 1) & 1) ? 0xFFFFFFFFu : 0u;  // position bit 6 = warp bit 1
+    flip<0, 32>(x, f);
+    reg_stages<1, 0, 32, 4, -1>(x);
+    flip<0, 32>(x, f);
+    bitonic_level<7>(x, S, k, r);
+    bitonic_level<8>(x, S, k, r);
+    bitonic_level<9>(x, S, k, r);
+    bitonic_level<10>(x, S, k, r);
+    flip<0, 32>(x, fr);
+}
+
+// to_row_major straight from a row sort's chunk layout: new row i gathers chunk i of every old
+// row k (positions 32i + j), which thread (i, k) holds; thread (k, i) takes it through S in one
+// exchange (word 1024 j + 32 i + ((k + i) mod 32): the writers of one warp and the readers of
+// one warp each see 32 distinct banks).  Thread (k, i) register j then holds new row i's
+// position 32j + k (the stride layout) -- and, read as a chunk-layout row, chunk k is old row
+// k's sorted chunk i.  Odd warps take their chunk reversed, so chunk pairs are bitonic.
+__device__ __forceinline__ void row_exchange(uint32_t (&x)[32], uint32_t* S, int k, int r) {
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+        S[j * kM + k * 32 + ((r + k) & 31)] = x[j];
+    __syncthreads();
+    const bool rev = (k & 1) != 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+        x[j] = S[(rev ? 31 - j : j) * kM + r * 32 + ((k + r) & 31)];
+}
+// the row sort that follows row_exchange: chunk layout in (bitonic chunk pairs), merge levels
+// 6..10 only, chunk layout out
+__device__ __forceinline__ void merge_chunks_row_sort(uint32_t (&x)[32], uint32_t* S, int k, int r, bool desc) {
+    const uint32_t fr = desc ? 0xFFFFFFFFu : 0u;
+    flip<0, 32>(x, fr);
+    bitonic_level<6>(x, S, k, r);
+    bitonic_level<7>(x, S, k, r);
+    bitonic_level<8>(x, S, k, r);
+    bitonic_level<9>(x, S, k, r);
+    bitonic_level<10>(x, S, k, r);
+    flip<0, 32>(x, fr);
+}
+
 // a ShortWideHook snapshot of the machine from the registers, row-major into dst:
 // stride = false: thread (k, r) holds row r positions 32k + j; true: positions 32j + c
 __device__ __forceinline__ void snap(uint32_t* dst, const uint32_t (&x)[32], int k, int r, bool stride, int c) {
@@ -376,6 +434,8 @@ __global__ void __launch_bounds__(1024, 1)
             const bool desc_alt = ((r & 1) == 0) != asc;
             if constexpr (COUNT)
                 count_row_sort(x, S, E, NX, k, r, desc_alt, nothing);
+            else if (!DMM_SW32_FULLROWS && pass == 1)
+                merge_chunks_row_sort(x, S, k, r, desc_alt);  // after row_exchange
             else
                 bitonic_row_sort(x, S, k, r, desc_alt);
             __syncthreads();  // S -> slabs
@@ -385,19 +445,34 @@ __global__ void __launch_bounds__(1024, 1)
             // row sort (asc or desc) into the stride layout to_row_major takes
             if constexpr (COUNT)
                 count_row_sort(x, S, E, NX, k, r, !asc, nothing);
-            else
+            else if constexpr (DMM_SW32_FULLROWS)
                 bitonic_row_sort(x, S, k, r, !asc);
-            chunk_to_stride(x, S, k, r, k);
-            __syncthreads();
-            warp_transpose(x, slab, r);  // to_row_major: chunk layout out
-            if (pass == 0 && snaps)
-                snap(snaps + kWords, x, k, r, false, 0);  // after_first_pass
+            else
+                merge_runs_row_sort(x, S, k, r, !asc);
+            if constexpr (COUNT || DMM_SW32_FULLROWS) {
+                chunk_to_stride(x, S, k, r, k);
+                __syncthreads();
+                warp_transpose(x, slab, r);  // to_row_major: chunk layout out
+                if (pass == 0 && snaps)
+                    snap(snaps + kWords, x, k, r, false, 0);  // after_first_pass
+            } else {
+                row_exchange(x, S, k, r);  // to_row_major: stride layout, odd warps reversed
+                if (pass == 0 && snaps) {
+                    // after_first_pass: register j holds position 32j + k (32 (31 - j) + k reversed)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        snaps[kWords + r * kM + 32 * ((k & 1) ? 31 - j : j) + k] = x[j];
+                }
+            }
         }
         // final row sort, chunk layout; the next machine streams into S meanwhile
         if constexpr (COUNT) {
             count_row_sort(x, S, E, NX, k, r, !asc, load_next);
         } else {
-            bitonic_row_sort(x, S, k, r, !asc);
+            if constexpr (DMM_SW32_FULLROWS)
+                bitonic_row_sort(x, S, k, r, !asc);
+            else
+                merge_chunks_row_sort(x, S, k, r, !asc);  // after row_exchange
             __syncthreads();
             load_next();
         }
