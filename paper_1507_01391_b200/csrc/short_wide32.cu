@@ -616,11 +616,28 @@ __global__ void __launch_bounds__(1024, 1)
             if (pass == 0 && snaps)
                 snap4(0, true);  // after_first_convert
             count_row_sort4(x, S, T, k, r, !asc, nothing);
-            chunk_to_stride(x, S, k, r, k);
-            __syncthreads();
-            warp_transpose(x, slab, r);  // to_row_major: chunk layout out
-            if (pass == 0 && snaps)
-                snap4(1, false);  // after_first_pass
+            if constexpr (DMM_SW32_FULLROWS) {
+                chunk_to_stride(x, S, k, r, k);
+                __syncthreads();
+                warp_transpose(x, slab, r);  // to_row_major: chunk layout out
+                if (pass == 0 && snaps)
+                    snap4(1, false);  // after_first_pass
+            } else {
+                // to_row_major as one exchange (the next counting row sort takes any
+                // arrangement of its row): stride layout, odd warps' words reversed
+                row_exchange(x, S, k, r);
+                if (pass == 0 && snaps) {  // after_first_pass
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        if (m0 + b >= count)
+                            break;
+                        uint32_t* dst = snaps + (uint64_t)b * 3 * kWords + kWords;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            dst[r * kM + 32 * ((k & 1) ? 31 - j : j) + k] = (x[j] >> (8 * b)) & 0xFFu;
+                    }
+                }
+            }
         }
         count_row_sort4(x, S, T, k, r, !asc, nothing);
         if (snaps)
