@@ -105,3 +105,16 @@ def test_cfg1_full_batch():
     bad = torch.nonzero(st.status).flatten().cpu().tolist()
     assert bad == [count // 2]
     assert bool((out[count // 2] == g[count // 2]).all())
+
+
+@pytest.mark.parametrize("m", MS)
+def test_single_instance_and_constant_keys(m):
+    # one instance (a CTA with three idle warps), domain 1 (one run), and a single-label batch
+    keys = np.zeros((1, 32, m), dtype=np.uint32)
+    out, st = dmm.integer_sort_general(keys, 1)
+    assert (dmm.as_uint32(out) == 0).all() and int(st.status[0]) == 0
+    keys = np.full((2, 32, m), 31, dtype=np.uint32)
+    out, st = dmm.integer_sort_general(keys, 32)
+    assert (dmm.as_uint32(out) == 31).all()
+    _, st = dmm.partition_general(keys, check=False)
+    assert st.status.cpu().tolist() == [dmm.InvalidInstance.status] * 2

@@ -111,3 +111,17 @@ def test_permute_tall_vs_oracle(port, w, m, n_inst):
             assert got[f] == orep[f], (w, m, s, f, got[f], orep[f])
     exp = np.arange(w * m, dtype=np.uint32).reshape(1, w, m)
     assert (out == exp).all()
+
+
+@pytest.mark.parametrize("w,m", [(32, 32), (64, 16), (128, 64)])
+def test_permute_in_place(port, w, m):
+    # out aliasing in: every row is read before any output cell is written (tall machines write
+    # their sentinels and deliveries straight into global memory after a machine barrier)
+    seeds = [7, 8, 9]
+    grids = np.stack([port.gen_instance(2, w, m, s) for s in seeds]).astype(np.uint32)
+    ref_out, ref_reps = dmm.permute(grids, seeds)
+    t = torch.from_numpy(grids.view(np.int32)).cuda()
+    out, reps = dmm.permute(t, seeds, out=t)
+    assert (dmm.as_uint32(t) == dmm.as_uint32(ref_out)).all()
+    for k in range(len(seeds)):
+        assert reps.report(k) == ref_reps.report(k)
