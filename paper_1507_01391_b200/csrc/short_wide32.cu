@@ -505,14 +505,15 @@ __global__ void __launch_bounds__(1024, 1)
 
 // The label machines, four per CTA (count_row_sort4): partition_short_wide, partition_general /
 // integer_sort_general with domain <= 32 and the partition's ShortWideHook probe.  Persistent
-// over groups of four machines; each CTA prefetches its next group into L2 (four 128 KB bulk
-// prefetches) at the start of the current one; machines move between HBM / L2 and the
+// over groups of four machines (an L2 prefetch of the next group, DMM_SW32_PF=4, measured
+// slower and read 1.6-1.8x the input bytes from DRAM: 148 SMs x 512 KB of prefetched inputs
+// beside the streaming results overflow L2 before the bulk loads arrive; off by default); machines move between HBM / L2 and the
 // shared staging copy by TMA bulk copies, one at a time (the staging copy is 128 KB).
 template <int MODE, bool DIRECT = false>
 __global__ void __launch_bounds__(1024, 1)
     k_short_wide32_labels(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count,
                           uint64_t domain, int ascending, dmm_general_stats* __restrict__ stats,
-                          uint8_t* __restrict__ status, uint32_t* __restrict__ probe) {
+                          uint8_t* __restrict__ status, uint32_t* __restrict__ probe, int pf) {
     extern __shared__ __align__(128) uint32_t smem[];
     uint32_t* S = smem;
     uint32_t* T = smem + kStage;
@@ -532,7 +533,8 @@ __global__ void __launch_bounds__(1024, 1)
     uint32_t parity = 0, bpar = 0;
     for (uint64_t m0 = (uint64_t)blockIdx.x * 4; m0 < count; m0 += (uint64_t)gridDim.x * 4, parity ^= 1) {
         const uint64_t nx = m0 + (uint64_t)gridDim.x * 4;
-        if (tid < 4 && nx + tid < count)
+        // L2 prefetch of the first pf machines of this CTA's next group (DMM_SW32_PF, default 0)
+        if (tid < pf && nx + tid < count)
             prefetch_l2(in + (nx + tid) * kWords, kBytes);
         uint32_t x[32];
         uint32_t bad = 0;
@@ -759,8 +761,11 @@ dmm_status launch_sw32_labels(const GeneralArgs& a) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t grid = std::min<uint64_t>((a.count + 3) / 4, uint64_t(sms));
+    // DMM_SW32_PF=n: L2-prefetch n machines of the next group (0 default: 198.6 vs 183.6 G keys/s
+    // with 4, DRAM reads 1.00x vs 1.63x the input; profiles/r02/pipeline_ab.txt)
+    static const int pf = getenv("DMM_SW32_PF") ? atoi(getenv("DMM_SW32_PF")) : 0;
     kern<<<unsigned(grid), 1024, smem, a.stream>>>(a.in, a.out, a.count, a.domain, a.ascending, a.stats, a.status,
-                                                   a.probe);
+                                                   a.probe, pf);
     return check_launch("k_short_wide32_labels");
 }
 }  // namespace
