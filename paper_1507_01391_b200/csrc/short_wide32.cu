@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(1024, 1)
 // slower and read 1.6-1.8x the input bytes from DRAM: 148 SMs x 512 KB of prefetched inputs
 // beside the streaming results overflow L2 before the bulk loads arrive; off by default); machines move between HBM / L2 and the
 // shared staging copy by TMA bulk copies, one at a time (the staging copy is 128 KB).
-template <int MODE, bool DIRECT = false>
+template <int MODE, bool DIRECT = false, bool PROBE = true>
 __global__ void __launch_bounds__(1024, 1)
     k_short_wide32_labels(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count,
                           uint64_t domain, int ascending, dmm_general_stats* __restrict__ stats,
@@ -596,7 +596,9 @@ __global__ void __launch_bounds__(1024, 1)
         }
         if (tid == 0)
             F[2 * (parity ^ 1)] = F[2 * (parity ^ 1) + 1] = 0;  // the next group's flags (last read a group ago)
-        uint32_t* snaps = probe != nullptr ? probe + m0 * 3 * kWords : nullptr;
+        // PROBE = false: no snapshot code at all (its address arithmetic cost registers, i.e.
+        // local-memory spills, in the hot instantiation)
+        uint32_t* snaps = PROBE && probe != nullptr ? probe + m0 * 3 * kWords : nullptr;
         auto snap4 = [&](int stage, bool stride) {
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
@@ -615,20 +617,20 @@ __global__ void __launch_bounds__(1024, 1)
             count_row_sort4(x, S, T, k, r, desc_alt, nothing);  // chunk layout out
             __syncthreads();
             warp_transpose(x, slab, r);  // to_column_major
-            if (pass == 0 && snaps)
+            if (PROBE && pass == 0 && snaps)
                 snap4(0, true);  // after_first_convert
             count_row_sort4(x, S, T, k, r, !asc, nothing);
             if constexpr (DMM_SW32_FULLROWS) {
                 chunk_to_stride(x, S, k, r, k);
                 __syncthreads();
                 warp_transpose(x, slab, r);  // to_row_major: chunk layout out
-                if (pass == 0 && snaps)
+                if (PROBE && pass == 0 && snaps)
                     snap4(1, false);  // after_first_pass
             } else {
                 // to_row_major as one exchange (the next counting row sort takes any
                 // arrangement of its row): stride layout, odd warps' words reversed
                 row_exchange(x, S, k, r);
-                if (pass == 0 && snaps) {  // after_first_pass
+                if (PROBE && pass == 0 && snaps) {  // after_first_pass
 #pragma unroll
                     for (int b = 0; b < 4; ++b) {
                         if (m0 + b >= count)
@@ -642,7 +644,7 @@ __global__ void __launch_bounds__(1024, 1)
             }
         }
         count_row_sort4(x, S, T, k, r, !asc, nothing);
-        if (snaps)
+        if (PROBE && snaps)
             snap4(2, false);  // done
         uint32_t mism = 0;
         if (part) {
@@ -750,10 +752,12 @@ dmm_status launch_sw32_labels(const GeneralArgs& a) {
     // warp's 16-byte accesses to 32 rows 4 KB apart cost 32 L1/L2 requests per instruction,
     // where the bulk copy streams each machine as 4 x 32 KB (profiles/r02/pipeline_ab.txt)
     static const bool direct = getenv("DMM_SW32_DIRECT") && getenv("DMM_SW32_DIRECT")[0] == '1';
-    auto kern = direct ? dmmdev::sw32::k_short_wide32_labels<MODE, true> : dmmdev::sw32::k_short_wide32_labels<MODE, false>;
+    auto kern = direct ? dmmdev::sw32::k_short_wide32_labels<MODE, true>
+                       : a.probe ? dmmdev::sw32::k_short_wide32_labels<MODE, false, true>
+                                 : dmmdev::sw32::k_short_wide32_labels<MODE, false, false>;
     constexpr size_t smem = size_t(dmmdev::sw32::kStage + dmmdev::sw32::kTab4 + 8) * 4;
-    static std::atomic<uint64_t> configured{0};
-    if (dmm_status e = configure_kernel(kern, smem, configured); e != DMM_OK)
+    static std::atomic<uint64_t> configured[3];  // per instantiation (static storage: zeroed)
+    if (dmm_status e = configure_kernel(kern, smem, configured[direct ? 0 : a.probe ? 1 : 2]); e != DMM_OK)
         return e;
     if (a.count == 0)
         return DMM_OK;
