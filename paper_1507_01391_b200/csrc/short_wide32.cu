@@ -376,7 +376,7 @@ template <bool COUNT, int MODE>
 __global__ void __launch_bounds__(1024, 1)
     k_short_wide32(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count, uint64_t domain,
                    int ascending, dmm_general_stats* __restrict__ stats, uint8_t* __restrict__ status,
-                   uint32_t* __restrict__ probe) {
+                   uint32_t* __restrict__ probe, int pf) {
     extern __shared__ __align__(128) uint32_t smem[];
     uint32_t* S = smem;
     uint32_t* E = smem + kStage;
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(1024, 1)
     uint32_t parity = 0;
     for (uint64_t inst = blockIdx.x; inst < count; inst += gridDim.x) {
         const uint64_t nxt = inst + gridDim.x;
-        if (tid == 0 && nxt < count)
+        if (pf && tid == 0 && nxt < count)  // DMM_SW32_SORT_PF (default 1)
             prefetch_l2(in + nxt * kWords, kBytes);
         // the next machine's load into S, once this machine no longer reads S
         auto load_next = [&]() {
@@ -741,8 +741,9 @@ dmm_status launch_sw32(const GeneralArgs& a) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t grid = std::min<uint64_t>(a.count, uint64_t(sms));
+    static const int pf = getenv("DMM_SW32_SORT_PF") ? atoi(getenv("DMM_SW32_SORT_PF")) : 1;
     kern<<<unsigned(grid), 1024, dmmdev::sw32::kSmemBytes, a.stream>>>(a.in, a.out, a.count, a.domain, a.ascending,
-                                                                       a.stats, a.status, a.probe);
+                                                                       a.stats, a.status, a.probe, pf);
     return check_launch("k_short_wide32");
 }
 template <int MODE>
