@@ -440,7 +440,7 @@ __device__ __forceinline__ bool finish_width(uint32_t width, const uint32_t* pk,
     return false;
 }
 
-template <int M, int R>
+template <int M, int R, bool METER = false>
 __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DMM_PERM_TALL_MINB : R == kWarp ? DMM_PERM_MINB32 : 1)) k_permute(
     const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t count, const uint64_t* __restrict__ seeds,
     const uint64_t* __restrict__ states, PermArgs a, dmm_permute_report* __restrict__ reps, uint64_t* __restrict__ hist,
@@ -474,8 +474,10 @@ __global__ void __launch_bounds__(perm_machines_per_cta<R>() * R, (R >= 128 ? DM
     if (k >= count)
         return;
 
-    uint32_t* meter = a.meter ? a.meter + k * kMeterWords : nullptr;
-    uint32_t* sort_in = a.meter ? a.sort_in + k * (uint64_t)W * M : nullptr;
+    // METER = false (the hot instantiation): the step-meter code is compiled out, which keeps
+    // its live ranges out of the register allocation
+    uint32_t* meter = METER && a.meter ? a.meter + k * kMeterWords : nullptr;
+    uint32_t* sort_in = METER && a.meter ? a.sort_in + k * (uint64_t)W * M : nullptr;
     uint64_t pre = 0;  // metered steps outside the finish's sort (machine-uniform)
     constexpr uint32_t kLogW = (uint32_t)ilog2_ceil_c(W);
     if (meter && row < kMeterWords)
@@ -851,12 +853,12 @@ dmm_status launch_permute(const uint32_t* in, uint32_t* out, uint64_t count, con
                           const uint64_t* states, const dmmdev::PermArgs& a, dmm_permute_report* reps, uint64_t* hist,
                           uint32_t* shifts, uint8_t* status, cudaStream_t s) {
     constexpr int kMach = dmmdev::perm_machines_per_cta<R>();
-    auto kern = dmmdev::k_permute<M, R>;
+    auto kern = a.meter ? dmmdev::k_permute<M, R, true> : dmmdev::k_permute<M, R, false>;
     // DMM_PERM_PAD_KB (occupancy sensitivity A/B): extra dynamic shared memory per CTA
     static const size_t pad = getenv("DMM_PERM_PAD_KB") ? size_t(atoi(getenv("DMM_PERM_PAD_KB"))) * 1024 : 0;
     const size_t smem = size_t(kMach) * dmmdev::perm_machine_words<M, R>() * sizeof(uint32_t) + pad;
-    static std::atomic<uint64_t> configured{0};  // devices configured, per instantiation
-    if (dmm_status e = configure_kernel(kern, smem, configured); e != DMM_OK)
+    static std::atomic<uint64_t> configured[2];  // devices configured, per instantiation (static: zeroed)
+    if (dmm_status e = configure_kernel(kern, smem, configured[a.meter ? 1 : 0]); e != DMM_OK)
         return e;
     const uint64_t blocks = (count + kMach - 1) / kMach;
     if (blocks > 0x7FFFFFFFull)
